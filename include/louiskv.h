@@ -1,0 +1,181 @@
+/*
+ * louiskv.h — C ABI of the B200-native LouisKV KV-retrieval hot path.
+ *
+ * Method: LouisKV (arXiv 2510.11292). Citations: P:n = PAPER.md line n.
+ *   cluster_prompt  = kvm.store_cache(K, V, 'prefill')   Alg. 1, §4.2
+ *   should_retrieve = is_new_segment / r_t vs tau        Alg. 1, §4.1
+ *   retrieve        = kvm.Retrieve(q_t, B)               Alg. 1, App. B
+ *   append_output   = kvm.store_cache(k_t, v_t,'decode') Alg. 1, §4.2
+ *   sparse_attn     = o_t over [KV_critical : KV_local]  Alg. 1, §3.1
+ *
+ * Conventions (all entry points):
+ *  - Pointers named d_* or documented "device" are CUDA device pointers; "host"
+ *    pointers are ordinary host memory. The library never takes ownership of
+ *    caller memory; device inputs are borrowed for the stream-ordered duration
+ *    of the call (the library copies what it keeps).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Hot calls only ENQUEUE work; none of should_retrieve / retrieve /
+ *    append_output / sparse_attn synchronises with the host, so a whole decode
+ *    step is CUDA-graph capturable.
+ *  - Layout: head_dim d must be 128. K/V/q/out elements are bf16 (uint16 bits),
+ *    d contiguous. Strides are in ELEMENTS.
+ *  - Errors: argument/state errors return synchronously and enqueue nothing.
+ *    An asynchronous CUDA fault surfaces as LOUISKV_ERR_CUDA on a later call
+ *    and is sticky: the context must be destroyed. louiskv_last_error() gives
+ *    a message. Degenerate inputs are not errors: P <= S gives zero prompt
+ *    units, B = 0 gives an empty selection, a zero query has cosine 0.
+ *  - There is no CPU fallback: every computation runs in sm_100a kernels.
+ *  - A context is single-owner and used from one stream at a time.
+ */
+#ifndef LOUISKV_H_
+#define LOUISKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct louiskv_ctx louiskv_ctx; /* opaque, library-owned */
+
+typedef enum {
+  LOUISKV_OK = 0,
+  LOUISKV_ERR_INVALID_ARG = 1,
+  LOUISKV_ERR_STATE = 2,
+  LOUISKV_ERR_CAPACITY = 3,
+  LOUISKV_ERR_OOM_DEVICE = 4,
+  LOUISKV_ERR_OOM_HOST = 5,
+  LOUISKV_ERR_CUDA = 6,
+  LOUISKV_ERR_NOT_IMPLEMENTED = 7
+} louiskv_status;
+
+enum { LOUISKV_TRIG_PREV_STEP = 0, LOUISKV_TRIG_LAST_RETRIEVAL = 1 };
+enum { LOUISKV_BOUNDARY_PER_LAYER = 0, LOUISKV_BOUNDARY_SHARED = 1 };
+enum { LOUISKV_FETCH_ZERO_COPY = 0 };
+enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
+
+typedef struct {
+  int32_t num_layers, num_q_heads, num_kv_heads, head_dim; /* head_dim must be 128 */
+  int32_t kv_head_begin, kv_head_count;                    /* KV-head shard owned by this ctx */
+  int32_t max_batch;
+  int64_t max_prompt_len, max_output_len;                  /* fix every capacity at create */
+  int32_t budget_tokens;     /* B: retrieved tokens per (b, layer, kv-head) */
+  int32_t sink_tokens;       /* S */
+  int32_t window_tokens;     /* W: local-buffer tokens */
+  double tau;                /* boundary threshold */
+  int32_t avg_cluster_size;  /* c: k = ceil((P-S)/c) clusters */
+  int32_t kmeans_iters;      /* Lloyd iterations (fixed count, no early exit) */
+  int32_t kmeans_impl;       /* LOUISKV_KMEANS_TC (tcgen05) | LOUISKV_KMEANS_SIMT */
+  uint64_t full_cache_layers; /* bitmask of layers that keep the full cache (0b11) */
+  int32_t trigger_ref;       /* LOUISKV_TRIG_PREV_STEP | _LAST_RETRIEVAL */
+  int32_t boundary_mode;     /* LOUISKV_BOUNDARY_PER_LAYER | _SHARED */
+  int32_t shared_layer;      /* designated layer for SHARED mode */
+  int32_t max_open_segment;  /* force-seal bound on the open segment (0 -> window_tokens) */
+  int32_t fetch_mode;        /* LOUISKV_FETCH_ZERO_COPY */
+  int32_t device;            /* CUDA device ordinal */
+} louiskv_config;
+
+typedef struct {
+  uint64_t retrievals;        /* flagged (b, layer) retrieve events */
+  uint64_t units_scored;      /* units scored over all flagged (b, layer, kv-head) */
+  uint64_t units_selected;
+  uint64_t units_reused;      /* selected units already resident (D2D copy) */
+  uint64_t units_fetched;     /* selected units read from the host pool */
+  uint64_t bytes_h2d;         /* host-pool bytes read by the gather */
+  uint64_t bytes_d2h;         /* bytes written to the host pool (prompt offload + evictions) */
+  uint64_t segments_evicted;
+} louiskv_stats;
+
+/* Allocates every device buffer and the pinned, device-mapped host pool.
+ * Errors: INVALID_ARG (bad geometry / head_dim != 128 / shard out of range),
+ * OOM_DEVICE, OOM_HOST, CUDA. *out is NULL on failure. */
+louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out);
+/* Synchronises the device, frees everything. NULL is a no-op. */
+void louiskv_destroy(louiskv_ctx* ctx);
+
+/* kvm.store_cache(K, V, 'prefill') for one layer.
+ * k, v: device bf16, element (b, t, h, e) at base + b*stride_b + t*stride_t + h*stride_h + e,
+ *   h in [0, kv_head_count) (the owned heads), t in [0, prompt_len).
+ * Retrieval layer: per (b, h) k-means of keys [S, P) into k = ceil((P-S)/c) clusters
+ *   (kmeans_iters Lloyd iterations, strided init, empty-cluster repair), centroids kept on
+ *   the device (fp32 + bf16), KV rows offloaded cluster-major to the host pool, sinks kept.
+ * Full-cache layer: K, V copied to the device cache.
+ * Must be called once per layer before the first decode step; resets that layer's decode
+ * state. Errors: INVALID_ARG (layer, batch > max_batch, prompt_len > max_prompt_len,
+ * batch differing from an earlier call), STATE. */
+louiskv_status louiskv_cluster_prompt(louiskv_ctx* ctx, int32_t layer, const void* k, const void* v,
+                                      int64_t stride_b, int64_t stride_t, int64_t stride_h,
+                                      int32_t batch, int64_t prompt_len, void* stream);
+
+/* Same as cluster_prompt but with the clustering supplied by the caller (external or
+ * reference clustering): h_assign host int32 [batch][kv_head_count][P-S] cluster ids in
+ * [0, k); h_centroids host fp32 [batch][kv_head_count][k][d]; every cluster non-empty.
+ * Synchronous (copies host arrays). Errors: INVALID_ARG, STATE. */
+louiskv_status louiskv_set_prompt_units(louiskv_ctx* ctx, int32_t layer, const void* k, const void* v,
+                                        int64_t stride_b, int64_t stride_t, int64_t stride_h,
+                                        int32_t batch, int64_t prompt_len, int32_t n_clusters,
+                                        const int32_t* h_assign, const float* h_centroids, void* stream);
+
+/* Decode step t (1-based, advanced by this call) of one layer: r_t and the retrieval flag
+ * (P:101-106). q_all: device bf16 [batch][num_q_heads][d] (ALL query heads),
+ * sequence b at q_all + b*stride_b. d_flag_out (uint8 [batch]) and d_r_out (double [batch])
+ * are optional DEVICE outputs. Per-step call order per layer:
+ * should_retrieve -> retrieve -> append_output -> sparse_attn. Full-cache layers write flag 0.
+ * Errors: INVALID_ARG, STATE (order broken, cluster_prompt missing, SHARED designated layer
+ * not yet called this step, more than max_output_len steps). */
+louiskv_status louiskv_should_retrieve(louiskv_ctx* ctx, int32_t layer, const void* q_all, int64_t stride_b,
+                                       uint8_t* d_flag_out, double* d_r_out, void* stream);
+
+/* kvm.Retrieve(q_t, B) for every flagged sequence: group-consistent scores
+ * A = mean_j softmax(q^j C^T / sqrt(d)) over all host-resident units of each owned KV head
+ * (App. B), greedy budgeted selection in (A desc, unit id asc) order, and the gather of
+ * the selected units' KV rows (new units from the pinned host pool over the host link, kept
+ * units device-to-device) into the working set. Unflagged sequences are untouched.
+ * q_own: device bf16 [batch][g*kv_head_count][d] (owned query heads). No-op on full-cache
+ * layers. Errors: INVALID_ARG, STATE. */
+louiskv_status louiskv_retrieve(louiskv_ctx* ctx, int32_t layer, const void* q_own, int64_t stride_b, void* stream);
+
+/* kvm.store_cache(k_t, v_t, 'decode'): seal the open segment at a boundary
+ * (or at max_open_segment), append (k_t, v_t), evict the oldest sealed segments while the
+ * local buffer holds more than W tokens (centroid = mean of its keys, rows offloaded to the
+ * host pool, appended as a new unit). k_t, v_t: device bf16 [batch][kv_head_count][d].
+ * Errors: INVALID_ARG, STATE, CAPACITY (pool full; sticky). */
+louiskv_status louiskv_append_output(louiskv_ctx* ctx, int32_t layer, const void* k_t, const void* v_t,
+                                     int64_t stride_b, void* stream);
+
+/* o = softmax(q K_I^T / sqrt(d)) V_I for every owned query head over
+ * I = sinks ∪ working set ∪ local buffer (incl. this step's k_t); full-cache layers attend
+ * to all P+t rows. q_own as in retrieve. out: device bf16
+ * [batch][g*kv_head_count][d] contiguous; out_f32 optional device fp32, same shape.
+ * Errors: INVALID_ARG, STATE. */
+louiskv_status louiskv_sparse_attn(louiskv_ctx* ctx, int32_t layer, const void* q_own, int64_t stride_b,
+                                   void* out, float* out_f32, void* stream);
+
+/* ---- introspection (synchronous: they synchronise the device) ---- */
+/* Current working-set unit ids of (layer, b, owned head h), ascending. */
+louiskv_status louiskv_get_selection(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,
+                                     int32_t* ids, int32_t cap, int32_t* n);
+/* Unit table of (layer, b, h): up to cap units. Any output pointer may be NULL.
+ * centroids_f32 host [cap][d]; sizes host [cap]; first_pos host [cap] (lowest member
+ * position); n_units receives the number of units (prompt clusters first, then evicted
+ * segments in eviction order). */
+louiskv_status louiskv_get_units(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h, int32_t cap,
+                                 float* centroids_f32, int32_t* sizes, int32_t* first_pos, int32_t* n_units);
+/* Token positions of the host-pool rows of (layer, b, h) in pool order (unit after unit,
+ * members ascending), up to cap. */
+louiskv_status louiskv_get_unit_positions(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,
+                                          int32_t* positions, int64_t cap, int64_t* n);
+/* Copies the current working set (K rows then V rows, bf16 bits) of (layer, b, h) to host
+ * arrays [cap][d]; *n_rows receives the row count. */
+louiskv_status louiskv_get_working_set(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,
+                                       uint16_t* k_rows, uint16_t* v_rows, int32_t cap, int32_t* n_rows);
+louiskv_status louiskv_get_stats(louiskv_ctx* ctx, louiskv_stats* out);
+const char* louiskv_last_error(const louiskv_ctx* ctx);
+/* Library build string (arch, version). */
+const char* louiskv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOUISKV_H_ */

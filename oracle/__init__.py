@@ -19,6 +19,7 @@ from .core import (  # noqa: F401
     select_greedy,
     kmeans,
     segment_centroid,
+    centroids_of,
     attention_f64,
     build_oracle,
 )

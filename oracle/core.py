@@ -59,6 +59,8 @@ def lib():
         L.lko_kmeans.restype = ctypes.c_int
         L.lko_kmeans.argtypes = [_f32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  _i32p, _f32p, _i32p, _f64p, _f32p]
+        L.lko_centroids_of.restype = ctypes.c_int
+        L.lko_centroids_of.argtypes = [_f32p, _i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _f32p]
         L.lko_segment_centroid.restype = None
         L.lko_segment_centroid.argtypes = [_f32p, ctypes.c_int, ctypes.c_int, _f32p]
         L.lko_attention_f64.restype = ctypes.c_int
@@ -146,6 +148,18 @@ def kmeans(X, k: int, iters: int, mode: int = 1):
     if rc != 0:
         raise ValueError(f"kmeans: invalid arguments (rc={rc})")
     return assign, C, counts, J[:iters], dmin
+
+
+def centroids_of(X, assign, k: int) -> np.ndarray:
+    """fp32 centroids (fp64 means) of a given clustering; raises on an empty cluster."""
+    X = _f32(X)
+    assign = np.ascontiguousarray(assign, dtype=np.int32)
+    N, d = X.shape
+    C = np.zeros((k, d), np.float32)
+    rc = lib().lko_centroids_of(X, assign, N, d, k, C)
+    if rc != 0:
+        raise ValueError("centroids_of: empty cluster")
+    return C
 
 
 def segment_centroid(keys) -> np.ndarray:

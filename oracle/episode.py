@@ -80,8 +80,11 @@ class OracleEpisode:
         self.row_bytes = 2 * 2 * self.d  # K+V bf16 per token per head
 
     # --------------------------------------------------------------- prefill
-    def cluster_prompt(self, layer: int, K: np.ndarray, V: np.ndarray):
-        """store_cache(K, V, 'prefill') (P:258-265). K, V: [b, P, Hkv_owned, d] fp32."""
+    def cluster_prompt(self, layer: int, K: np.ndarray, V: np.ndarray, assign: Optional[np.ndarray] = None):
+        """store_cache(K, V, 'prefill') (P:258-265). K, V: [b, P, Hkv_owned, d] fp32.
+
+        ``assign`` ([b, Hkv_owned, P-S] cluster ids) replaces the k-means step with a given
+        clustering (centroids are still the means of the members)."""
         K = np.asarray(K, np.float32)
         V = np.asarray(V, np.float32)
         b, P, H, d = K.shape
@@ -101,11 +104,15 @@ class OracleEpisode:
                     k = self.cfg.n_clusters if self.cfg.clusters_override else -(-N // self.c)
                     k = min(k, N)
                     X = K[bb, S:, hh]
-                    assign, C, counts, J, _ = core.kmeans(X, k, self.iters, self.kmeans_mode)
-                    self.kmeans_J[key] = J
+                    if assign is None:
+                        a_i, C, counts, J, _ = core.kmeans(X, k, self.iters, self.kmeans_mode)
+                        self.kmeans_J[key] = J
+                    else:
+                        a_i = np.asarray(assign[bb, hh], np.int32)
+                        C = core.centroids_of(X, a_i, k)
                     Cb = core.bf16_round(C)
                     for j in range(k):
-                        mem = np.nonzero(assign == j)[0]
+                        mem = np.nonzero(a_i == j)[0]
                         inst.units.append(Unit(j, mem + S, X[mem].copy(), V[bb, S + mem, hh].copy(),
                                                C[j].copy(), Cb[j].copy()))
                     self.stats["bytes_d2h"] += N * self.row_bytes

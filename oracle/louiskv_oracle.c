@@ -376,3 +376,23 @@ void lko_bf16_round_n(const float* x, float* y, long long n) {
 void lko_exp_r3_n(const float* x, float* y, long long n) {
   for (long long i = 0; i < n; ++i) y[i] = lko_exp_r3(x[i]);
 }
+
+/* Centroids of a given clustering: C_j = mean of {x_i : a_i = j} in fp64, stored fp32
+ * ("calculates the centroid C_i for each cluster by averaging all its key vectors";
+ * the same update step as lko_kmeans (iii)). Returns -1 if a cluster is empty. */
+int lko_centroids_of(const float* X, const int* assign, int N, int d, int k, float* C) {
+  double* sum = (double*)calloc((size_t)k * d, sizeof(double));
+  int* cnt = (int*)calloc((size_t)k, sizeof(int));
+  if (!sum || !cnt) { free(sum); free(cnt); return -2; }
+  for (int i = 0; i < N; ++i) {
+    cnt[assign[i]]++;
+    for (int e = 0; e < d; ++e) sum[(size_t)assign[i] * d + e] += (double)X[(size_t)i * d + e];
+  }
+  int rc = 0;
+  for (int j = 0; j < k; ++j) {
+    if (cnt[j] == 0) { rc = -1; continue; }
+    for (int e = 0; e < d; ++e) C[(size_t)j * d + e] = (float)(sum[(size_t)j * d + e] / (double)cnt[j]);
+  }
+  free(sum); free(cnt);
+  return rc;
+}

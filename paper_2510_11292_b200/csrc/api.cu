@@ -1,0 +1,625 @@
+// C ABI of the LouisKV B200 library: context, capacities, state machine, kernel sequencing.
+// See include/louiskv.h for the contract of every entry point (paper citations there).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lkv_internal.cuh"
+
+using namespace lkv;
+
+struct louiskv_ctx {
+  louiskv_config cfg{};
+  int L = 0, Hq = 0, Hkv = 0, h0 = 0, hn = 0, g = 0, Bmax = 0, S = 0, W = 0, Bud = 0, c = 0, iters = 0;
+  int max_open = 0, ring_cap = 0, kmax = 0, Umax = 0, nchunk_max = 0;
+  int64_t Pmax = 0, Mmax = 0, Nmax = 0, pool_rows_cap = 0, full_cap = 0;
+  int n_r = 0, n_f = 0;
+  std::vector<int> ridx, fidx;
+  int batch = 0;
+  std::vector<int64_t> P;
+  std::vector<int> t, stage;
+  int64_t n_inst = 0;  // n_r * Bmax * hn
+  int inst_per_layer = 0;
+  // device state
+  InstState* d_inst = nullptr;
+  bf16* d_sinks = nullptr;
+  bf16* d_ws = nullptr;
+  int64_t ws_buf_stride = 0, ws_inst_stride = 0;
+  bf16* d_ring = nullptr;
+  int2* d_fifo = nullptr;
+  float* d_cent = nullptr;
+  bf16* d_centb = nullptr;
+  int32_t* d_usize = nullptr;
+  int64_t* d_uoff = nullptr;
+  int32_t* d_ufirst = nullptr;
+  uint8_t* d_sel = nullptr;
+  int32_t* d_seloff = nullptr;
+  int32_t* d_pool_pos = nullptr;
+  uint8_t* d_flag = nullptr;
+  double* d_r = nullptr;
+  bf16* d_qref = nullptr;
+  bf16* d_full = nullptr;
+  uint8_t* h_pool = nullptr;
+  uint8_t* d_pool = nullptr;
+  int64_t pool_inst_bytes = 0;
+  // scratch
+  float* d_se = nullptr;
+  unsigned long long* d_skey = nullptr;
+  GatherJob* d_jobs = nullptr;
+  RowSrc* d_rows = nullptr;
+  float* d_part = nullptr;
+  int* d_counters = nullptr;
+  int max_splits = 64;
+  float* d_km_half = nullptr;
+  int32_t* d_km_assign = nullptr;
+  float* d_km_dmin = nullptr;
+  int32_t* d_km_cc = nullptr;
+  int32_t* d_km_off = nullptr;
+  int32_t* d_km_cnt = nullptr;
+  int32_t* d_km_perm = nullptr;
+  int32_t* d_km_flags = nullptr;
+  StatsDev* d_stats = nullptr;
+  std::vector<void*> allocs;
+  std::string err;
+  bool sticky = false;
+};
+
+namespace {
+
+louiskv_status fail(louiskv_ctx* c, louiskv_status s, const std::string& m) {
+  if (c) {
+    c->err = m;
+    if (s == LOUISKV_ERR_CUDA || s == LOUISKV_ERR_CAPACITY) c->sticky = true;
+  }
+  return s;
+}
+
+louiskv_status cuda_fail(louiskv_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, LOUISKV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+bool dalloc(louiskv_ctx* c, T** p, size_t n) {
+  if (n == 0) n = 1;
+  void* v = nullptr;
+  if (cudaMalloc(&v, n * sizeof(T)) != cudaSuccess) return false;
+  cudaMemset(v, 0, n * sizeof(T));
+  c->allocs.push_back(v);
+  *p = reinterpret_cast<T*>(v);
+  return true;
+}
+
+#define LKV_CHECK_CTX(c)                                                        \
+  do {                                                                          \
+    if (!(c)) return LOUISKV_ERR_INVALID_ARG;                                   \
+    if ((c)->sticky) return fail((c), LOUISKV_ERR_CUDA, (c)->err);               \
+    if (cudaSetDevice((c)->cfg.device) != cudaSuccess)                           \
+      return fail((c), LOUISKV_ERR_CUDA, "cudaSetDevice failed");                \
+  } while (0)
+
+#define LKV_LAUNCH(c, expr, where)                            \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail((c), _e, where);  \
+  } while (0)
+
+bool is_full(const louiskv_ctx* c, int layer) { return (c->cfg.full_cache_layers >> layer) & 1ull; }
+
+int64_t inst_base(const louiskv_ctx* c, int layer) { return (int64_t)c->ridx[layer] * c->inst_per_layer; }
+
+}  // namespace
+
+extern "C" {
+
+const char* louiskv_version(void) { return "louiskv-b200 0.1 (sm_100a, tcgen05/TMEM k-means, zero-copy gather)"; }
+
+const char* louiskv_last_error(const louiskv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void louiskv_destroy(louiskv_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->h_pool) cudaFreeHost(ctx->h_pool);
+  delete ctx;
+}
+
+louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
+  if (!cfg || !out) return LOUISKV_ERR_INVALID_ARG;
+  *out = nullptr;
+  const louiskv_config& k = *cfg;
+  if (k.head_dim != D || k.num_layers <= 0 || k.num_layers > 64 || k.num_q_heads <= 0 || k.num_kv_heads <= 0 ||
+      k.num_q_heads % k.num_kv_heads != 0 || k.kv_head_begin < 0 || k.kv_head_count <= 0 ||
+      k.kv_head_begin + k.kv_head_count > k.num_kv_heads || k.max_batch <= 0 || k.max_prompt_len <= 0 ||
+      k.max_output_len <= 0 || k.budget_tokens < 0 || k.sink_tokens < 0 || k.window_tokens < 1 ||
+      k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) ||
+      (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
+    return LOUISKV_ERR_INVALID_ARG;
+  const int g = k.num_q_heads / k.num_kv_heads;
+  if (g != 1 && g != 2 && g != 4 && g != 8) return LOUISKV_ERR_INVALID_ARG;
+  if (k.max_prompt_len > (1ll << 30) || k.max_output_len > (1ll << 30)) return LOUISKV_ERR_INVALID_ARG;
+  if (cudaSetDevice(k.device) != cudaSuccess) return LOUISKV_ERR_CUDA;
+
+  louiskv_ctx* c = new louiskv_ctx();
+  c->cfg = k;
+  c->L = k.num_layers;
+  c->Hq = k.num_q_heads;
+  c->Hkv = k.num_kv_heads;
+  c->h0 = k.kv_head_begin;
+  c->hn = k.kv_head_count;
+  c->g = g;
+  c->Bmax = k.max_batch;
+  c->S = k.sink_tokens;
+  c->W = k.window_tokens;
+  c->Bud = k.budget_tokens;
+  c->c = k.avg_cluster_size;
+  c->iters = k.kmeans_iters;
+  c->max_open = k.max_open_segment > 0 ? k.max_open_segment : k.window_tokens;
+  c->ring_cap = std::max(c->W, c->max_open) + 2;
+  c->Pmax = k.max_prompt_len;
+  c->Mmax = k.max_output_len;
+  c->Nmax = std::max<int64_t>(0, c->Pmax - c->S);
+  c->kmax = (int)((c->Nmax + c->c - 1) / c->c);
+  c->Umax = (int)std::min<int64_t>((int64_t)c->kmax + c->Mmax, 1ll << 16);
+  if ((int64_t)c->kmax + c->Mmax > (1ll << 16)) {  // 16-bit unit ids in the selection key
+    delete c;
+    return LOUISKV_ERR_INVALID_ARG;
+  }
+  c->nchunk_max = (int)((c->Nmax + 1023) / 1024);
+  c->pool_rows_cap = c->Nmax + c->Mmax;
+  c->full_cap = c->Pmax + c->Mmax;
+  c->ridx.assign(c->L, -1);
+  c->fidx.assign(c->L, -1);
+  for (int l = 0; l < c->L; ++l) {
+    if (is_full(c, l))
+      c->fidx[l] = c->n_f++;
+    else
+      c->ridx[l] = c->n_r++;
+  }
+  c->P.assign(c->L, -1);
+  c->t.assign(c->L, 0);
+  c->stage.assign(c->L, 0);
+  c->inst_per_layer = c->Bmax * c->hn;
+  c->n_inst = (int64_t)c->n_r * c->inst_per_layer;
+  const int64_t ni = c->n_inst, nl = c->inst_per_layer;
+
+  bool ok = true;
+  ok = ok && dalloc(c, &c->d_inst, ni);
+  ok = ok && dalloc(c, &c->d_sinks, (size_t)ni * 2 * std::max(c->S, 1) * D);
+  c->ws_inst_stride = (int64_t)2 * std::max(c->Bud, 1) * D;
+  c->ws_buf_stride = ni * c->ws_inst_stride;
+  ok = ok && dalloc(c, &c->d_ws, (size_t)2 * c->ws_buf_stride);
+  ok = ok && dalloc(c, &c->d_ring, (size_t)ni * 2 * c->ring_cap * D);
+  ok = ok && dalloc(c, &c->d_fifo, (size_t)ni * c->ring_cap);
+  ok = ok && dalloc(c, &c->d_cent, (size_t)ni * c->Umax * D);
+  ok = ok && dalloc(c, &c->d_centb, (size_t)ni * c->Umax * D);
+  ok = ok && dalloc(c, &c->d_usize, (size_t)ni * c->Umax);
+  ok = ok && dalloc(c, &c->d_uoff, (size_t)ni * c->Umax);
+  ok = ok && dalloc(c, &c->d_ufirst, (size_t)ni * c->Umax);
+  ok = ok && dalloc(c, &c->d_sel, (size_t)ni * c->Umax);
+  ok = ok && dalloc(c, &c->d_seloff, (size_t)ni * c->Umax);
+  ok = ok && dalloc(c, &c->d_pool_pos, (size_t)ni * c->pool_rows_cap);
+  ok = ok && dalloc(c, &c->d_flag, (size_t)c->L * c->Bmax);
+  ok = ok && dalloc(c, &c->d_r, (size_t)c->L * c->Bmax);
+  ok = ok && dalloc(c, &c->d_qref, (size_t)c->L * c->Bmax * c->Hq * D);
+  ok = ok && dalloc(c, &c->d_full, (size_t)c->n_f * nl * 2 * c->full_cap * D);
+  ok = ok && dalloc(c, &c->d_se, (size_t)nl * g * c->Umax);
+  ok = ok && dalloc(c, &c->d_skey, (size_t)nl * c->Umax);
+  ok = ok && dalloc(c, &c->d_jobs, (size_t)nl);
+  ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
+  ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
+  ok = ok && dalloc(c, &c->d_counters, (size_t)nl);
+  ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * std::max(c->kmax, 1));
+  ok = ok && dalloc(c, &c->d_km_assign, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
+  ok = ok && dalloc(c, &c->d_km_dmin, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
+  ok = ok && dalloc(c, &c->d_km_cc, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
+  ok = ok && dalloc(c, &c->d_km_off, (size_t)nl * (c->kmax + 1));
+  ok = ok && dalloc(c, &c->d_km_cnt, (size_t)nl * std::max(c->kmax, 1));
+  ok = ok && dalloc(c, &c->d_km_perm, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
+  ok = ok && dalloc(c, &c->d_km_flags, (size_t)nl);
+  ok = ok && dalloc(c, &c->d_stats, 1);
+  if (!ok) {
+    louiskv_destroy(c);
+    return LOUISKV_ERR_OOM_DEVICE;
+  }
+  c->pool_inst_bytes = c->pool_rows_cap * POOL_ROW_BYTES;
+  const size_t pool_bytes = (size_t)std::max<int64_t>(ni, 1) * c->pool_inst_bytes;
+  if (pool_bytes > 0) {
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, pool_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      louiskv_destroy(c);
+      return LOUISKV_ERR_OOM_HOST;
+    }
+    c->h_pool = reinterpret_cast<uint8_t*>(hp);
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, hp, 0) != cudaSuccess) {
+      louiskv_destroy(c);
+      return LOUISKV_ERR_CUDA;
+    }
+    c->d_pool = reinterpret_cast<uint8_t*>(dp);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    louiskv_destroy(c);
+    return LOUISKV_ERR_CUDA;
+  }
+  *out = c;
+  return LOUISKV_OK;
+}
+
+static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k, const void* v, int64_t sb,
+                                    int64_t st_, int64_t sh, int32_t batch, int64_t P, int32_t n_clusters,
+                                    const int32_t* h_assign, const float* h_cent, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !k || !v || batch <= 0 || batch > c->Bmax || P < 0 || P > c->Pmax)
+    return fail(c, LOUISKV_ERR_INVALID_ARG, "cluster_prompt: bad layer/pointer/batch/prompt_len");
+  if (c->batch != 0 && batch != c->batch)
+    return fail(c, LOUISKV_ERR_INVALID_ARG, "cluster_prompt: batch differs from an earlier layer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  c->batch = batch;
+  c->P[layer] = P;
+  c->t[layer] = 0;
+  c->stage[layer] = 0;
+  LKV_LAUNCH(c, cudaMemsetAsync(c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, 0, sizeof(bf16) * c->Bmax * c->Hq * D, st),
+             "memset q_ref");
+  LKV_LAUNCH(c, cudaMemsetAsync(c->d_flag + (size_t)layer * c->Bmax, 0, c->Bmax, st), "memset flag");
+  if (is_full(c, layer)) {
+    if (h_assign) return fail(c, LOUISKV_ERR_INVALID_ARG, "set_prompt_units on a full-cache layer");
+    LKV_LAUNCH(c,
+               launch_full_prompt(reinterpret_cast<const bf16*>(k), reinterpret_cast<const bf16*>(v), sb, st_, sh, batch,
+                                  c->hn, P, c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D,
+                                  c->full_cap, st),
+               "full prompt");
+    return LOUISKV_OK;
+  }
+  const int64_t N = std::max<int64_t>(0, P - c->S);
+  const int kc = N > 0 ? (int)((N + c->c - 1) / c->c) : 0;
+  const int64_t ib = inst_base(c, layer);
+  KmArgs a{};
+  a.k = reinterpret_cast<const bf16*>(k);
+  a.v = reinterpret_cast<const bf16*>(v);
+  a.sb = sb;
+  a.st = st_;
+  a.sh = sh;
+  a.batch = batch;
+  a.hn = c->hn;
+  a.S = (int)std::min<int64_t>(c->S, P);
+  a.N = (int)N;
+  a.kc = kc;
+  a.iters = c->iters;
+  a.impl = c->cfg.kmeans_impl;
+  a.cent = c->d_cent + ib * c->Umax * D;
+  a.centb = c->d_centb + ib * c->Umax * D;
+  a.Umax = c->Umax;
+  a.usize = c->d_usize + ib * c->Umax;
+  a.uoff = c->d_uoff + ib * c->Umax;
+  a.ufirst = c->d_ufirst + ib * c->Umax;
+  a.sel = c->d_sel + ib * c->Umax;
+  a.pool_pos = c->d_pool_pos + ib * c->pool_rows_cap;
+  a.pool_rows_cap = c->pool_rows_cap;
+  a.pool = c->d_pool + ib * c->pool_inst_bytes;
+  a.pool_inst_bytes = c->pool_inst_bytes;
+  a.sinks = c->d_sinks + ib * 2 * std::max(c->S, 1) * D;
+  a.S_cap = c->S;
+  a.inst = c->d_inst + ib;
+  a.half = c->d_km_half;
+  a.assign = c->d_km_assign;
+  a.dmin = c->d_km_dmin;
+  a.cc = c->d_km_cc;
+  a.off = c->d_km_off;
+  a.cnt = c->d_km_cnt;
+  a.perm = c->d_km_perm;
+  a.flags = c->d_km_flags;
+  a.Nmax = std::max<int64_t>(c->Nmax, 1);
+  a.kmax = std::max(c->kmax, 1);
+  a.nchunk_max = std::max(c->nchunk_max, 1);
+  a.stats = c->d_stats;
+  int32_t* d_ea = nullptr;
+  float* d_ec = nullptr;
+  if (h_assign) {
+    if (n_clusters != kc) return fail(c, LOUISKV_ERR_INVALID_ARG, "set_prompt_units: n_clusters != ceil((P-S)/c)");
+    const size_t na = (size_t)batch * c->hn * N, nc = (size_t)batch * c->hn * kc * D;
+    for (size_t i = 0; i < na; ++i)
+      if (h_assign[i] < 0 || h_assign[i] >= kc) return fail(c, LOUISKV_ERR_INVALID_ARG, "set_prompt_units: id out of range");
+    if (cudaMalloc(&d_ea, std::max<size_t>(na, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&d_ec, std::max<size_t>(nc, 1) * 4) != cudaSuccess)
+      return fail(c, LOUISKV_ERR_OOM_DEVICE, "set_prompt_units scratch");
+    cudaMemcpy(d_ea, h_assign, na * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ec, h_cent, nc * 4, cudaMemcpyHostToDevice);
+    a.ext_assign = d_ea;
+    a.ext_cent = d_ec;
+  }
+  cudaError_t e = run_kmeans_prompt(a, st);
+  if (h_assign) {
+    cudaStreamSynchronize(st);
+    cudaFree(d_ea);
+    cudaFree(d_ec);
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "cluster_prompt");
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_cluster_prompt(louiskv_ctx* ctx, int32_t layer, const void* k, const void* v, int64_t stride_b,
+                                      int64_t stride_t, int64_t stride_h, int32_t batch, int64_t prompt_len,
+                                      void* stream) {
+  return prompt_common(ctx, layer, k, v, stride_b, stride_t, stride_h, batch, prompt_len, 0, nullptr, nullptr, stream);
+}
+
+louiskv_status louiskv_set_prompt_units(louiskv_ctx* ctx, int32_t layer, const void* k, const void* v, int64_t stride_b,
+                                        int64_t stride_t, int64_t stride_h, int32_t batch, int64_t prompt_len,
+                                        int32_t n_clusters, const int32_t* h_assign, const float* h_centroids,
+                                        void* stream) {
+  if (!h_assign || !h_centroids) return fail(ctx, LOUISKV_ERR_INVALID_ARG, "set_prompt_units: null host arrays");
+  return prompt_common(ctx, layer, k, v, stride_b, stride_t, stride_h, batch, prompt_len, n_clusters, h_assign,
+                       h_centroids, stream);
+}
+
+louiskv_status louiskv_should_retrieve(louiskv_ctx* c, int32_t layer, const void* q_all, int64_t stride_b,
+                                       uint8_t* d_flag_out, double* d_r_out, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !q_all) return fail(c, LOUISKV_ERR_INVALID_ARG, "should_retrieve: bad args");
+  if (c->P[layer] < 0) return fail(c, LOUISKV_ERR_STATE, "should_retrieve before cluster_prompt");
+  if (c->stage[layer] != 0 && c->stage[layer] != 3)
+    return fail(c, LOUISKV_ERR_STATE, "should_retrieve: previous step incomplete");
+  if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "should_retrieve: max_output_len reached");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int t = c->t[layer] + 1;
+  uint8_t* flag = c->d_flag + (size_t)layer * c->Bmax;
+  double* r = c->d_r + (size_t)layer * c->Bmax;
+  if (is_full(c, layer)) {
+    LKV_LAUNCH(c, launch_copy_flags(nullptr, nullptr, flag, r, d_flag_out, d_r_out, c->batch, st), "flags");
+  } else if (c->cfg.boundary_mode == LOUISKV_BOUNDARY_SHARED && layer != c->cfg.shared_layer) {
+    const int sl = c->cfg.shared_layer;
+    if (c->t[sl] < t) return fail(c, LOUISKV_ERR_STATE, "SHARED: designated layer not yet called this step");
+    LKV_LAUNCH(c,
+               launch_copy_flags(c->d_flag + (size_t)sl * c->Bmax, c->d_r + (size_t)sl * c->Bmax, flag, r, d_flag_out,
+                                 d_r_out, c->batch, st),
+               "flags");
+  } else {
+    LKV_LAUNCH(c,
+               launch_trigger(reinterpret_cast<const bf16*>(q_all), stride_b, c->batch, c->Hq,
+                              c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, flag, r, d_flag_out, d_r_out, t,
+                              c->cfg.tau, c->cfg.trigger_ref, st),
+               "trigger");
+  }
+  c->t[layer] = t;
+  c->stage[layer] = 1;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_retrieve(louiskv_ctx* c, int32_t layer, const void* q_own, int64_t stride_b, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !q_own) return fail(c, LOUISKV_ERR_INVALID_ARG, "retrieve: bad args");
+  if (c->stage[layer] != 1) return fail(c, LOUISKV_ERR_STATE, "retrieve must follow should_retrieve");
+  c->stage[layer] = 2;
+  if (is_full(c, layer)) return LOUISKV_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t ib = inst_base(c, layer);
+  RetrieveArgs a{};
+  a.q_own = reinterpret_cast<const bf16*>(q_own);
+  a.stride_b = stride_b;
+  a.batch = c->batch;
+  a.hn = c->hn;
+  a.g = c->g;
+  a.Umax = c->Umax;
+  a.budget = c->Bud;
+  a.flag = c->d_flag + (size_t)layer * c->Bmax;
+  a.inst = c->d_inst + ib;
+  a.centb = c->d_centb + ib * c->Umax * D;
+  a.usize = c->d_usize + ib * c->Umax;
+  a.uoff = c->d_uoff + ib * c->Umax;
+  a.sel = c->d_sel + ib * c->Umax;
+  a.seloff = c->d_seloff + ib * c->Umax;
+  a.pool = c->d_pool + ib * c->pool_inst_bytes;
+  a.pool_inst_bytes = c->pool_inst_bytes;
+  a.ws = c->d_ws;
+  a.ws_buf_stride = c->ws_buf_stride;
+  a.ws_inst_stride = c->ws_inst_stride;
+  a.inst_global_base = ib;
+  a.scratch_e = c->d_se;
+  a.scratch_key = c->d_skey;
+  a.jobs = c->d_jobs;
+  a.rows = c->d_rows;
+  a.stats = c->d_stats;
+  LKV_LAUNCH(c, launch_score_select(a, st), "score_select");
+  LKV_LAUNCH(c, launch_gather(c->d_jobs, c->d_rows, c->batch * c->hn, std::max(c->Bud, 1), st), "gather");
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* k_t, const void* v_t, int64_t stride_b,
+                                     void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !k_t || !v_t) return fail(c, LOUISKV_ERR_INVALID_ARG, "append_output: bad args");
+  if (c->stage[layer] != 1 && c->stage[layer] != 2)
+    return fail(c, LOUISKV_ERR_STATE, "append_output must follow should_retrieve/retrieve");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int t = c->t[layer];
+  if (is_full(c, layer)) {
+    LKV_LAUNCH(c,
+               launch_full_append(reinterpret_cast<const bf16*>(k_t), reinterpret_cast<const bf16*>(v_t), stride_b,
+                                  c->batch, c->hn,
+                                  c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D,
+                                  c->full_cap, c->P[layer] + t - 1, st),
+               "full append");
+  } else {
+    const int64_t ib = inst_base(c, layer);
+    AppendArgs a{};
+    a.k_t = reinterpret_cast<const bf16*>(k_t);
+    a.v_t = reinterpret_cast<const bf16*>(v_t);
+    a.stride_b = stride_b;
+    a.batch = c->batch;
+    a.hn = c->hn;
+    a.t = t;
+    a.W = c->W;
+    a.max_open = c->max_open;
+    a.ring_cap = c->ring_cap;
+    a.Umax = c->Umax;
+    a.flag = c->d_flag + (size_t)layer * c->Bmax;
+    a.inst = c->d_inst + ib;
+    a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
+    a.fifo = c->d_fifo + ib * c->ring_cap;
+    a.cent = c->d_cent + ib * c->Umax * D;
+    a.centb = c->d_centb + ib * c->Umax * D;
+    a.usize = c->d_usize + ib * c->Umax;
+    a.uoff = c->d_uoff + ib * c->Umax;
+    a.ufirst = c->d_ufirst + ib * c->Umax;
+    a.sel = c->d_sel + ib * c->Umax;
+    a.pool_pos = c->d_pool_pos + ib * c->pool_rows_cap;
+    a.pool_rows_cap = c->pool_rows_cap;
+    a.pool = c->d_pool + ib * c->pool_inst_bytes;
+    a.pool_inst_bytes = c->pool_inst_bytes;
+    a.stats = c->d_stats;
+    LKV_LAUNCH(c, launch_append(a, st), "append");
+  }
+  c->stage[layer] = 3;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_own, int64_t stride_b, void* out,
+                                   float* out_f32, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !q_own || !out) return fail(c, LOUISKV_ERR_INVALID_ARG, "sparse_attn: bad args");
+  if (c->stage[layer] != 3) return fail(c, LOUISKV_ERR_STATE, "sparse_attn must follow append_output");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  AttnArgs a{};
+  a.q_own = reinterpret_cast<const bf16*>(q_own);
+  a.stride_b = stride_b;
+  a.batch = c->batch;
+  a.hn = c->hn;
+  a.g = c->g;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  a.out = reinterpret_cast<bf16*>(out);
+  a.out_f32 = out_f32;
+  a.part = c->d_part;
+  a.counters = c->d_counters;
+  const int n_ctas = c->batch * c->hn;
+  int64_t max_rows;
+  if (is_full(c, layer)) {
+    a.full = c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D;
+    a.full_cap = c->full_cap;
+    a.full_rows = c->P[layer] + c->t[layer];
+    max_rows = a.full_rows;
+  } else {
+    const int64_t ib = inst_base(c, layer);
+    a.inst = c->d_inst + ib;
+    a.sinks = c->d_sinks + ib * 2 * std::max(c->S, 1) * D;
+    a.S = std::max(c->S, 1);
+    a.ws = c->d_ws;
+    a.ws_buf_stride = c->ws_buf_stride;
+    a.ws_inst_stride = c->ws_inst_stride;
+    a.inst_global_base = ib;
+    a.B = std::max(c->Bud, 1);
+    a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
+    a.ring_cap = c->ring_cap;
+    max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
+  }
+  // split-K: aim for ~2 waves of CTAs over 148 SMs, >= 64 rows per split
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((296 + n_ctas - 1) / n_ctas, max_rows / 64));
+  a.splits = std::min(splits, c->max_splits);
+  LKV_LAUNCH(c, launch_attn(a, st), "attn");
+  return LOUISKV_OK;
+}
+
+// ---------------------------------------------------------------- introspection
+static louiskv_status inst_lookup(louiskv_ctx* c, int layer, int b, int h, int64_t* gi) {
+  if (layer < 0 || layer >= c->L || b < 0 || b >= c->Bmax || h < 0 || h >= c->hn)
+    return fail(c, LOUISKV_ERR_INVALID_ARG, "bad (layer, b, h)");
+  if (is_full(c, layer)) return fail(c, LOUISKV_ERR_INVALID_ARG, "full-cache layer has no units");
+  *gi = inst_base(c, layer) + (int64_t)b * c->hn + h;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_selection(louiskv_ctx* c, int32_t layer, int32_t b, int32_t h, int32_t* ids, int32_t cap,
+                                     int32_t* n) {
+  LKV_CHECK_CTX(c);
+  int64_t gi;
+  louiskv_status s = inst_lookup(c, layer, b, h, &gi);
+  if (s) return s;
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_selection");
+  InstState is;
+  cudaMemcpy(&is, c->d_inst + gi, sizeof(is), cudaMemcpyDeviceToHost);
+  std::vector<uint8_t> sel(std::max(is.n_units, 1));
+  cudaMemcpy(sel.data(), c->d_sel + gi * c->Umax, is.n_units, cudaMemcpyDeviceToHost);
+  int cnt = 0;
+  for (int u = 0; u < is.n_units; ++u)
+    if (sel[u]) {
+      if (ids && cnt < cap) ids[cnt] = u;
+      ++cnt;
+    }
+  if (n) *n = cnt;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_units(louiskv_ctx* c, int32_t layer, int32_t b, int32_t h, int32_t cap, float* cf,
+                                 int32_t* sizes, int32_t* first_pos, int32_t* n_units) {
+  LKV_CHECK_CTX(c);
+  int64_t gi;
+  louiskv_status s = inst_lookup(c, layer, b, h, &gi);
+  if (s) return s;
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_units");
+  InstState is;
+  cudaMemcpy(&is, c->d_inst + gi, sizeof(is), cudaMemcpyDeviceToHost);
+  const int n = std::min(is.n_units, std::max(cap, 0));
+  if (cf && n) cudaMemcpy(cf, c->d_cent + gi * c->Umax * D, sizeof(float) * n * D, cudaMemcpyDeviceToHost);
+  if (sizes && n) cudaMemcpy(sizes, c->d_usize + gi * c->Umax, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+  if (first_pos && n) cudaMemcpy(first_pos, c->d_ufirst + gi * c->Umax, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+  if (n_units) *n_units = is.n_units;
+  if (is.error) return fail(c, LOUISKV_ERR_CAPACITY, "unit table / host pool capacity exceeded");
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_unit_positions(louiskv_ctx* c, int32_t layer, int32_t b, int32_t h, int32_t* positions,
+                                          int64_t cap, int64_t* n) {
+  LKV_CHECK_CTX(c);
+  int64_t gi;
+  louiskv_status s = inst_lookup(c, layer, b, h, &gi);
+  if (s) return s;
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_unit_positions");
+  InstState is;
+  cudaMemcpy(&is, c->d_inst + gi, sizeof(is), cudaMemcpyDeviceToHost);
+  const int64_t m = std::min<int64_t>(is.pool_rows, std::max<int64_t>(cap, 0));
+  if (positions && m)
+    cudaMemcpy(positions, c->d_pool_pos + gi * c->pool_rows_cap, sizeof(int32_t) * m, cudaMemcpyDeviceToHost);
+  if (n) *n = is.pool_rows;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_working_set(louiskv_ctx* c, int32_t layer, int32_t b, int32_t h, uint16_t* k_rows,
+                                       uint16_t* v_rows, int32_t cap, int32_t* n_rows) {
+  LKV_CHECK_CTX(c);
+  int64_t gi;
+  louiskv_status s = inst_lookup(c, layer, b, h, &gi);
+  if (s) return s;
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_working_set");
+  InstState is;
+  cudaMemcpy(&is, c->d_inst + gi, sizeof(is), cudaMemcpyDeviceToHost);
+  const int m = std::min(is.ws_rows, std::max(cap, 0));
+  const bf16* K = c->d_ws + is.ws_cur * c->ws_buf_stride + gi * c->ws_inst_stride;
+  const bf16* V = K + (int64_t)std::max(c->Bud, 1) * D;
+  if (k_rows && m) cudaMemcpy(k_rows, K, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
+  if (v_rows && m) cudaMemcpy(v_rows, V, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
+  if (n_rows) *n_rows = is.ws_rows;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_stats(louiskv_ctx* c, louiskv_stats* out) {
+  LKV_CHECK_CTX(c);
+  if (!out) return fail(c, LOUISKV_ERR_INVALID_ARG, "get_stats: null");
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_stats");
+  StatsDev sd;
+  cudaMemcpy(&sd, c->d_stats, sizeof(sd), cudaMemcpyDeviceToHost);
+  out->retrievals = sd.retrievals;
+  out->units_scored = sd.units_scored;
+  out->units_selected = sd.units_selected;
+  out->units_reused = sd.units_reused;
+  out->units_fetched = sd.units_fetched;
+  out->bytes_h2d = sd.bytes_h2d;
+  out->bytes_d2h = sd.bytes_d2h;
+  out->segments_evicted = sd.segments_evicted;
+  return LOUISKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,450 @@
+// kvm.store_cache(K, V, 'prefill') — P:120 [§4.2 Prefill stage: k-means of keys, centroid =
+// mean of the cluster's keys, offload to the CPU pool], P:258-265 [Alg. 1], P:126 [clustering
+// kernel].
+//
+// Per (b, owned kv-head) instance with N = P - S keys and k = ceil(N / c) clusters:
+//   init      C_j = x_{floor(j N / k)}                                    (reading R-AMB8)
+//   repeat iters times:
+//     assign  a_i = argmax_j (x_i · bf16(C_j) - ½||C_j||²), ties -> lower j  (tcgen05 GEMM with
+//             fused argmax epilogue in k_kmeans_tc.cu; SIMT fallback kernel here)
+//     hist    per 1024-key chunk cluster histogram
+//     scan    per-cluster exclusive prefix over chunks + cluster offsets (counting sort)
+//     repair  empty clusters take the farthest keys (largest dmin, ties -> lower index) from
+//             clusters with >= 2 members (reading R-AMB9); rare, one CTA per instance
+//     scatter stable counting-sort scatter: perm = keys grouped by cluster, positions ascending
+//     update  C_j = (sequential fp32 sum of member keys) / |j|, one warp per cluster
+//   offload   KV rows permuted cluster-major and written to the pinned host pool (zero-copy
+//             stores), unit table, sinks kept on the device.
+#include "lkv_internal.cuh"
+
+namespace lkv {
+
+constexpr int KM_CHUNK = 1024;
+
+__device__ __forceinline__ const bf16* xrow(const KmArgs& a, int li, int i) {
+  const int b = li / a.hn, h = li % a.hn;
+  return a.k + (int64_t)b * a.sb + (int64_t)(a.S + i) * a.st + (int64_t)h * a.sh;
+}
+__device__ __forceinline__ const bf16* vrow(const KmArgs& a, int li, int i) {
+  const int b = li / a.hn, h = li % a.hn;
+  return a.v + (int64_t)b * a.sb + (int64_t)(a.S + i) * a.st + (int64_t)h * a.sh;
+}
+
+// ---- init: C_j = x_{floor(j N / k)}; bf16 copy; ½||C_j||²  (warp per cluster)
+__global__ void km_init_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + warp;
+  if (j >= a.kc) return;
+  const int src = (int)(((int64_t)j * a.N) / a.kc);
+  const uint2 u = reinterpret_cast<const uint2*>(xrow(a, li, src))[lane];
+  float c[4] = {__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                __uint_as_float(u.y & 0xFFFF0000u)};
+  float* C = a.cent + ((int64_t)li * a.Umax + j) * D;
+  uint16_t* Cb = reinterpret_cast<uint16_t*>(a.centb) + ((int64_t)li * a.Umax + j) * D;
+  float ss = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    C[lane * 4 + e] = c[e];
+    Cb[lane * 4 + e] = f2bf_rne(c[e]);
+    ss = fmaf(c[e], c[e], ss);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) a.half[(int64_t)li * a.kmax + j] = 0.5f * ss;
+}
+
+// ---- SIMT assignment (correctness reference path; the tcgen05 kernel is the fast path)
+constexpr int AS_TILE = 32;
+__global__ void __launch_bounds__(128) km_assign_simt_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int i = blockIdx.x * 128 + threadIdx.x;
+  __shared__ uint32_t sc[AS_TILE][D / 2];
+  __shared__ float sh[AS_TILE];
+  float x[D];
+  float xn = 0.f;
+  if (i < a.N) {
+    const uint4* r = reinterpret_cast<const uint4*>(xrow(a, li, i));
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) unpack8(r[c], x + c * 8);
+#pragma unroll
+    for (int e = 0; e < D; ++e) xn = fmaf(x[e], x[e], xn);
+  }
+  float best = -INFINITY;
+  int bi = 0;
+  const uint32_t* Cb = reinterpret_cast<const uint32_t*>(a.centb + (int64_t)li * a.Umax * D);
+  const float* half = a.half + (int64_t)li * a.kmax;
+  for (int j0 = 0; j0 < a.kc; j0 += AS_TILE) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < AS_TILE * D / 2; t += 128) {
+      const int jj = t / (D / 2);
+      sc[jj][t % (D / 2)] = (j0 + jj < a.kc) ? Cb[(int64_t)(j0 + jj) * (D / 2) + t % (D / 2)] : 0u;
+    }
+    if (threadIdx.x < AS_TILE) sh[threadIdx.x] = (j0 + threadIdx.x < a.kc) ? half[j0 + threadIdx.x] : INFINITY;
+    __syncthreads();
+    const int jn = min(AS_TILE, a.kc - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      float dot = 0.f;
+#pragma unroll
+      for (int e2 = 0; e2 < D / 2; ++e2) {
+        const uint32_t w = sc[jj][e2];
+        dot = fmaf(x[2 * e2], __uint_as_float(w << 16), dot);
+        dot = fmaf(x[2 * e2 + 1], __uint_as_float(w & 0xFFFF0000u), dot);
+      }
+      const float s = dot - sh[jj];
+      if (s > best) {
+        best = s;
+        bi = j0 + jj;
+      }
+    }
+  }
+  if (i < a.N) {
+    a.assign[(int64_t)li * a.Nmax + i] = bi;
+    a.dmin[(int64_t)li * a.Nmax + i] = fmaf(-2.f, best, xn);
+  }
+}
+
+// ---- per-chunk histogram
+__global__ void __launch_bounds__(256) km_hist_kernel(KmArgs a, int nchunk) {
+  extern __shared__ int hist[];
+  const int li = blockIdx.y, c = blockIdx.x;
+  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  const int i0 = c * KM_CHUNK, i1 = min(a.N, i0 + KM_CHUNK);
+  const int32_t* as = a.assign + (int64_t)li * a.Nmax;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&hist[as[i]], 1);
+  __syncthreads();
+  int32_t* cc = a.cc + ((int64_t)li * a.nchunk_max + c) * a.kmax;
+  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) cc[j] = hist[j];
+}
+
+// column scan of cc + cluster offsets; one 1024-thread CTA per instance
+__device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
+  __shared__ int s_part[1024];
+  __shared__ int s_empty;
+  int32_t* cc = a.cc + (int64_t)li * a.nchunk_max * a.kmax;
+  int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
+  int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  if (threadIdx.x == 0) s_empty = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < nchunk; ++c) {
+      const int v = cc[(int64_t)c * a.kmax + j];
+      cc[(int64_t)c * a.kmax + j] = run;
+      run += v;
+    }
+    cnt[j] = run;
+    if (run == 0) s_empty = 1;
+  }
+  __syncthreads();
+  const int per = (a.kc + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * per, j1 = min(a.kc, j0 + per);
+  int local = 0;
+  for (int j = j0; j < j1; ++j) local += cnt[j];
+  s_part[threadIdx.x] = local;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int y = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  int run = s_part[threadIdx.x] - local;
+  for (int j = j0; j < j1; ++j) {
+    off[j] = run;
+    run += cnt[j];
+  }
+  if (threadIdx.x == 0) {
+    off[a.kc] = a.N;
+    a.flags[li] = s_empty;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) km_scan_kernel(KmArgs a, int nchunk) { km_scan_block(a, blockIdx.x, nchunk); }
+
+// empty-cluster repair (reading R-AMB9), then recount; only instances with an empty cluster
+__global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
+  const int li = blockIdx.x;
+  if (!a.flags[li]) return;
+  int32_t* as = a.assign + (int64_t)li * a.Nmax;
+  float* dm = a.dmin + (int64_t)li * a.Nmax;
+  int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
+  __shared__ float s_bv[32];
+  __shared__ int s_bi[32];
+  __shared__ int s_donor;
+  for (int j = 0; j < a.kc; ++j) {
+    if (cnt[j] != 0) continue;  // uniform: every thread reads the same value
+    float bv = -INFINITY;
+    int bi = 0x7FFFFFFF;
+    for (int i = threadIdx.x; i < a.N; i += blockDim.x) {
+      const float v = dm[i];
+      if (v == -INFINITY || cnt[as[i]] < 2) continue;
+      if (v > bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_bv[threadIdx.x >> 5] = bv;
+      s_bi[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float v = -INFINITY;
+      int d = 0x7FFFFFFF;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (s_bv[w] > v || (s_bv[w] == v && s_bi[w] < d)) {
+          v = s_bv[w];
+          d = s_bi[w];
+        }
+      s_donor = d;
+      if (d != 0x7FFFFFFF) {
+        cnt[as[d]] -= 1;
+        as[d] = j;
+        cnt[j] = 1;
+        dm[d] = -INFINITY;
+      }
+    }
+    __syncthreads();
+  }
+  // recount chunk histograms for this instance
+  int32_t* cc = a.cc + (int64_t)li * a.nchunk_max * a.kmax;
+  for (int64_t t = threadIdx.x; t < (int64_t)nchunk * a.kmax; t += blockDim.x) cc[t] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.N; i += blockDim.x) atomicAdd(&cc[(int64_t)(i / KM_CHUNK) * a.kmax + as[i]], 1);
+  __threadfence_block();
+  __syncthreads();
+  km_scan_block(a, li, nchunk);
+}
+
+// stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
+__global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
+  extern __shared__ int base[];  // [kc] running offsets of this chunk
+  const int li = blockIdx.y, c = blockIdx.x, lane = threadIdx.x;
+  const int32_t* cc = a.cc + ((int64_t)li * a.nchunk_max + c) * a.kmax;
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  for (int j = lane; j < a.kc; j += 32) base[j] = cc[j] + off[j];
+  __syncwarp();
+  const int32_t* as = a.assign + (int64_t)li * a.Nmax;
+  int32_t* perm = a.perm + (int64_t)li * a.Nmax;
+  const int i0 = c * KM_CHUNK, i1 = min(a.N, i0 + KM_CHUNK);
+  for (int r0 = i0; r0 < i1; r0 += 32) {
+    const int i = r0 + lane;
+    const bool valid = i < i1;
+    const int cl = valid ? as[i] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, cl);
+    const int leader = __ffs(peers) - 1;
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int bs = 0;
+    if (valid && lane == leader) bs = base[cl];
+    bs = __shfl_sync(0xffffffffu, bs, leader);
+    if (valid) perm[bs + rank] = i;
+    __syncwarp();
+    if (valid && lane == leader) base[cl] = bs + __popc(peers);
+    __syncwarp();
+  }
+}
+
+// centroid update: warp per cluster, sequential fp32 sum over members in position order
+__global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + warp;
+  if (j >= a.kc) return;
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
+  const int m0 = off[j], m1 = off[j + 1];
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  int m = m0;
+  for (; m + 4 <= m1; m += 4) {
+    uint2 u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = reinterpret_cast<const uint2*>(xrow(a, li, perm[m + q]))[lane];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s[0] = __fadd_rn(s[0], __uint_as_float(u[q].x << 16));
+      s[1] = __fadd_rn(s[1], __uint_as_float(u[q].x & 0xFFFF0000u));
+      s[2] = __fadd_rn(s[2], __uint_as_float(u[q].y << 16));
+      s[3] = __fadd_rn(s[3], __uint_as_float(u[q].y & 0xFFFF0000u));
+    }
+  }
+  for (; m < m1; ++m) {
+    const uint2 u = reinterpret_cast<const uint2*>(xrow(a, li, perm[m]))[lane];
+    s[0] = __fadd_rn(s[0], __uint_as_float(u.x << 16));
+    s[1] = __fadd_rn(s[1], __uint_as_float(u.x & 0xFFFF0000u));
+    s[2] = __fadd_rn(s[2], __uint_as_float(u.y << 16));
+    s[3] = __fadd_rn(s[3], __uint_as_float(u.y & 0xFFFF0000u));
+  }
+  const float n = (float)(m1 - m0);
+  float* C = a.cent + ((int64_t)li * a.Umax + j) * D;
+  uint16_t* Cb = reinterpret_cast<uint16_t*>(a.centb) + ((int64_t)li * a.Umax + j) * D;
+  float ss = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float c = m1 > m0 ? __fdiv_rn(s[e], n) : C[lane * 4 + e];
+    C[lane * 4 + e] = c;
+    Cb[lane * 4 + e] = f2bf_rne(c);
+    ss = fmaf(c, c, ss);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) a.half[(int64_t)li * a.kmax + j] = 0.5f * ss;
+}
+
+// caller-supplied clustering: copy assignment and centroids in
+__global__ void km_ext_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.N; t += (int64_t)gridDim.x * blockDim.x)
+    a.assign[(int64_t)li * a.Nmax + t] = a.ext_assign[(int64_t)li * a.N + t];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.kc * D;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const float c = a.ext_cent[(int64_t)li * a.kc * D + t];
+    a.cent[(int64_t)li * a.Umax * D + t] = c;
+    reinterpret_cast<uint16_t*>(a.centb)[(int64_t)li * a.Umax * D + t] = f2bf_rne(c);
+  }
+}
+
+// offload: pool row r (cluster-major order) <- key perm[r]; unit-major spans [K rows | V rows]
+__global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 4), sub = threadIdx.x & 15;
+  if (r >= a.N) return;
+  const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  const int i = perm[r];
+  const int j = a.assign[(int64_t)li * a.Nmax + i];
+  const int o = off[j], n = off[j + 1] - o;
+  uint4* dst = reinterpret_cast<uint4*>(a.pool + (int64_t)li * a.pool_inst_bytes + (int64_t)o * POOL_ROW_BYTES);
+  dst[(int64_t)(r - o) * 16 + sub] = reinterpret_cast<const uint4*>(xrow(a, li, i))[sub];
+  dst[(int64_t)(n + r - o) * 16 + sub] = reinterpret_cast<const uint4*>(vrow(a, li, i))[sub];
+  if (sub == 0) a.pool_pos[(int64_t)li * a.pool_rows_cap + r] = a.S + i;
+}
+
+// unit table + instance reset after clustering
+__global__ void km_units_kernel(KmArgs a, int P) {
+  const int li = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  if (j < a.kc) {
+    a.usize[(int64_t)li * a.Umax + j] = off[j + 1] - off[j];
+    a.uoff[(int64_t)li * a.Umax + j] = off[j];
+    a.ufirst[(int64_t)li * a.Umax + j] = a.S + a.perm[(int64_t)li * a.Nmax + off[j]];
+    a.sel[(int64_t)li * a.Umax + j] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    InstState s{};
+    s.n_units = a.kc;
+    s.n_prompt_units = a.kc;
+    s.pool_rows = a.N;
+    s.prompt_len = P;
+    s.s_eff = min(a.S_cap, P);
+    a.inst[li] = s;
+    atomicAdd(&a.stats->bytes_d2h, (unsigned long long)a.N * POOL_ROW_BYTES);
+  }
+}
+
+// sinks [0, S) stay on the device
+__global__ void km_sinks_kernel(KmArgs a, int s_eff) {
+  const int li = blockIdx.y;
+  const int b = li / a.hn, h = li % a.hn;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 4), sub = threadIdx.x & 15;
+  if (r >= s_eff) return;
+  const bf16* ks = a.k + (int64_t)b * a.sb + (int64_t)r * a.st + (int64_t)h * a.sh;
+  const bf16* vs = a.v + (int64_t)b * a.sb + (int64_t)r * a.st + (int64_t)h * a.sh;
+  bf16* dk = a.sinks + (int64_t)li * 2 * a.S_cap * D + (int64_t)r * D;
+  bf16* dv = dk + (int64_t)a.S_cap * D;
+  reinterpret_cast<uint4*>(dk)[sub] = reinterpret_cast<const uint4*>(ks)[sub];
+  reinterpret_cast<uint4*>(dv)[sub] = reinterpret_cast<const uint4*>(vs)[sub];
+}
+
+__global__ void reset_insts_kernel(InstState* inst, int n, int P, int s_eff) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  InstState s{};
+  s.prompt_len = P;
+  s.s_eff = s_eff;
+  inst[i] = s;
+}
+
+cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st);  // k_kmeans_tc.cu
+
+static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool repair, cudaStream_t st) {
+  km_hist_kernel<<<dim3(nchunk, ni), 256, sizeof(int) * a.kc, st>>>(a, nchunk);
+  km_scan_kernel<<<ni, 1024, 0, st>>>(a, nchunk);
+  if (repair) km_repair_kernel<<<ni, 1024, 0, st>>>(a, nchunk);
+  km_scatter_kernel<<<dim3(nchunk, ni), 32, sizeof(int) * a.kc, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st) {
+  const int ni = a.batch * a.hn;
+  const int P = a.S + a.N;
+  const int s_eff = min(a.S_cap, P);
+  cudaError_t e;
+  if (s_eff > 0) km_sinks_kernel<<<dim3((s_eff + 7) / 8, ni), 128, 0, st>>>(a, s_eff);
+  if (a.N <= 0 || a.kc <= 0) {
+    reset_insts_kernel<<<(ni + 127) / 128, 128, 0, st>>>(a.inst, ni, P, s_eff);
+    return cudaGetLastError();
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(km_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(km_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int nchunk = (a.N + KM_CHUNK - 1) / KM_CHUNK;
+  const dim3 gk((a.kc + 3) / 4, ni);
+  if (a.ext_assign) {
+    km_ext_kernel<<<dim3(64, ni), 256, 0, st>>>(a);
+    if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
+  } else {
+    km_init_kernel<<<gk, 128, 0, st>>>(a);
+    for (int it = 0; it < a.iters; ++it) {
+      if (a.impl == LOUISKV_KMEANS_TC && kmeans_tc_available()) {
+        if ((e = launch_assign_tc(a, st)) != cudaSuccess) return e;
+      } else {
+        km_assign_simt_kernel<<<dim3((a.N + 127) / 128, ni), 128, 0, st>>>(a);
+      }
+      if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
+      km_update_kernel<<<gk, 128, 0, st>>>(a);
+    }
+  }
+  km_offload_kernel<<<dim3((a.N + 7) / 8, ni), 128, 0, st>>>(a);
+  km_units_kernel<<<dim3((a.kc + 255) / 256, ni), 256, 0, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+__global__ void full_prompt_kernel(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int hn,
+                                   int64_t P, bf16* full, int64_t full_cap) {
+  const int li = blockIdx.y, b = li / hn, h = li % hn;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 4);
+  const int sub = threadIdx.x & 15;
+  if (r >= P) return;
+  bf16* K = full + (int64_t)li * 2 * full_cap * D;
+  bf16* V = K + full_cap * D;
+  reinterpret_cast<uint4*>(K + r * D)[sub] = reinterpret_cast<const uint4*>(k + b * sb + r * st_ + h * sh)[sub];
+  reinterpret_cast<uint4*>(V + r * D)[sub] = reinterpret_cast<const uint4*>(v + b * sb + r * st_ + h * sh)[sub];
+}
+
+cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int batch, int hn,
+                               int64_t P, bf16* full, int64_t full_cap, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  full_prompt_kernel<<<dim3((unsigned)((P + 7) / 8), batch * hn), 128, 0, st>>>(k, v, sb, st_, sh, hn, P, full,
+                                                                                full_cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st) {
+  reset_insts_kernel<<<(n + 127) / 128, 128, 0, st>>>(inst, n, P, s_eff);
+  return cudaGetLastError();
+}
+
+}  // namespace lkv

@@ -1,0 +1,214 @@
+// Internal declarations of the LouisKV B200 library (not part of the ABI).
+// Kernels live in k_*.cu; the C ABI and all state management in api.cu.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "louiskv.h"
+
+namespace lkv {
+
+constexpr int D = 128;               // head_dim (the paper's models all use 128)
+constexpr int ROW_BYTES = D * 2;     // one bf16 K (or V) row
+constexpr int POOL_ROW_BYTES = 2 * ROW_BYTES;  // K+V of one token in the host pool
+
+typedef __nv_bfloat16 bf16;
+
+// Per (retrieval layer, b, owned kv-head) decode state, device resident.
+struct InstState {
+  int32_t n_units;        // prompt clusters + evicted segments (scorable units)
+  int32_t n_prompt_units; // k
+  int64_t pool_rows;      // rows used in this instance's host-pool region
+  int32_t ws_cur;         // which working-set buffer is current (0/1)
+  int32_t ws_rows;        // rows in the current working set
+  int32_t open_len;       // tokens in the open segment
+  int32_t open_start;     // decode index (0-based) of the first open token
+  int32_t buffered;       // tokens in the local buffer (sealed + open)
+  int32_t ring_head;      // decode index of the oldest buffered token
+  int32_t fifo_head;      // sealed-segment FIFO (ring of ring_cap int2 entries)
+  int32_t fifo_count;
+  int32_t error;          // capacity overflow (sticky)
+  int32_t prompt_len;     // P
+  int32_t s_eff;          // min(S, P)
+  int32_t pad;
+};
+
+// One gather job per active instance (written by score_select, read by gather).
+struct GatherJob {
+  int32_t n_rows;
+  int32_t pad;
+  bf16* dstK;
+  bf16* dstV;
+};
+struct RowSrc {
+  const uint4* k;
+  const uint4* v;
+};
+
+struct StatsDev {
+  unsigned long long retrievals, units_scored, units_selected, units_reused, units_fetched, bytes_h2d,
+      bytes_d2h, segments_evicted;
+};
+
+// ---------------------------------------------------------------- kernel launchers
+// trigger (k_trigger.cu)
+cudaError_t launch_trigger(const bf16* q_all, int64_t stride_b, int batch, int Hq, bf16* q_ref, uint8_t* flag,
+                           double* r, uint8_t* flag_out, double* r_out, int t, double tau, int trigger_ref,
+                           cudaStream_t st);
+cudaError_t launch_copy_flags(const uint8_t* src_flag, const double* src_r, uint8_t* flag, double* r,
+                              uint8_t* flag_out, double* r_out, int batch, cudaStream_t st);
+
+// retrieve (k_retrieve.cu)
+struct RetrieveArgs {
+  const bf16* q_own;
+  int64_t stride_b;
+  int batch, hn, g, Umax, budget;
+  const uint8_t* flag;       // [batch] of this layer
+  InstState* inst;           // layer base, [batch*hn]
+  const bf16* centb;         // layer base [batch*hn][Umax][D]
+  const int32_t* usize;      // [batch*hn][Umax]
+  const int64_t* uoff;       // [batch*hn][Umax]
+  uint8_t* sel;              // [batch*hn][Umax]
+  int32_t* seloff;           // [batch*hn][Umax]
+  const uint8_t* pool;       // host pool (device-mapped pointer), layer base
+  int64_t pool_inst_bytes;   // bytes per instance region
+  bf16* ws;                  // working sets: [2][n_inst_total][2][B][D]
+  int64_t ws_buf_stride;     // elements between buffer 0 and 1
+  int64_t ws_inst_stride;    // elements per instance (2*B*D)
+  int64_t inst_global_base;  // global instance index of this layer's first instance
+  float* scratch_e;          // [batch*hn][g][Umax]
+  unsigned long long* scratch_key;  // [batch*hn][Umax]
+  GatherJob* jobs;           // [batch*hn]
+  RowSrc* rows;              // [batch*hn][B]
+  StatsDev* stats;
+};
+cudaError_t launch_score_select(const RetrieveArgs& a, cudaStream_t st);
+cudaError_t launch_gather(const GatherJob* jobs, const RowSrc* rows, int n_inst, int budget, cudaStream_t st);
+
+// append (k_append.cu)
+struct AppendArgs {
+  const bf16* k_t;
+  const bf16* v_t;
+  int64_t stride_b;
+  int batch, hn, t, W, max_open, ring_cap, Umax;
+  const uint8_t* flag;  // [batch]
+  InstState* inst;
+  bf16* ring;           // layer base [batch*hn][2][ring_cap][D]
+  int2* fifo;           // [batch*hn][ring_cap]
+  float* cent;          // [batch*hn][Umax][D]
+  bf16* centb;
+  int32_t* usize;
+  int64_t* uoff;
+  int32_t* ufirst;
+  uint8_t* sel;
+  int32_t* pool_pos;    // [batch*hn][pool_rows_cap]
+  int64_t pool_rows_cap;
+  uint8_t* pool;        // host pool (device-mapped), layer base
+  int64_t pool_inst_bytes;
+  StatsDev* stats;
+};
+cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);
+cudaError_t launch_full_append(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
+                               int64_t full_cap, int64_t pos, cudaStream_t st);
+
+// attention (k_attn.cu)
+struct AttnArgs {
+  const bf16* q_own;
+  int64_t stride_b;
+  int batch, hn, g;
+  float scale_log2;  // log2(e)/sqrt(d)
+  // sparse layers
+  const InstState* inst;  // may be null for full layers
+  const bf16* sinks;      // [batch*hn][2][S][D]
+  int S;
+  const bf16* ws;         // global working-set base
+  int64_t ws_buf_stride, ws_inst_stride, inst_global_base;
+  int B;
+  const bf16* ring;       // [batch*hn][2][ring_cap][D]
+  int ring_cap;
+  // full layers
+  const bf16* full;       // [batch*hn][2][full_cap][D]
+  int64_t full_cap;
+  int64_t full_rows;
+  // outputs
+  bf16* out;
+  float* out_f32;
+  // scratch
+  float* part;            // [batch*hn][splits][g][D+2]
+  int* counters;          // [batch*hn]
+  int splits;
+};
+cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+
+// k-means / prompt (k_kmeans.cu)
+struct KmArgs {
+  const bf16* k;
+  const bf16* v;
+  int64_t sb, st, sh;
+  int batch, hn, S, N, kc, iters, impl;
+  // outputs / state (layer bases)
+  float* cent;       // [ni][Umax][D]
+  bf16* centb;
+  int Umax;
+  int32_t* usize;
+  int64_t* uoff;
+  int32_t* ufirst;
+  uint8_t* sel;
+  int32_t* pool_pos;
+  int64_t pool_rows_cap;
+  uint8_t* pool;
+  int64_t pool_inst_bytes;
+  bf16* sinks;       // [ni][2][S][D]
+  int S_cap;
+  InstState* inst;
+  // scratch
+  float* half;       // [ni][kmax]
+  int32_t* assign;   // [ni][Nmax]
+  float* dmin;       // [ni][Nmax]
+  int32_t* cc;       // [ni][nchunk][kmax]
+  int32_t* off;      // [ni][kmax+1]
+  int32_t* cnt;      // [ni][kmax]
+  int32_t* perm;     // [ni][Nmax]
+  int32_t* flags;    // [ni]
+  int64_t Nmax;
+  int kmax;
+  int nchunk_max;
+  StatsDev* stats;
+  const int32_t* ext_assign;   // device copy of caller-provided assignment (set_prompt_units)
+  const float* ext_cent;       // device copy of caller-provided centroids
+};
+cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st);
+cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int batch, int hn,
+                               int64_t P, bf16* full, int64_t full_cap, cudaStream_t st);
+cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st);
+
+bool kmeans_tc_available();
+
+}  // namespace lkv
+
+// ---------------------------------------------------------------- device helpers
+#ifdef __CUDACC__
+namespace lkv {
+__device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+__device__ __forceinline__ void unpack8(const uint4 u, float* f) {
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xFFFF0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xFFFF0000u);
+  f[4] = __uint_as_float(u.z << 16);
+  f[5] = __uint_as_float(u.z & 0xFFFF0000u);
+  f[6] = __uint_as_float(u.w << 16);
+  f[7] = __uint_as_float(u.w & 0xFFFF0000u);
+}
+// fp32 -> bf16 bits, round to nearest even (NaN-free inputs)
+__device__ __forceinline__ uint16_t f2bf_rne(float x) {
+  uint32_t u = __float_as_uint(x);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+}  // namespace lkv
+#endif

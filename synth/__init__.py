@@ -56,13 +56,27 @@ def planted(cfg: Config, layer: int, seed: int, device="cpu") -> LayerPlant:
     return LayerPlant(mu0, mu)
 
 
-def prompt_kv(cfg: Config, layer: int, seed: int, device="cpu", plant: Optional[LayerPlant] = None):
-    """K, V bf16 [b, P, Hkv, d] for one layer (positions scattered over planted groups)."""
+def prompt_kv(cfg: Config, layer: int, seed: int, device="cpu", plant: Optional[LayerPlant] = None,
+              layout: str = "scattered", return_labels: bool = False):
+    """K, V bf16 [b, P, Hkv, d] for one layer.
+
+    layout="scattered": each position draws its planted group at random (the sparse input
+    layout of P:90); layout="blocked": group j occupies positions [S + j*N/k_pl, ...), so
+    the strided k-means init seeds one centroid per group (well-separated parity inputs).
+    With return_labels, also returns the planted group id per (b, position, head)."""
     if plant is None:
         plant = planted(cfg, layer, seed, device)
     g = _gen(device, seed, 2, layer)
     b, P, H, d = cfg.batch, cfg.prompt_len, cfg.num_kv_heads, cfg.head_dim
-    cid = torch.randint(0, cfg.k_planted, (b, P, H), generator=g, device=device)
+    if layout == "blocked":
+        S = min(cfg.sink_tokens, P)
+        N = P - S
+        pos = torch.arange(P, device=device)
+        grp = torch.clamp(((pos - S).clamp(min=0) * cfg.k_planted) // max(N, 1), max=cfg.k_planted - 1)
+        cid = grp.view(1, P, 1).expand(b, P, H).contiguous()
+        _ = torch.randint(0, 2, (1,), generator=g, device=device)
+    else:
+        cid = torch.randint(0, cfg.k_planted, (b, P, H), generator=g, device=device)
     # gather planted direction per (b, pos, head)
     mu = plant.mu  # [b, H, k, d]
     idx = cid.permute(0, 2, 1)  # [b, H, P]
@@ -70,6 +84,8 @@ def prompt_kv(cfg: Config, layer: int, seed: int, device="cpu", plant: Optional[
     K = plant.mu0.unsqueeze(2) + sel + _randn((b, H, P, d), g, device, cfg.key_noise)
     K = K.permute(0, 2, 1, 3).contiguous()
     V = _randn((b, P, H, d), g, device)
+    if return_labels:
+        return K.to(torch.bfloat16), V.to(torch.bfloat16), cid
     return K.to(torch.bfloat16), V.to(torch.bfloat16)
 
 

@@ -1,0 +1,355 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same
+seeded inputs (north_star tolerances: trigger decisions and retrieved index sets
+bit-exact; centroids 1e-3 relative; attention 2e-2 absolute)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle.episode import OracleEpisode, PREV_STEP, LAST_RETRIEVAL, PER_LAYER, SHARED
+from synth.configs import Config, C1, C2
+
+from _pair import bf16_bits, make_inputs, np32, oracle_assign, planted_assign
+
+pytestmark = pytest.mark.gpu
+
+ATTN_TOL = 2e-2
+
+
+def _lkv():
+    import paper_2510_11292_b200 as lkv
+    return lkv
+
+
+def small_cfg(**kw):
+    base = dict(name="small", num_layers=3, num_q_heads=8, num_kv_heads=2, head_dim=128, batch=2,
+                prompt_len=1100, decode_steps=40, sink_tokens=16, window_tokens=24, budget_tokens=96,
+                tau=0.85, avg_cluster_size=16, kmeans_iters=4, full_cache_layers=(0,), seg_mean=5.0)
+    base.update(kw)
+    return Config(**base)
+
+
+def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
+                check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True):
+    """Drive GPU and oracle through `steps` decode steps; assert parity at every step."""
+    lkv = _lkv()
+    hn = cfg.num_kv_heads - kv_head_begin if kv_head_count is None else kv_head_count
+    h0 = kv_head_begin
+    g = cfg.group
+    ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
+                                      boundary_mode=boundary_mode, max_open_segment=max_open or 0))
+    ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
+                       kv_head_begin=h0, kv_head_count=hn)
+    L, b = cfg.num_layers, cfg.batch
+    for l in range(L):
+        Kl = inp.K[l][:, :, h0:h0 + hn]
+        Vl = inp.V[l][:, :, h0:h0 + hn]
+        Kn, Vn = np32(Kl), np32(Vl)
+        if l in cfg.full_cache_layers:
+            ctx.cluster_prompt(l, Kl, Vl)
+            ep.cluster_prompt(l, Kn, Vn)
+        else:
+            a = assign_fn(l, Kn)
+            ep.cluster_prompt(l, Kn, Vn, assign=a)
+            cen = np.stack([[np.stack([u.centroid for u in ep.units(l, bb, hh)]) for hh in range(hn)]
+                            for bb in range(b)]) if cfg.prompt_len > cfg.sink_tokens else np.zeros((b, hn, 0, 128))
+            ctx.set_prompt_units(l, Kl, Vl, a, cen)
+    flag_d = torch.zeros(b, dtype=torch.uint8, device="cuda")
+    r_d = torch.zeros(b, dtype=torch.float64, device="cuda")
+    out = torch.zeros((b, g * hn, 128), dtype=torch.bfloat16, device="cuda")
+    out32 = torch.zeros((b, g * hn, 128), dtype=torch.float32, device="cuda")
+    worst = 0.0
+    n_flags = 0
+    for t in range(steps):
+        for l in range(L):
+            qa = inp.q[t, l]
+            qo = qa[:, h0 * g:(h0 + hn) * g]
+            kt = inp.k[t, l][:, h0:h0 + hn]
+            vt = inp.v[t, l][:, h0:h0 + hn]
+            ctx.should_retrieve(l, qa, flag_d, r_d)
+            ctx.retrieve(l, qo)
+            ctx.append_output(l, kt.contiguous(), vt.contiguous())
+            ctx.sparse_attn(l, qo, out, out32)
+            f_o, r_o = ep.should_retrieve(l, np32(qa))
+            ep.retrieve(l, np32(qo))
+            ep.append_output(l, np32(kt), np32(vt))
+            o_o = ep.sparse_attn(l, np32(qo))
+            torch.cuda.synchronize()
+            f_g = flag_d.cpu().numpy()
+            r_g = r_d.cpu().numpy()
+            assert np.array_equal(f_g.astype(np.int32), f_o), (t, l, f_g, f_o)
+            if l not in cfg.full_cache_layers:
+                assert np.array_equal(r_g.view(np.uint64), r_o.view(np.uint64)), (t, l, r_g, r_o)
+                n_flags += int(f_o.sum())
+            err = np.abs(out32.cpu().numpy().astype(np.float64) - o_o).max()
+            errb = np.abs(out.float().cpu().numpy().astype(np.float64) - o_o).max()
+            worst = max(worst, err, errb)
+            assert err < ATTN_TOL and errb < ATTN_TOL, (t, l, err, errb)
+            if check_every_step and l not in cfg.full_cache_layers:
+                for bb in range(b):
+                    for hh in range(hn):
+                        sel_g = ctx.get_selection(l, bb, hh)
+                        sel_o = np.array(ep.selection(l, bb, hh), np.int32)
+                        assert np.array_equal(sel_g, sel_o), (t, l, bb, hh, sel_g, sel_o)
+                        if compare_ws and f_o[bb]:
+                            Kw, Vw = ctx.get_working_set(l, bb, hh)
+                            units = ep.units(l, bb, hh)
+                            if len(sel_o):
+                                Ko = np.concatenate([units[u].K for u in sel_o])
+                                Vo = np.concatenate([units[u].V for u in sel_o])
+                            else:
+                                Ko = Vo = np.zeros((0, 128), np.float32)
+                            assert np.array_equal(Kw, bf16_bits(Ko)) and np.array_equal(Vw, bf16_bits(Vo))
+    # unit tables (prompt clusters + evicted segments), bit-exact
+    for l in range(L):
+        if l in cfg.full_cache_layers:
+            continue
+        for bb in range(b):
+            for hh in range(hn):
+                cen, sizes, first = ctx.get_units(l, bb, hh)
+                units = ep.units(l, bb, hh)
+                assert len(sizes) == len(units)
+                assert np.array_equal(sizes, [u.positions.size for u in units])
+                assert np.array_equal(first, [int(u.positions[0]) for u in units])
+                assert np.array_equal(cen.view(np.uint32), np.stack([u.centroid for u in units]).view(np.uint32)) \
+                    if units else True
+                pos = ctx.get_unit_positions(l, bb, hh)
+                assert np.array_equal(pos, np.concatenate([u.positions for u in units]) if units else pos)
+    st_g, st_o = ctx.stats(), ep.stats
+    for key in ("retrievals", "units_scored", "units_selected", "units_reused", "units_fetched", "bytes_h2d",
+                "bytes_d2h", "segments_evicted"):
+        assert st_g[key] == st_o[key], (key, st_g[key], st_o[key])
+    ctx.close()
+    return worst, n_flags, st_o
+
+
+# ------------------------------------------------------------------ episodes
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_episode_oracle_clustering_small(seed):
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, seed)
+    worst, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn))
+    assert n_flags > 5 and st["segments_evicted"] > 0 and st["units_reused"] > 0
+
+
+def test_episode_c1_shape():
+    # BASELINE C1: one KV head, 4096-token prompt, 64 clusters, 10 iters, 16 decode queries (g=1),
+    # plus the GQA variant with 4 query heads.
+    for hq in (1, 4):
+        cfg = C1.replace(num_q_heads=hq)
+        inp = make_inputs(cfg, cfg.decode_steps, 0)
+        run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn))
+
+
+def test_episode_last_retrieval_and_shared_modes():
+    cfg = small_cfg(decode_steps=30)
+    inp = make_inputs(cfg, 30, 3)
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), trigger_ref=LAST_RETRIEVAL)
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), boundary_mode=SHARED)
+
+
+def test_episode_degenerate_tau_budget_force_seal():
+    cfg = small_cfg(decode_steps=20, tau=1.01, budget_tokens=0)   # retrieve every step, empty budget
+    inp = make_inputs(cfg, 20, 4)
+    _, n_flags, st = run_episode(cfg, inp, 20, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
+    assert st["units_selected"] == 0
+    cfg = small_cfg(decode_steps=20, tau=-1.0)                      # only t == 1
+    _, n_flags, st = run_episode(cfg, inp, 20, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
+    assert st["retrievals"] == cfg.batch * 2
+    cfg = small_cfg(decode_steps=30, tau=-1.0, window_tokens=6)     # force-seal at max_open=3
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3)
+
+
+def test_superset_budget_equals_full_attention():
+    cfg = small_cfg(num_layers=2, full_cache_layers=(0,), budget_tokens=2000, window_tokens=64,
+                    decode_steps=12, prompt_len=700, tau=1.01)
+    inp = make_inputs(cfg, 12, 5)
+    lkv = _lkv()
+    run_episode(cfg, inp, 12, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
+    # direct check against the dense definition for layer 1 (retrieval) == layer-0-style full attention
+    ctx = lkv.Context(lkv.make_config(cfg))
+    for l in range(2):
+        if l == 0:
+            ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+        else:
+            a = planted_assign(cfg, inp.labels[l])
+            Kn = np32(inp.K[l])
+            cen = np.stack([[oracle.centroids_of(Kn[bb, cfg.sink_tokens:, hh], a[bb, hh], a.max() + 1)
+                             for hh in range(2)] for bb in range(2)])
+            ctx.set_prompt_units(l, inp.K[l], inp.V[l], a, cen)
+    out32 = torch.zeros((2, 8, 128), dtype=torch.float32, device="cuda")
+    out = torch.zeros((2, 8, 128), dtype=torch.bfloat16, device="cuda")
+    for t in range(12):
+        for l in range(2):
+            ctx.should_retrieve(l, inp.q[t, l])
+            ctx.retrieve(l, inp.q[t, l])
+            ctx.append_output(l, inp.k[t, l], inp.v[t, l])
+            ctx.sparse_attn(l, inp.q[t, l], out, out32)
+            if l == 1:
+                o = out32.cpu().numpy()
+                for bb in range(2):
+                    for hh in range(2):
+                        Kf = np.concatenate([np32(inp.K[1][bb, :, hh]), np32(inp.k[:t + 1, 1, bb, hh])])
+                        Vf = np.concatenate([np32(inp.V[1][bb, :, hh]), np32(inp.v[:t + 1, 1, bb, hh])])
+                        ref = oracle.attention_f64(np32(inp.q[t, 1, bb, 4 * hh:4 * hh + 4]), Kf, Vf)
+                        assert np.abs(o[bb, 4 * hh:4 * hh + 4] - ref).max() < ATTN_TOL
+    ctx.close()
+
+
+def test_near_threshold_trigger_bit_exact():
+    """tau set exactly at (and one ulp above) the oracle's r_t: the decision must flip identically."""
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=12, batch=1)
+    inp = make_inputs(cfg, 12, 6)
+    q = np32(inp.q[:, 0, 0])
+    lkv = _lkv()
+    for t_probe in (3, 7):
+        r = oracle.trigger_r1(q[t_probe - 2], q[t_probe - 1], t_probe, 0.0)[1]
+        for tau in (r, np.nextafter(r, 2.0), np.nextafter(r, -2.0)):
+            c = cfg.replace(tau=float(tau))
+            ctx = lkv.Context(lkv.make_config(c))
+            ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+            fl = torch.zeros(1, dtype=torch.uint8, device="cuda")
+            rr = torch.zeros(1, dtype=torch.float64, device="cuda")
+            for t in range(1, t_probe + 1):
+                ctx.should_retrieve(0, inp.q[t - 1, 0], fl, rr)
+                ctx.retrieve(0, inp.q[t - 1, 0])
+                ctx.append_output(0, inp.k[t - 1, 0], inp.v[t - 1, 0])
+            torch.cuda.synchronize()
+            f_o, r_o = oracle.trigger_r1(q[t_probe - 2], q[t_probe - 1], t_probe, float(tau))
+            assert int(fl.item()) == f_o and rr.item() == r_o
+            ctx.close()
+
+
+def test_duplicate_centroids_ties_to_lower_id():
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=6, batch=1, num_kv_heads=1, num_q_heads=4,
+                    budget_tokens=40)
+    inp = make_inputs(cfg, 6, 7)
+    Kn = np32(inp.K[0])
+    N = cfg.prompt_len - cfg.sink_tokens
+    k = -(-N // 16)
+    # two keys sets with exactly identical content -> duplicated centroids -> exact A ties
+    K2 = inp.K[0].clone()
+    half = N // 2
+    K2[:, cfg.sink_tokens + half:cfg.sink_tokens + 2 * half] = K2[:, cfg.sink_tokens:cfg.sink_tokens + half]
+    a = np.zeros((1, 1, N), np.int32)
+    a[0, 0, :2 * half] = np.concatenate([np.arange(half) % (k // 2), np.arange(half) % (k // 2) + k // 2])
+    a[0, 0, 2 * half:] = k - 1
+    inp.K[0] = K2
+    run_episode(cfg, inp, 6, lambda l, Kn_: a)
+
+
+def test_zero_query_and_prompt_shorter_than_sinks():
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=6, batch=1, prompt_len=12, sink_tokens=16)
+    inp = make_inputs(cfg, 6, 8)
+    inp.q[2] = 0  # zero query: cosine 0
+    run_episode(cfg, inp, 6, lambda l, Kn: np.zeros((1, 2, 0), np.int32))
+
+
+def test_head_shard_equals_full_run():
+    """Multi-GPU decomposition: a ctx owning KV heads [1, 2) reproduces the 2-head run bitwise."""
+    cfg = small_cfg(decode_steps=16)
+    inp = make_inputs(cfg, 16, 9)
+    # the shard's clustering is the corresponding slice of the full clustering
+    full_assign = {l: planted_assign(cfg, inp.labels[l]) for l in range(cfg.num_layers)}
+    run_episode(cfg, inp, 16, lambda l, Kn: full_assign[l][:, 1:2], kv_head_begin=1, kv_head_count=1)
+
+
+# ------------------------------------------------------------------ k-means (GPU clustering)
+def _gpu_units(ctx, l, b, h, N, S):
+    cen, sizes, first = ctx.get_units(l, b, h)
+    pos = ctx.get_unit_positions(l, b, h)
+    assign = np.empty(N, np.int32)
+    o = 0
+    for j, s in enumerate(sizes):
+        assign[pos[o:o + s] - S] = j
+        o += s
+    return assign, cen
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+def test_kmeans_well_separated_exact(impl):
+    lkv = _lkv()
+    cfg = C1.replace(kmeans_iters=10)
+    inp = make_inputs(cfg, 1, 0, layout="blocked")
+    ctx = lkv.Context(lkv.make_config(cfg, kmeans_impl=impl))
+    ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+    X = np32(inp.K[0])[0, :, 0]
+    a_o, C_o, cnt, J, _ = oracle.kmeans(X, 64, 10, mode=1)
+    a_g, C_g = _gpu_units(ctx, 0, 0, 0, 4096, 0)
+    assert np.array_equal(a_g, a_o)
+    rel = np.abs(C_g - C_o) / np.maximum(np.abs(C_o), 1e-3 * np.abs(C_o).max())
+    assert rel.max() < 1e-3
+    ctx.close()
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+def test_kmeans_overlapping_near_ties_only(impl):
+    lkv = _lkv()
+    cfg = C1.replace(k_planted=16, kmeans_iters=10, num_kv_heads=1)
+    inp = make_inputs(cfg, 1, 1)
+    ctx = lkv.Context(lkv.make_config(cfg, kmeans_impl=impl))
+    ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+    X = np32(inp.K[0])[0, :, 0]
+    a_o, C_o, cnt, J_o, _ = oracle.kmeans(X, 64, 10, mode=1)
+    a_g, C_g = _gpu_units(ctx, 0, 0, 0, 4096, 0)
+    # partition: every key in exactly one non-empty cluster
+    assert np.bincount(a_g, minlength=64).min() >= 1
+    # centroid = mean of members within 1e-3 relative
+    C_chk = oracle.centroids_of(X, a_g, 64)
+    assert np.abs(C_g - C_chk).max() <= 1e-3 * np.abs(C_chk).max()
+    # objective parity and mismatch rate
+    J_g = ((X.astype(np.float64) - C_g[a_g].astype(np.float64)) ** 2).sum()
+    assert J_g <= J_o[-1] * (1 + 1e-3)
+    mismatch = (a_g != a_o).mean()
+    print(f"kmeans overlapping: mismatch rate {mismatch:.4%}, J_gpu/J_oracle = {J_g / J_o[-1]:.6f}")
+    assert mismatch < 0.05
+    ctx.close()
+
+
+def test_kmeans_tiny_tail_and_repair():
+    """N < k*c tails and identical keys (empty-cluster repair path)."""
+    lkv = _lkv()
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), batch=1, num_kv_heads=1, num_q_heads=1, prompt_len=16 + 37,
+                    kmeans_iters=3)
+    inp = make_inputs(cfg, 1, 2)
+    K = inp.K[0].clone()
+    K[:, 16:40] = K[:, 16:17]  # 24 identical keys
+    ctx = lkv.Context(lkv.make_config(cfg, kmeans_impl=1))
+    ctx.cluster_prompt(0, K, inp.V[0])
+    cen, sizes, first = ctx.get_units(0, 0, 0)
+    assert len(sizes) == 3 and sizes.min() >= 1 and sizes.sum() == 37
+    pos = ctx.get_unit_positions(0, 0, 0)
+    assert sorted(pos.tolist()) == list(range(16, 53))
+    ctx.close()
+
+
+# ------------------------------------------------------------------ full sizes (bench launch config)
+def test_c2_layer_full_size_sampled():
+    """One C2 retrieval layer + one full-cache layer at full size (32K prompt, 8 KV heads, g=4)
+    in the bench's launch configuration; clustering = planted labels (an oracle k-means at this
+    size is out of reach); 24 decode steps compared every step on every head."""
+    cfg = C2.replace(num_layers=2, full_cache_layers=(0,), decode_steps=24)
+    inp = make_inputs(cfg, 24, 0)
+    worst, n_flags, st = run_episode(cfg, inp, 24, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
+                                     compare_ws=False)
+    assert n_flags >= 3
+
+
+def test_c2_kmeans_full_size_properties():
+    lkv = _lkv()
+    cfg = C2.replace(num_layers=1, full_cache_layers=(), k_planted=512)
+    inp = make_inputs(cfg, 1, 0)
+    ctx = lkv.Context(lkv.make_config(cfg))
+    ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+    N, S, k = 32736, 32, 2046
+    Xall = np32(inp.K[0])[0]
+    for h in (0, 5):
+        a_g, C_g = _gpu_units(ctx, 0, 0, h, N, S)
+        cnt = np.bincount(a_g, minlength=k)
+        assert cnt.min() >= 1 and cnt.sum() == N
+        X = Xall[S:, h]
+        for j in np.random.default_rng(h).integers(0, k, 40):
+            ref = X[a_g == j].astype(np.float64).mean(0)
+            assert np.abs(C_g[j] - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1.0)
+    ctx.close()
