@@ -62,6 +62,8 @@ struct louiskv_ctx {
   int32_t* d_km_perm = nullptr;
   int32_t* d_km_flags = nullptr;
   StatsDev* d_stats = nullptr;
+  int* d_step = nullptr;   // [L] device decode-step counters (graph-replay safe)
+  int* d_error = nullptr;  // device capacity-overflow flag
   std::vector<void*> allocs;
   std::string err;
   bool sticky = false;
@@ -221,6 +223,8 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_km_perm, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
   ok = ok && dalloc(c, &c->d_km_flags, (size_t)nl);
   ok = ok && dalloc(c, &c->d_stats, 1);
+  ok = ok && dalloc(c, &c->d_step, (size_t)c->L);
+  ok = ok && dalloc(c, &c->d_error, 1);
   if (!ok) {
     louiskv_destroy(c);
     return LOUISKV_ERR_OOM_DEVICE;
@@ -266,6 +270,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, 0, sizeof(bf16) * c->Bmax * c->Hq * D, st),
              "memset q_ref");
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_flag + (size_t)layer * c->Bmax, 0, c->Bmax, st), "memset flag");
+  LKV_LAUNCH(c, cudaMemsetAsync(c->d_step + layer, 0, sizeof(int), st), "memset step");
   if (is_full(c, layer)) {
     if (h_assign) return fail(c, LOUISKV_ERR_INVALID_ARG, "set_prompt_units on a full-cache layer");
     LKV_LAUNCH(c,
@@ -370,19 +375,20 @@ louiskv_status louiskv_should_retrieve(louiskv_ctx* c, int32_t layer, const void
   uint8_t* flag = c->d_flag + (size_t)layer * c->Bmax;
   double* r = c->d_r + (size_t)layer * c->Bmax;
   if (is_full(c, layer)) {
-    LKV_LAUNCH(c, launch_copy_flags(nullptr, nullptr, flag, r, d_flag_out, d_r_out, c->batch, st), "flags");
+    LKV_LAUNCH(c, launch_copy_flags(nullptr, nullptr, flag, r, d_flag_out, d_r_out, c->batch, c->d_step + layer, st),
+               "flags");
   } else if (c->cfg.boundary_mode == LOUISKV_BOUNDARY_SHARED && layer != c->cfg.shared_layer) {
     const int sl = c->cfg.shared_layer;
     if (c->t[sl] < t) return fail(c, LOUISKV_ERR_STATE, "SHARED: designated layer not yet called this step");
     LKV_LAUNCH(c,
                launch_copy_flags(c->d_flag + (size_t)sl * c->Bmax, c->d_r + (size_t)sl * c->Bmax, flag, r, d_flag_out,
-                                 d_r_out, c->batch, st),
+                                 d_r_out, c->batch, c->d_step + layer, st),
                "flags");
   } else {
     LKV_LAUNCH(c,
                launch_trigger(reinterpret_cast<const bf16*>(q_all), stride_b, c->batch, c->Hq,
-                              c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, flag, r, d_flag_out, d_r_out, t,
-                              c->cfg.tau, c->cfg.trigger_ref, st),
+                              c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, flag, r, d_flag_out, d_r_out,
+                              c->d_step + layer, c->cfg.tau, c->cfg.trigger_ref, st),
                "trigger");
   }
   c->t[layer] = t;
@@ -436,13 +442,13 @@ louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* 
   if (c->stage[layer] != 1 && c->stage[layer] != 2)
     return fail(c, LOUISKV_ERR_STATE, "append_output must follow should_retrieve/retrieve");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int t = c->t[layer];
+
   if (is_full(c, layer)) {
     LKV_LAUNCH(c,
                launch_full_append(reinterpret_cast<const bf16*>(k_t), reinterpret_cast<const bf16*>(v_t), stride_b,
                                   c->batch, c->hn,
                                   c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D,
-                                  c->full_cap, c->P[layer] + t - 1, st),
+                                  c->full_cap, c->P[layer], c->d_step + layer, c->d_error, st),
                "full append");
   } else {
     const int64_t ib = inst_base(c, layer);
@@ -452,7 +458,7 @@ louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* 
     a.stride_b = stride_b;
     a.batch = c->batch;
     a.hn = c->hn;
-    a.t = t;
+    a.step = c->d_step + layer;
     a.W = c->W;
     a.max_open = c->max_open;
     a.ring_cap = c->ring_cap;
@@ -500,8 +506,9 @@ louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_
   if (is_full(c, layer)) {
     a.full = c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D;
     a.full_cap = c->full_cap;
-    a.full_rows = c->P[layer] + c->t[layer];
-    max_rows = a.full_rows;
+    a.full_P = c->P[layer];
+    a.step = c->d_step + layer;
+    max_rows = c->P[layer] + c->t[layer];
   } else {
     const int64_t ib = inst_base(c, layer);
     a.inst = c->d_inst + ib;
@@ -611,6 +618,11 @@ louiskv_status louiskv_get_stats(louiskv_ctx* c, louiskv_stats* out) {
   if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_stats");
   StatsDev sd;
   cudaMemcpy(&sd, c->d_stats, sizeof(sd), cudaMemcpyDeviceToHost);
+  int derr = 0;
+  cudaMemcpy(&derr, c->d_error, sizeof(int), cudaMemcpyDeviceToHost);
+  std::vector<InstState> is(std::max<int64_t>(c->n_inst, 1));
+  if (c->n_inst) cudaMemcpy(is.data(), c->d_inst, sizeof(InstState) * c->n_inst, cudaMemcpyDeviceToHost);
+  for (int64_t i = 0; i < c->n_inst; ++i) derr |= is[i].error;
   out->retrievals = sd.retrievals;
   out->units_scored = sd.units_scored;
   out->units_selected = sd.units_selected;
@@ -619,6 +631,7 @@ louiskv_status louiskv_get_stats(louiskv_ctx* c, louiskv_stats* out) {
   out->bytes_h2d = sd.bytes_h2d;
   out->bytes_d2h = sd.bytes_d2h;
   out->segments_evicted = sd.segments_evicted;
+  if (derr) return fail(c, LOUISKV_ERR_CAPACITY, "device capacity exceeded (host pool, unit table or full cache)");
   return LOUISKV_OK;
 }
 

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   const int tid = threadIdx.x;
   InstState* S = a.inst + li;
   const int flag = a.flag ? a.flag[b] : 0;
-  const int dec = a.t - 1;  // decode index of this token
+  const int dec = *a.step - 1;  // decode index of this token (device step counter)
   const int cap = a.ring_cap;
   int2* fifo = a.fifo + (int64_t)li * cap;
   bf16* ringK = a.ring + (int64_t)li * 2 * cap * D;
@@ -107,9 +107,14 @@ __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
 }
 
 __global__ void full_append_kernel(const bf16* k_t, const bf16* v_t, int64_t stride_b, int hn, bf16* full,
-                                   int64_t full_cap, int64_t pos) {
+                                   int64_t full_cap, int64_t P, const int* step, int* error) {
   const int li = blockIdx.x, b = li / hn, h = li % hn;
   const int tid = threadIdx.x;  // 32 threads
+  const int64_t pos = P + *step - 1;
+  if (pos >= full_cap) {
+    if (tid == 0) *error = 1;
+    return;
+  }
   bf16* K = full + (int64_t)li * 2 * full_cap * D;
   bf16* V = K + full_cap * D;
   const bf16* src = (tid < 16 ? k_t : v_t) + (int64_t)b * stride_b + (int64_t)h * D;
@@ -123,8 +128,8 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_full_append(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
-                               int64_t full_cap, int64_t pos, cudaStream_t st) {
-  full_append_kernel<<<batch * hn, 32, 0, st>>>(k_t, v_t, stride_b, hn, full, full_cap, pos);
+                               int64_t full_cap, int64_t P, const int* step, int* error, cudaStream_t st) {
+  full_append_kernel<<<batch * hn, 32, 0, st>>>(k_t, v_t, stride_b, hn, full, full_cap, P, step, error);
   return cudaGetLastError();
 }
 

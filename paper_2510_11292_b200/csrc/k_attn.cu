@@ -70,12 +70,13 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
   } else {
     sp.k0 = a.full + (int64_t)li * 2 * a.full_cap * D;
     sp.v0 = sp.k0 + a.full_cap * D;
-    sp.n0 = (int)a.full_rows;
+    const int64_t rows = a.full_P + *a.step;
+    n_rows = (int)(rows < a.full_cap ? rows : a.full_cap);
+    sp.n0 = n_rows;
     sp.n1 = 0;
     sp.k1 = sp.v1 = sp.k2 = sp.v2 = nullptr;
     sp.head = 0;
     sp.cap = 1;
-    n_rows = (int)a.full_rows;
   }
   const int r_begin = (int)((int64_t)n_rows * split / gridDim.y);
   const int r_end = (int)((int64_t)n_rows * (split + 1) / gridDim.y);

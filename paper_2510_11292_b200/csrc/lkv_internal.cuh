@@ -56,11 +56,13 @@ struct StatsDev {
 
 // ---------------------------------------------------------------- kernel launchers
 // trigger (k_trigger.cu)
+// Both kernels run as a single CTA and own the per-layer device step counter: they read
+// t = step[layer] + 1 and commit step[layer] = t at the end (graph-replay safe).
 cudaError_t launch_trigger(const bf16* q_all, int64_t stride_b, int batch, int Hq, bf16* q_ref, uint8_t* flag,
-                           double* r, uint8_t* flag_out, double* r_out, int t, double tau, int trigger_ref,
+                           double* r, uint8_t* flag_out, double* r_out, int* step, double tau, int trigger_ref,
                            cudaStream_t st);
 cudaError_t launch_copy_flags(const uint8_t* src_flag, const double* src_r, uint8_t* flag, double* r,
-                              uint8_t* flag_out, double* r_out, int batch, cudaStream_t st);
+                              uint8_t* flag_out, double* r_out, int batch, int* step, cudaStream_t st);
 
 // retrieve (k_retrieve.cu)
 struct RetrieveArgs {
@@ -94,7 +96,8 @@ struct AppendArgs {
   const bf16* k_t;
   const bf16* v_t;
   int64_t stride_b;
-  int batch, hn, t, W, max_open, ring_cap, Umax;
+  int batch, hn, W, max_open, ring_cap, Umax;
+  const int* step;      // device step counter of this layer (t, 1-based, already advanced)
   const uint8_t* flag;  // [batch]
   InstState* inst;
   bf16* ring;           // layer base [batch*hn][2][ring_cap][D]
@@ -113,7 +116,7 @@ struct AppendArgs {
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);
 cudaError_t launch_full_append(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
-                               int64_t full_cap, int64_t pos, cudaStream_t st);
+                               int64_t full_cap, int64_t P, const int* step, int* error, cudaStream_t st);
 
 // attention (k_attn.cu)
 struct AttnArgs {
@@ -133,7 +136,8 @@ struct AttnArgs {
   // full layers
   const bf16* full;       // [batch*hn][2][full_cap][D]
   int64_t full_cap;
-  int64_t full_rows;
+  int64_t full_P;         // rows = full_P + *step (capped at full_cap)
+  const int* step;
   // outputs
   bf16* out;
   float* out_f32;

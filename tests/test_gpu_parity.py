@@ -150,12 +150,12 @@ def test_episode_last_retrieval_and_shared_modes():
 
 
 def test_episode_degenerate_tau_budget_force_seal():
-    cfg = small_cfg(decode_steps=20, tau=1.01, budget_tokens=0)   # retrieve every step, empty budget
-    inp = make_inputs(cfg, 20, 4)
-    _, n_flags, st = run_episode(cfg, inp, 20, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
+    cfg = small_cfg(decode_steps=30, tau=1.01, budget_tokens=0)   # retrieve every step, empty budget
+    inp = make_inputs(cfg, 30, 4)
+    _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
     assert st["units_selected"] == 0
-    cfg = small_cfg(decode_steps=20, tau=-1.0)                      # only t == 1
-    _, n_flags, st = run_episode(cfg, inp, 20, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
+    cfg = small_cfg(decode_steps=30, tau=-1.0)                      # only t == 1
+    _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
     assert st["retrievals"] == cfg.batch * 2
     cfg = small_cfg(decode_steps=30, tau=-1.0, window_tokens=6)     # force-seal at max_open=3
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3)
