@@ -85,6 +85,8 @@ typedef struct {
   uint64_t bytes_h2d;         /* host-pool bytes read by the gather */
   uint64_t bytes_d2h;         /* bytes written to the host pool (prompt offload + evictions) */
   uint64_t segments_evicted;
+  uint64_t kmeans_tc_iters;   /* Lloyd assignment passes run on the tcgen05 kernel */
+  uint64_t kmeans_simt_iters; /* ... on the SIMT kernel (impl SIMT, or TMA-incompatible strides) */
 } louiskv_stats;
 
 /* Allocates every device buffer and the pinned, device-mapped host pool.

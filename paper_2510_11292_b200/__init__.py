@@ -52,7 +52,8 @@ class Config(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("retrievals", "units_scored", "units_selected", "units_reused",
-                                                "units_fetched", "bytes_h2d", "bytes_d2h", "segments_evicted")]
+                                                "units_fetched", "bytes_h2d", "bytes_d2h", "segments_evicted",
+                                                "kmeans_tc_iters", "kmeans_simt_iters")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

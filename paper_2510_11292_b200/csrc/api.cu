@@ -47,7 +47,7 @@ struct louiskv_ctx {
   int64_t pool_inst_bytes = 0;
   // scratch
   float* d_se = nullptr;
-  unsigned long long* d_skey = nullptr;
+  uint8_t* d_ssort = nullptr;
   GatherJob* d_jobs = nullptr;
   RowSrc* d_rows = nullptr;
   float* d_part = nullptr;
@@ -64,6 +64,7 @@ struct louiskv_ctx {
   StatsDev* d_stats = nullptr;
   int* d_step = nullptr;   // [L] device decode-step counters (graph-replay safe)
   int* d_error = nullptr;  // device capacity-overflow flag
+  uint64_t km_tc_iters = 0, km_simt_iters = 0;
   std::vector<void*> allocs;
   std::string err;
   bool sticky = false;
@@ -165,8 +166,9 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   c->Mmax = k.max_output_len;
   c->Nmax = std::max<int64_t>(0, c->Pmax - c->S);
   c->kmax = (int)((c->Nmax + c->c - 1) / c->c);
-  c->Umax = (int)std::min<int64_t>((int64_t)c->kmax + c->Mmax, 1ll << 16);
-  if ((int64_t)c->kmax + c->Mmax > (1ll << 16)) {  // 16-bit unit ids in the selection key
+  // unit-table rows padded to whole 256-row centroid tiles (the tcgen05 k-means TMA box)
+  c->Umax = (int)((((int64_t)c->kmax + c->Mmax) + 255) / 256 * 256);
+  if (c->Umax > (1 << 16) || k.budget_tokens > 65534) {  // 16-bit unit ids / sizes in the selection
     delete c;
     return LOUISKV_ERR_INVALID_ARG;
   }
@@ -209,12 +211,12 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_qref, (size_t)c->L * c->Bmax * c->Hq * D);
   ok = ok && dalloc(c, &c->d_full, (size_t)c->n_f * nl * 2 * c->full_cap * D);
   ok = ok && dalloc(c, &c->d_se, (size_t)nl * g * c->Umax);
-  ok = ok && dalloc(c, &c->d_skey, (size_t)nl * c->Umax);
+  ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 14);
   ok = ok && dalloc(c, &c->d_jobs, (size_t)nl);
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
   ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
   ok = ok && dalloc(c, &c->d_counters, (size_t)nl);
-  ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * std::max(c->kmax, 1));
+  ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * (((std::max(c->kmax, 1) + 255) / 256) * 256));
   ok = ok && dalloc(c, &c->d_km_assign, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
   ok = ok && dalloc(c, &c->d_km_dmin, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
   ok = ok && dalloc(c, &c->d_km_cc, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
@@ -311,6 +313,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.S_cap = c->S;
   a.inst = c->d_inst + ib;
   a.half = c->d_km_half;
+  a.hstride = ((std::max(c->kmax, 1) + 255) / 256) * 256;
   a.assign = c->d_km_assign;
   a.dmin = c->d_km_dmin;
   a.cc = c->d_km_cc;
@@ -337,7 +340,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
     a.ext_assign = d_ea;
     a.ext_cent = d_ec;
   }
-  cudaError_t e = run_kmeans_prompt(a, st);
+  cudaError_t e = run_kmeans_prompt(a, st, &c->km_tc_iters, &c->km_simt_iters);
   if (h_assign) {
     cudaStreamSynchronize(st);
     cudaFree(d_ea);
@@ -426,7 +429,7 @@ louiskv_status louiskv_retrieve(louiskv_ctx* c, int32_t layer, const void* q_own
   a.ws_inst_stride = c->ws_inst_stride;
   a.inst_global_base = ib;
   a.scratch_e = c->d_se;
-  a.scratch_key = c->d_skey;
+  a.scratch_sort = c->d_ssort;
   a.jobs = c->d_jobs;
   a.rows = c->d_rows;
   a.stats = c->d_stats;
@@ -631,6 +634,8 @@ louiskv_status louiskv_get_stats(louiskv_ctx* c, louiskv_stats* out) {
   out->bytes_h2d = sd.bytes_h2d;
   out->bytes_d2h = sd.bytes_d2h;
   out->segments_evicted = sd.segments_evicted;
+  out->kmeans_tc_iters = c->km_tc_iters;
+  out->kmeans_simt_iters = c->km_simt_iters;
   if (derr) return fail(c, LOUISKV_ERR_CAPACITY, "device capacity exceeded (host pool, unit table or full cache)");
   return LOUISKV_OK;
 }

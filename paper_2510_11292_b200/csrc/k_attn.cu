@@ -11,9 +11,8 @@
 
 namespace lkv {
 
-constexpr int AT_THREADS = 128;
+constexpr int AT_THREADS = 256;
 constexpr int AT_HW = AT_THREADS / 16;  // half-warps per CTA
-constexpr int AT_MAXG = 8;
 
 struct RowSpan {
   const bf16* k0;  // sinks
@@ -100,77 +99,122 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
     for (int k = 0; k < 8; ++k) acc[j][k] = 0.f;
   }
 
-  // warp-uniform loop: each warp takes 4 consecutive rows per iteration (2 per half-warp),
-  // so both half-warps always execute the same shuffles.
+  // warp-uniform loop: each half-warp takes 4 rows per iteration (8 x 16-B loads in flight per
+  // lane), then one block-wise online-softmax update for the 4 rows.
   const int warp = tid >> 5, half = hw & 1;
   constexpr int NWARP = AT_THREADS / 32;
-  for (int base = r_begin + warp * 4; base < r_end; base += 4 * NWARP) {
-    const int ra = base + half, rb = base + 2 + half;
-    const bool va = ra < r_end, vb = rb < r_end;
-    uint4 ku0 = make_uint4(0, 0, 0, 0), vu0 = ku0, ku1 = ku0, vu1 = ku0;
-    const uint4 *kp, *vp;
-    if (va) {
-      row_ptrs(sp, ra, kp, vp);
-      ku0 = __ldg(kp + sub);
-      vu0 = __ldg(vp + sub);
-    }
-    if (vb) {
-      row_ptrs(sp, rb, kp, vp);
-      ku1 = __ldg(kp + sub);
-      vu1 = __ldg(vp + sub);
-    }
+  constexpr int RB = 4;
+  for (int base = r_begin + warp * (2 * RB); base < r_end; base += 2 * RB * NWARP) {
+    uint4 ku[RB], vu[RB];
+    bool valid[RB];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const bool valid = rr ? vb : va;
-      float kf[8], vf[8];
-      unpack8(rr ? ku1 : ku0, kf);
-      unpack8(rr ? vu1 : vu0, vf);
+    for (int i = 0; i < RB; ++i) {
+      const int r = base + half + 2 * i;
+      valid[i] = r < r_end;
+      ku[i] = make_uint4(0, 0, 0, 0);
+      vu[i] = ku[i];
+      if (valid[i]) {
+        const uint4 *kp, *vp;
+        row_ptrs(sp, r, kp, vp);
+        ku[i] = __ldg(kp + sub);
+        vu[i] = __ldg(vp + sub);
+      }
+    }
+    float s[RB][G];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      float kf[8];
+      unpack8(ku[i], kf);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        float s = 0.f;
+        float t = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) s = fmaf(q[j][k], kf[k], s);
-        s += __shfl_xor_sync(0xffffffffu, s, 8);
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        if (valid) {
-          const float mn = fmaxf(m[j], s);
-          const float corr = exp2f(m[j] - mn);
-          const float p = exp2f(s - mn);
-          l[j] = l[j] * corr + p;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[j][k] = fmaf(acc[j][k], corr, p * vf[k]);
-          m[j] = mn;
-        }
+        for (int k = 0; k < 8; ++k) t = fmaf(q[j][k], kf[k], t);
+        s[i][j] = t;
       }
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        float t = s[i][j];
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        s[i][j] = valid[i] ? t : -INFINITY;
+      }
+    float vf[RB][8];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) unpack8(vu[i], vf[i]);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      float mb = m[j];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) mb = fmaxf(mb, s[i][j]);
+      if (mb == -INFINITY) continue;  // no valid row yet for this half-warp
+      const float corr = exp2f(m[j] - mb);
+      float p[RB], ps = 0.f;
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        p[i] = exp2f(s[i][j] - mb);
+        ps += p[i];
+      }
+      l[j] = fmaf(l[j], corr, ps);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float t = acc[j][k] * corr;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) t = fmaf(p[i], vf[i][k], t);
+        acc[j][k] = t;
+      }
+      m[j] = mb;
     }
   }
 
-  // ---- merge half-warps through shared memory
-  __shared__ float s_m[AT_HW][G], s_l[AT_HW][G];
-  __shared__ float s_acc[AT_HW][G][D];
-  if (sub == 0) {
+  // ---- merge the two half-warps of each warp (lane ^ 16 holds the same dims), then the warps
+  // through shared memory
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      s_m[hw][j] = m[j];
-      s_l[hw][j] = l[j];
+  for (int j = 0; j < G; ++j) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m[j], 16);
+    const float lo = __shfl_xor_sync(0xffffffffu, l[j], 16);
+    const float M = fmaxf(m[j], mo);
+    const float sa = M == -INFINITY ? 0.f : exp2f(m[j] - M);
+    const float sb = M == -INFINITY ? 0.f : exp2f(mo - M);
+    l[j] = l[j] * sa + lo * sb;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float ao = __shfl_xor_sync(0xffffffffu, acc[j][k], 16);
+      acc[j][k] = acc[j][k] * sa + ao * sb;
     }
+    m[j] = M;
   }
+  constexpr int AT_W = AT_THREADS / 32;
+  __shared__ float s_m[AT_W][G], s_l[AT_W][G];
+  __shared__ float s_acc[AT_W][G][D];
+  if ((tid & 31) < 16) {
+    if (sub == 0) {
 #pragma unroll
-  for (int j = 0; j < G; ++j)
+      for (int j = 0; j < G; ++j) {
+        s_m[warp][j] = m[j];
+        s_l[warp][j] = l[j];
+      }
+    }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s_acc[hw][j][sub * 8 + k] = acc[j][k];
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_acc[warp][j][sub * 8 + k] = acc[j][k];
+  }
   __syncthreads();
 
   float* part = a.part + ((int64_t)li * gridDim.y + split) * G * (D + 2);
   for (int idx = tid; idx < G * D; idx += AT_THREADS) {
     const int j = idx / D, e = idx % D;
     float M = -INFINITY;
-    for (int w = 0; w < AT_HW; ++w) M = fmaxf(M, s_m[w][j]);
+    for (int w = 0; w < AT_W; ++w) M = fmaxf(M, s_m[w][j]);
     float Lsum = 0.f, A = 0.f;
     if (M != -INFINITY) {
-      for (int w = 0; w < AT_HW; ++w) {
+      for (int w = 0; w < AT_W; ++w) {
         const float sc = exp2f(s_m[w][j] - M);
         Lsum += s_l[w][j] * sc;
         A += s_acc[w][j][e] * sc;
@@ -195,22 +239,31 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
   if (!s_last) return;
   __threadfence();
   const float* P0 = a.part + (int64_t)li * gridDim.y * G * (D + 2);
+  const int Y = gridDim.y;
+  __shared__ float s_w[64][G];  // per-split weights exp2(m_y - M) / L
+  if (tid < G) {
+    const int j = tid;
+    float M = -INFINITY;
+    for (int y = 0; y < Y; ++y) M = fmaxf(M, __ldcg(P0 + (y * G + j) * (D + 2) + D));
+    float Lsum = 0.f;
+    for (int y = 0; y < Y; ++y) {
+      const float my = __ldcg(P0 + (y * G + j) * (D + 2) + D);
+      const float w = my == -INFINITY ? 0.f : exp2f(my - M);
+      s_w[y][j] = w;
+      Lsum += w * __ldcg(P0 + (y * G + j) * (D + 2) + D + 1);
+    }
+    const float inv = 1.f / Lsum;
+    for (int y = 0; y < Y; ++y) s_w[y][j] *= inv;
+  }
+  __syncthreads();
   for (int idx = tid; idx < G * D; idx += AT_THREADS) {
     const int j = idx / D, e = idx % D;
-    float M = -INFINITY;
-    for (int y = 0; y < (int)gridDim.y; ++y) M = fmaxf(M, __ldcg(P0 + (y * G + j) * (D + 2) + D));
-    float Lsum = 0.f, A = 0.f;
-    for (int y = 0; y < (int)gridDim.y; ++y) {
-      const float my = __ldcg(P0 + (y * G + j) * (D + 2) + D);
-      if (my == -INFINITY) continue;
-      const float sc = exp2f(my - M);
-      Lsum += __ldcg(P0 + (y * G + j) * (D + 2) + D + 1) * sc;
-      A += __ldcg(P0 + (y * G + j) * (D + 2) + e) * sc;
-    }
-    const float o = A / Lsum;
+    float A = 0.f;
+#pragma unroll 4
+    for (int y = 0; y < Y; ++y) A = fmaf(s_w[y][j], __ldcg(P0 + (y * G + j) * (D + 2) + e), A);
     const int64_t oi = ((int64_t)(b * a.hn + h) * G + j) * D + e;
-    a.out[oi] = __float2bfloat16_rn(o);
-    if (a.out_f32) a.out_f32[oi] = o;
+    a.out[oi] = __float2bfloat16_rn(A);
+    if (a.out_f32) a.out_f32[oi] = A;
   }
   if (tid == 0) a.counters[li] = 0;
 }

@@ -50,7 +50,13 @@ __global__ void km_init_kernel(KmArgs a) {
     ss = fmaf(c[e], c[e], ss);
   }
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) a.half[(int64_t)li * a.kmax + j] = 0.5f * ss;
+  if (lane == 0) a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+}
+
+// ---- +inf half-norms for the padded centroid columns [kc, hstride) (masked in the argmax)
+__global__ void km_half_pad_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  for (int j = a.kc + threadIdx.x; j < a.hstride; j += blockDim.x) a.half[(int64_t)li * a.hstride + j] = INFINITY;
 }
 
 // ---- SIMT assignment (correctness reference path; the tcgen05 kernel is the fast path)
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(128) km_assign_simt_kernel(KmArgs a) {
   float best = -INFINITY;
   int bi = 0;
   const uint32_t* Cb = reinterpret_cast<const uint32_t*>(a.centb + (int64_t)li * a.Umax * D);
-  const float* half = a.half + (int64_t)li * a.kmax;
+  const float* half = a.half + (int64_t)li * a.hstride;
   for (int j0 = 0; j0 < a.kc; j0 += AS_TILE) {
     __syncthreads();
     for (int t = threadIdx.x; t < AS_TILE * D / 2; t += 128) {
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
     ss = fmaf(c, c, ss);
   }
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) a.half[(int64_t)li * a.kmax + j] = 0.5f * ss;
+  if (lane == 0) a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
 }
 
 // caller-supplied clustering: copy assignment and centroids in
@@ -384,7 +390,7 @@ static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool rep
   return cudaGetLastError();
 }
 
-cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st) {
+cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_iters, uint64_t* simt_iters) {
   const int ni = a.batch * a.hn;
   const int P = a.S + a.N;
   const int s_eff = min(a.S_cap, P);
@@ -407,12 +413,17 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st) {
     if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
   } else {
     km_init_kernel<<<gk, 128, 0, st>>>(a);
+    km_half_pad_kernel<<<dim3(1, ni), 256, 0, st>>>(a);
     for (int it = 0; it < a.iters; ++it) {
+      bool done = false;
       if (a.impl == LOUISKV_KMEANS_TC && kmeans_tc_available()) {
-        if ((e = launch_assign_tc(a, st)) != cudaSuccess) return e;
-      } else {
-        km_assign_simt_kernel<<<dim3((a.N + 127) / 128, ni), 128, 0, st>>>(a);
+        e = launch_assign_tc(a, st);
+        if (e == cudaSuccess) done = true;
+        else if (e != cudaErrorNotSupported) return e;
+        else cudaGetLastError();
       }
+      if (!done) km_assign_simt_kernel<<<dim3((a.N + 127) / 128, ni), 128, 0, st>>>(a);
+      ++*(done ? tc_iters : simt_iters);
       if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
       km_update_kernel<<<gk, 128, 0, st>>>(a);
     }

@@ -22,7 +22,8 @@
 namespace lkv {
 
 constexpr int SS_THREADS = 512;
-constexpr int MAX_G = 16;
+constexpr int SS_WARPS = SS_THREADS / 32;
+constexpr int SORT_CAP = 12288;  // units whose sort buffers live in shared memory (else global scratch)
 
 __device__ __forceinline__ float exp_r3(float x, const float* c) {
   const float log2e = __double2float_rn(1.4426950408889634074);
@@ -45,33 +46,104 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
   return ((unsigned long long)hi << 32) | lo;
 }
 
-__global__ void __launch_bounds__(SS_THREADS) score_select_kernel(RetrieveArgs a) {
-  const int li = blockIdx.x;  // local instance = b*hn + h
+// ---- logits (recipe R2 step 1): one thread per unit, all g heads; spread over many CTAs
+template <int G>
+__global__ void __launch_bounds__(128) logits_kernel(RetrieveArgs a) {
+  const int li = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
+  if (!a.flag[b]) return;
+  const int n = a.inst[li].n_units;
+  if ((int)blockIdx.x * 128 >= n) return;
+  __shared__ float sq[G][D];
+  const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)h * G * D;
+  for (int i = threadIdx.x; i < G * D; i += 128) sq[i / D][i % D] = bf2f(qb[i]);
+  __syncthreads();
+  const int u = blockIdx.x * 128 + threadIdx.x;
+  if (u >= n) return;
+  const uint4* row = reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D);
+  uint4 cr[D / 8];
+#pragma unroll
+  for (int c8 = 0; c8 < D / 8; ++c8) cr[c8] = __ldg(row + c8);
+  float acc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) acc[j] = 0.0f;
+#pragma unroll
+  for (int c8 = 0; c8 < D / 8; ++c8) {
+    float cf[8];
+    unpack8(cr[c8], cf);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < G; ++j) acc[j] = __fmaf_rn(sq[j][c8 * 8 + k], cf[k], acc[j]);
+  }
+  const float inv_sqrt_d = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn((double)D)));
+  float* E = a.scratch_e + (int64_t)li * G * a.Umax;
+#pragma unroll
+  for (int j = 0; j < G; ++j) E[(int64_t)j * a.Umax + u] = __fmul_rn(acc[j], inv_sqrt_d);
+}
+
+// block-wide exclusive scan of one int per thread (512 threads); returns the exclusive prefix
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < SS_WARPS ? s_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < SS_WARPS) s_warp[lane] = wi - w;
+    if (lane == SS_WARPS - 1) s_warp[SS_WARPS] = wi;
+  }
+  __syncthreads();
+  const int r = s_warp[warp] + incl - v;
+  total = s_warp[SS_WARPS];
+  __syncthreads();
+  return r;
+}
+
+// ---- group scores, sort, budgeted greedy, working-set layout: one CTA per flagged instance
+template <int G>
+__global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
+  const int li = blockIdx.x;
+  const int b = li / a.hn;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = SS_THREADS / 32;
   if (!a.flag[b]) {
     if (tid == 0) a.jobs[li].n_rows = 0;
     return;
   }
   InstState* S = a.inst + li;
   const int n = S->n_units;
-  const int g = a.g;
 
-  __shared__ float sq[MAX_G][D];
   __shared__ float s_coef[7];
-  __shared__ float s_red[NW][MAX_G];
-  __shared__ float s_m[MAX_G];
-  __shared__ unsigned long long s_z[MAX_G];
-  __shared__ float s_Z[MAX_G];
-  __shared__ int s_hist[256];
-  __shared__ long long s_red64[NW];
-  __shared__ unsigned long long s_prefix;
-  __shared__ int s_need;
-  __shared__ int s_scan[SS_THREADS];
-  extern __shared__ uint32_t s_taken[];  // bitmap [ceil(Umax/32)]
+  __shared__ float s_red[SS_WARPS][G];
+  __shared__ float s_m[G];
+  __shared__ unsigned long long s_z[G];
+  __shared__ float s_Z[G];
+  __shared__ int s_cnt[SS_WARPS][256];
+  __shared__ int s_warp[SS_WARPS + 1];
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_taken = s_dyn;  // bitmap [ceil(Umax/32)]
+  // sort buffers (shared memory when n <= SORT_CAP, else this instance's global scratch)
+  uint8_t* sb = reinterpret_cast<uint8_t*>(s_dyn + (a.Umax + 31) / 32);
+  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
+  if (n > cap) sb = a.scratch_sort + (int64_t)li * a.Umax * 14;
+  const int m_ = n > cap ? a.Umax : cap;
+  uint32_t* kA = reinterpret_cast<uint32_t*>(sb);
+  uint32_t* kB = kA + m_;
+  uint16_t* vA = reinterpret_cast<uint16_t*>(kB + m_);
+  uint16_t* vB = vA + m_;
+  uint16_t* s_sz = vB + m_;
 
-  // recipe constants (identical IEEE double evaluation on both sides)
   if (tid == 0) {
     double p = 1.0, fact = 1.0;
     const double ln2 = 0.6931471805599453094;
@@ -83,214 +155,182 @@ __global__ void __launch_bounds__(SS_THREADS) score_select_kernel(RetrieveArgs a
       s_coef[i] = __double2float_rn(__ddiv_rn(p, fact));
     }
   }
-  const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)h * g * D;
-  for (int i = tid; i < g * D; i += SS_THREADS) sq[i / D][i % D] = bf2f(qb[i]);
   for (int i = tid; i < (a.Umax + 31) / 32; i += SS_THREADS) s_taken[i] = 0u;
-  if (tid < MAX_G) s_z[tid] = 0ull;
-  __syncthreads();
-
-  const float inv_sqrt_d = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn((double)D)));
-  float* E = a.scratch_e + (int64_t)li * g * a.Umax;
-  unsigned long long* KEY = a.scratch_key + (int64_t)li * a.Umax;
-  const uint4* C = reinterpret_cast<const uint4*>(a.centb + (int64_t)li * a.Umax * D);
+  if (tid < G) s_z[tid] = 0ull;
+  float* E = a.scratch_e + (int64_t)li * G * a.Umax;
   const int32_t* usize = a.usize + (int64_t)li * a.Umax;
 
-  // ---- 1. logits + per-head max
-  float mymax[MAX_G];
+  // ---- max of the logits per head (exact, order independent)
+  float mymax[G];
 #pragma unroll
-  for (int j = 0; j < MAX_G; ++j) mymax[j] = -INFINITY;
-  for (int u = tid; u < n; u += SS_THREADS) {
-    float acc[MAX_G];
+  for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
+  for (int u = tid; u < n; u += SS_THREADS)
 #pragma unroll
-    for (int j = 0; j < MAX_G; ++j) acc[j] = 0.0f;
-    const uint4* row = C + (int64_t)u * (D / 8);
-#pragma unroll 2
-    for (int c8 = 0; c8 < D / 8; ++c8) {
-      float cf[8];
-      unpack8(__ldg(row + c8), cf);
+    for (int j = 0; j < G; ++j) mymax[j] = fmaxf(mymax[j], E[(int64_t)j * a.Umax + u]);
 #pragma unroll
-      for (int j = 0; j < MAX_G; ++j) {
-        if (j < g) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[j] = __fmaf_rn(sq[j][c8 * 8 + k], cf[k], acc[j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < MAX_G; ++j) {
-      if (j < g) {
-        float l = __fmul_rn(acc[j], inv_sqrt_d);
-        E[(int64_t)j * a.Umax + u] = l;
-        mymax[j] = fmaxf(mymax[j], l);
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < MAX_G; ++j) {
-    if (j < g) {
-      float m = mymax[j];
-      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) s_red[warp][j] = m;
-    }
+  for (int j = 0; j < G; ++j) {
+    float m = mymax[j];
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_red[warp][j] = m;
   }
   __syncthreads();
-  if (tid < g) {
+  if (tid < G) {
     float m = -INFINITY;
-    for (int w = 0; w < NW; ++w) m = fmaxf(m, s_red[w][tid]);
+    for (int w = 0; w < SS_WARPS; ++w) m = fmaxf(m, s_red[w][tid]);
     s_m[tid] = m;
   }
   __syncthreads();
 
-  // ---- 2. exp + exact fixed-point normaliser
-  unsigned long long zl[MAX_G];
+  // ---- exp + exact fixed-point normaliser (recipe R2/R3)
+  unsigned long long zl[G];
 #pragma unroll
-  for (int j = 0; j < MAX_G; ++j) zl[j] = 0ull;
+  for (int j = 0; j < G; ++j) zl[j] = 0ull;
   for (int u = tid; u < n; u += SS_THREADS) {
 #pragma unroll
-    for (int j = 0; j < MAX_G; ++j) {
-      if (j < g) {
-        float e = exp_r3(__fsub_rn(E[(int64_t)j * a.Umax + u], s_m[j]), s_coef);
-        E[(int64_t)j * a.Umax + u] = e;
-        zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
-      }
+    for (int j = 0; j < G; ++j) {
+      const float e = exp_r3(__fsub_rn(E[(int64_t)j * a.Umax + u], s_m[j]), s_coef);
+      E[(int64_t)j * a.Umax + u] = e;
+      zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
     }
   }
 #pragma unroll
-  for (int j = 0; j < MAX_G; ++j) {
-    if (j < g) {
-      unsigned long long z = zl[j];
-      for (int o = 16; o; o >>= 1) z += shfl_xor_u64(z, o);
-      if (lane == 0) atomicAdd(&s_z[j], z);
-    }
+  for (int j = 0; j < G; ++j) {
+    unsigned long long z = zl[j];
+    for (int o = 16; o; o >>= 1) z += shfl_xor_u64(z, o);
+    if (lane == 0) atomicAdd(&s_z[j], z);
   }
   __syncthreads();
-  if (tid < g) s_Z[tid] = __fmul_rn(__ull2float_rn(s_z[tid]), __int_as_float((127 - 40) << 23));
+  if (tid < G) s_Z[tid] = __fmul_rn(__ull2float_rn(s_z[tid]), __int_as_float((127 - 40) << 23));
   __syncthreads();
 
-  // ---- 3. group score and sort key
+  // ---- A_u and the sort key ~bits(A_u); values = unit ids in ascending order (stable sort ->
+  // ties keep the lower id first); sizes clamped to 16 bits (B <= 65534: a clamped unit never fits)
   for (int u = tid; u < n; u += SS_THREADS) {
     float A = 0.0f;
-    for (int j = 0; j < g; ++j) A = __fadd_rn(A, __fdiv_rn(E[(int64_t)j * a.Umax + u], s_Z[j]));
-    A = __fdiv_rn(A, (float)g);
-    unsigned long long key = ((unsigned long long)(~__float_as_uint(A)) << 16) | (unsigned)u;
-    KEY[u] = key;
+#pragma unroll
+    for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[(int64_t)j * a.Umax + u], s_Z[j]));
+    A = __fdiv_rn(A, (float)G);
+    kA[u] = ~__float_as_uint(A);
+    vA[u] = (uint16_t)u;
+    const int sz = usize[u];
+    s_sz[u] = (uint16_t)(sz > 0xFFFF ? 0xFFFF : sz);
   }
   __syncthreads();
 
-  // ---- 4. budgeted greedy selection via weighted radix-select rounds
-  int rem = a.budget;
-  bool lo_valid = false;
-  unsigned long long lo = 0ull;
-  while (rem > 0 && n > 0) {
-    // total candidate weight
-    long long tot = 0;
-    for (int u = tid; u < n; u += SS_THREADS) {
-      unsigned long long k = KEY[u];
-      int sz = usize[u];
-      if ((!lo_valid || k > lo) && sz <= rem) tot += sz;
-    }
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0) s_red64[warp] = tot;
-    __syncthreads();
-    if (tid == 0) {
-      long long t2 = 0;
-      for (int w = 0; w < NW; ++w) t2 += s_red64[w];
-      s_red64[0] = t2;
-    }
-    __syncthreads();
-    tot = s_red64[0];
-    __syncthreads();
-    if (tot <= rem) {
-      for (int u = tid; u < n; u += SS_THREADS) {
-        unsigned long long k = KEY[u];
-        if ((!lo_valid || k > lo) && usize[u] <= rem) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
+  // ---- stable LSD radix sort of (key, id), 4 passes of 8 bits; warp w owns a contiguous chunk
+  {
+    const int chunk = (((n + 31) / 32 + SS_WARPS - 1) / SS_WARPS) * 32;
+    const int c0 = warp * chunk, c1 = min(n, c0 + chunk);
+    uint32_t *kin = kA, *kout = kB;
+    uint16_t *vin = vA, *vout = vB;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 8 * pass;
+      for (int i = tid; i < SS_WARPS * 256; i += SS_THREADS) (&s_cnt[0][0])[i] = 0;
+      __syncthreads();
+      for (int r0 = c0; r0 < c1; r0 += 32) {
+        const int i = r0 + lane;
+        const int d = i < c1 ? (int)((kin[i] >> shift) & 255u) : 256 + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (i < c1 && lane == __ffs(peers) - 1) s_cnt[warp][d] += __popc(peers);
+        __syncwarp();
       }
       __syncthreads();
-      break;
-    }
-    if (tid == 0) {
-      s_prefix = 0ull;
-      s_need = rem;
-    }
-    __syncthreads();
-    for (int pass = 0; pass < 6; ++pass) {
-      const int shift = 40 - 8 * pass;
-      const unsigned long long hi_mask = (pass == 0) ? 0ull : (~0ull << (shift + 8)) & 0xFFFFFFFFFFFFull;
-      for (int i = tid; i < 256; i += SS_THREADS) s_hist[i] = 0;
-      __syncthreads();
-      const unsigned long long prefix = s_prefix;
-      for (int u = tid; u < n; u += SS_THREADS) {
-        unsigned long long k = KEY[u];
-        int sz = usize[u];
-        if ((!lo_valid || k > lo) && sz <= rem && (k & hi_mask) == prefix)
-          atomicAdd(&s_hist[(k >> shift) & 255], sz);
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // bucket with cumulative weight > need; lane handles 8 consecutive buckets
-        int v[8], ls = 0;
+      // exclusive offsets in (digit, warp) order: thread t owns digit t/2, warps (t%2)*8 .. +8
+      {
+        const int d = tid >> 1, w0 = (tid & 1) * (SS_WARPS / 2);
+        int v[SS_WARPS / 2], loc = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v[i] = s_hist[lane * 8 + i];
-          ls += v[i];
+        for (int w = 0; w < SS_WARPS / 2; ++w) {
+          v[w] = s_cnt[w0 + w][d];
+          loc += v[w];
         }
-        int incl = ls;
+        int total;
+        int run = block_excl_scan(loc, s_warp, total);
+#pragma unroll
+        for (int w = 0; w < SS_WARPS / 2; ++w) {
+          s_cnt[w0 + w][d] = run;
+          run += v[w];
+        }
+      }
+      __syncthreads();
+      for (int r0 = c0; r0 < c1; r0 += 32) {
+        const int i = r0 + lane;
+        const bool valid = i < c1;
+        const uint32_t k = valid ? kin[i] : 0u;
+        const int d = valid ? (int)((k >> shift) & 255u) : 256 + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (valid) base = s_cnt[warp][d];
+        __syncwarp();
+        if (valid) {
+          const int pos = base + __popc(peers & ((1u << lane) - 1u));
+          kout[pos] = k;
+          vout[pos] = vin[i];
+          if (lane == leader) s_cnt[warp][d] = base + __popc(peers);
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      uint32_t* tk = kin;
+      kin = kout;
+      kout = tk;
+      uint16_t* tv = vin;
+      vin = vout;
+      vout = tv;
+    }
+    // after 4 passes the sorted data is back in (kA, vA)
+  }
+
+  // ---- greedy skip-and-continue in sorted order (single warp): take u iff size_u <= remaining
+  if (warp == 0) {
+    int rem = a.budget;
+    for (int c = 0; c < n && rem > 0; c += 32) {
+      const int i = c + lane;
+      int u = 0, sz = 0x7FFFFFFF;
+      if (i < n) {
+        u = vA[i];
+        sz = s_sz[u];
+      }
+      bool pending = i < n;
+      while (true) {
+        const bool cand = pending && sz <= rem;
+        const unsigned cm = __ballot_sync(0xffffffffu, cand);
+        if (cm == 0u) break;
+        int incl = cand ? sz : 0;
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += y;
         }
-        int excl = incl - ls;
-        const int need = s_need;
-        unsigned hit = __ballot_sync(0xffffffffu, incl > need);
-        int first = __ffs(hit) - 1;  // lane containing the bucket (always exists: tot > rem)
-        if (lane == first) {
-          int cum = excl, bk = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (cum + v[i] > need) {
-              bk = i;
-              break;
-            }
-            cum += v[i];
-          }
-          s_need = need - cum;
-          s_prefix = prefix | ((unsigned long long)(lane * 8 + bk) << shift);
+        const unsigned over = __ballot_sync(0xffffffffu, cand && incl > rem);
+        if (over == 0u) {
+          if (cand) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
+          rem -= __shfl_sync(0xffffffffu, incl, 31);
+          break;
         }
+        const int first = __ffs(over) - 1;
+        const int before = __shfl_sync(0xffffffffu, incl, first > 0 ? first - 1 : 0);
+        if (cand && lane < first) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
+        rem -= first > 0 ? before : 0;
+        pending = pending && lane > first;
       }
-      __syncthreads();
     }
-    const unsigned long long pivot = s_prefix;
-    for (int u = tid; u < n; u += SS_THREADS) {
-      unsigned long long k = KEY[u];
-      if ((!lo_valid || k > lo) && usize[u] <= rem && k < pivot) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
-    }
-    rem = s_need;
-    lo = pivot;
-    lo_valid = true;
-    __syncthreads();
   }
   __syncthreads();
 
-  // ---- 5. layout of the new working set (id order) + row sources
+  // ---- layout of the new working set (selected units in id order) + row sources; diff with the
+  // previous selection: kept units are copied device->device, new ones read from the host pool
   const int per = (n + SS_THREADS - 1) / SS_THREADS;
   const int u0 = tid * per, u1 = min(n, u0 + per);
   int local = 0, local_cnt = 0;
   for (int u = u0; u < u1; ++u)
     if (s_taken[u >> 5] >> (u & 31) & 1u) {
-      local += usize[u];
+      local += s_sz[u];
       ++local_cnt;
     }
-  s_scan[tid] = local;
-  __syncthreads();
-  // Hillis-Steele inclusive scan
-  for (int o = 1; o < SS_THREADS; o <<= 1) {
-    int y = tid >= o ? s_scan[tid - o] : 0;
-    __syncthreads();
-    s_scan[tid] += y;
-    __syncthreads();
-  }
-  const int total = s_scan[SS_THREADS - 1];
-  int dst = s_scan[tid] - local;
+  int total;
+  int dst = block_excl_scan(local, s_warp, total);
 
   const int cur = S->ws_cur, nxt = cur ^ 1;
   const int64_t gi = a.inst_global_base + li;
@@ -308,7 +348,7 @@ __global__ void __launch_bounds__(SS_THREADS) score_select_kernel(RetrieveArgs a
     const bool take = s_taken[u >> 5] >> (u & 31) & 1u;
     const bool had = sel[u] != 0;
     if (take) {
-      const int sz = usize[u];
+      const int sz = s_sz[u];
       if (had) {
         const int so = seloff[u];
         for (int i = 0; i < sz; ++i)
@@ -330,23 +370,21 @@ __global__ void __launch_bounds__(SS_THREADS) score_select_kernel(RetrieveArgs a
       sel[u] = 0;
     }
   }
-  // stats (warp-aggregated)
   for (int o = 16; o; o >>= 1) {
     reused += __shfl_xor_sync(0xffffffffu, reused, o);
     fetched += __shfl_xor_sync(0xffffffffu, fetched, o);
     hbytes += __shfl_xor_sync(0xffffffffu, hbytes, o);
+    local_cnt += __shfl_xor_sync(0xffffffffu, local_cnt, o);
   }
   if (lane == 0 && (reused | fetched)) {
     atomicAdd(&a.stats->units_reused, reused);
     atomicAdd(&a.stats->units_fetched, fetched);
     atomicAdd(&a.stats->bytes_h2d, hbytes);
+    atomicAdd(&a.stats->units_selected, (unsigned long long)local_cnt);
   }
-  int cnt = local_cnt;
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0 && cnt) atomicAdd(&a.stats->units_selected, (unsigned long long)cnt);
   if (tid == 0) {
     atomicAdd(&a.stats->units_scored, (unsigned long long)n);
-    if (h == 0) atomicAdd(&a.stats->retrievals, 1ull);
+    if (li % a.hn == 0) atomicAdd(&a.stats->retrievals, 1ull);
     a.jobs[li] = GatherJob{total, 0, nxtK, nxtV};
     S->ws_cur = nxt;
     S->ws_rows = total;
@@ -387,16 +425,29 @@ __global__ void __launch_bounds__(GA_THREADS) gather_kernel(const GatherJob* __r
   }
 }
 
-cudaError_t launch_score_select(const RetrieveArgs& a, cudaStream_t st) {
-  if (a.g > MAX_G) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr_set = true;
+template <int G>
+static cudaError_t launch_retrieve_g(const RetrieveArgs& a, cudaStream_t st) {
+  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
+  const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32) + 14ull * cap;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(select_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
   }
-  score_select_kernel<<<a.batch * a.hn, SS_THREADS, smem, st>>>(a);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  logits_kernel<G><<<dim3((a.Umax + 127) / 128, a.batch * a.hn), 128, 0, st>>>(a);
+  select_kernel<G><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_score_select(const RetrieveArgs& a, cudaStream_t st) {
+  switch (a.g) {
+    case 1: return launch_retrieve_g<1>(a, st);
+    case 2: return launch_retrieve_g<2>(a, st);
+    case 4: return launch_retrieve_g<4>(a, st);
+    case 8: return launch_retrieve_g<8>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_gather(const GatherJob* jobs, const RowSrc* rows, int n_inst, int budget, cudaStream_t st) {

@@ -23,16 +23,28 @@ __global__ void __launch_bounds__(1024) trigger_kernel(const uint16_t* __restric
   const int t = *step + 1;
   for (int p = threadIdx.x; p < batch * Hq; p += blockDim.x) {
     const int b = p / Hq, h = p % Hq;
-    const uint16_t* a = q_ref + ((int64_t)b * Hq + h) * D;
-    const uint16_t* c = q_all + (int64_t)b * stride_b + (int64_t)h * D;
+    const uint4* a4 = reinterpret_cast<const uint4*>(q_ref + ((int64_t)b * Hq + h) * D);
+    const uint4* c4 = reinterpret_cast<const uint4*>(q_all + (int64_t)b * stride_b + (int64_t)h * D);
+    // issue all 32 vector loads first (they do not depend on the fp64 chains)
+    uint4 ua[D / 8], uc[D / 8];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      ua[i] = a4[i];
+      uc[i] = c4[i];
+    }
     double dot = 0.0, na = 0.0, nb = 0.0;
-#pragma unroll 4
-    for (int e = 0; e < D; ++e) {
-      double x = (double)bf2f(a[e]);
-      double y = (double)bf2f(c[e]);
-      dot = __dadd_rn(dot, __dmul_rn(x, y));
-      na = __dadd_rn(na, __dmul_rn(x, x));
-      nb = __dadd_rn(nb, __dmul_rn(y, y));
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      float fa[8], fc[8];
+      unpack8(ua[i], fa);
+      unpack8(uc[i], fc);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double x = (double)fa[e], y = (double)fc[e];
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+      }
     }
     double cs = 0.0;
     if (na != 0.0 && nb != 0.0) {

@@ -83,7 +83,7 @@ struct RetrieveArgs {
   int64_t ws_inst_stride;    // elements per instance (2*B*D)
   int64_t inst_global_base;  // global instance index of this layer's first instance
   float* scratch_e;          // [batch*hn][g][Umax]
-  unsigned long long* scratch_key;  // [batch*hn][Umax]
+  uint8_t* scratch_sort;     // [batch*hn][Umax * 14] sort buffers when n exceeds the smem capacity
   GatherJob* jobs;           // [batch*hn]
   RowSrc* rows;              // [batch*hn][B]
   StatsDev* stats;
@@ -170,7 +170,8 @@ struct KmArgs {
   int S_cap;
   InstState* inst;
   // scratch
-  float* half;       // [ni][kmax]
+  float* half;       // [ni][hstride], entries [kc, hstride) = +inf (masked centroid columns)
+  int hstride;       // multiple of 256
   int32_t* assign;   // [ni][Nmax]
   float* dmin;       // [ni][Nmax]
   int32_t* cc;       // [ni][nchunk][kmax]
@@ -185,7 +186,8 @@ struct KmArgs {
   const int32_t* ext_assign;   // device copy of caller-provided assignment (set_prompt_units)
   const float* ext_cent;       // device copy of caller-provided centroids
 };
-cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st);
+// tc_iters / simt_iters: host counters of which assignment kernel ran
+cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_iters, uint64_t* simt_iters);
 cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int batch, int hn,
                                int64_t P, bf16* full, int64_t full_cap, cudaStream_t st);
 cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st);

@@ -277,6 +277,8 @@ def test_kmeans_well_separated_exact(impl):
     X = np32(inp.K[0])[0, :, 0]
     a_o, C_o, cnt, J, _ = oracle.kmeans(X, 64, 10, mode=1)
     a_g, C_g = _gpu_units(ctx, 0, 0, 0, 4096, 0)
+    st = ctx.stats()
+    assert st["kmeans_tc_iters" if impl == 0 else "kmeans_simt_iters"] == 10, st
     assert np.array_equal(a_g, a_o)
     rel = np.abs(C_g - C_o) / np.maximum(np.abs(C_o), 1e-3 * np.abs(C_o).max())
     assert rel.max() < 1e-3
@@ -342,6 +344,7 @@ def test_c2_kmeans_full_size_properties():
     inp = make_inputs(cfg, 1, 0)
     ctx = lkv.Context(lkv.make_config(cfg))
     ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+    assert ctx.stats()["kmeans_tc_iters"] == 10
     N, S, k = 32736, 32, 2046
     Xall = np32(inp.K[0])[0]
     for h in (0, 5):
