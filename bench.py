@@ -118,12 +118,19 @@ def dist_setup():
     return world, rank, local
 
 
+def rank_seed(seed: int, rank: int) -> int:
+    """Weak scaling: every rank draws its own independent sequences."""
+    return seed + 1000 * rank
+
+
 def max_over_ranks(x: float, world: int) -> float:
+    """Max of a per-rank device time over all ranks (nccl on GPUs, gloo in the CPU tests)."""
     if world <= 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -221,7 +228,7 @@ def main():
     K, W = args.steps, args.warmup
     A = args.attr_steps
     T = 1 + W + K + K + A + 2  # direct step + warmup + timed + e2e + attribution (+slack)
-    seed = args.seed + 1000 * rank
+    seed = rank_seed(args.seed, rank)
     ctx = lkv.Context(lkv.make_config(cfg, max_output_len=max(cfg.max_output_len, T + 1), device=local,
                                       kmeans_impl=args.kmeans_impl))
 
