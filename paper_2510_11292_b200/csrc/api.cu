@@ -61,6 +61,10 @@ struct louiskv_ctx {
   int32_t* d_km_cnt = nullptr;
   int32_t* d_km_perm = nullptr;
   int32_t* d_km_flags = nullptr;
+  int32_t* d_km_toff = nullptr;
+  int32_t* d_km_ccT = nullptr;
+  float* d_km_upart = nullptr;
+  int km_task_max = 0;
   StatsDev* d_stats = nullptr;
   int* d_step = nullptr;   // [L] device decode-step counters (graph-replay safe)
   int* d_error = nullptr;  // device capacity-overflow flag
@@ -224,6 +228,10 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_km_cnt, (size_t)nl * std::max(c->kmax, 1));
   ok = ok && dalloc(c, &c->d_km_perm, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
   ok = ok && dalloc(c, &c->d_km_flags, (size_t)nl);
+  c->km_task_max = std::max(c->kmax, 1) + (int)((c->Nmax + 31) / 32);
+  ok = ok && dalloc(c, &c->d_km_toff, (size_t)nl * (c->kmax + 1));
+  ok = ok && dalloc(c, &c->d_km_ccT, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
+  ok = ok && dalloc(c, &c->d_km_upart, (size_t)nl * c->km_task_max * D);
   ok = ok && dalloc(c, &c->d_stats, 1);
   ok = ok && dalloc(c, &c->d_step, (size_t)c->L);
   ok = ok && dalloc(c, &c->d_error, 1);
@@ -321,6 +329,10 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.cnt = c->d_km_cnt;
   a.perm = c->d_km_perm;
   a.flags = c->d_km_flags;
+  a.toff = c->d_km_toff;
+  a.ccT = c->d_km_ccT;
+  a.upart = c->d_km_upart;
+  a.task_max = c->km_task_max;
   a.Nmax = std::max<int64_t>(c->Nmax, 1);
   a.kmax = std::max(c->kmax, 1);
   a.nchunk_max = std::max(c->nchunk_max, 1);

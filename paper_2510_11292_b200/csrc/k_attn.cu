@@ -13,6 +13,10 @@ namespace lkv {
 
 constexpr int AT_THREADS = 256;
 constexpr int AT_HW = AT_THREADS / 16;  // half-warps per CTA
+constexpr int AT_CHUNK = 64;           // rows per pipeline stage
+constexpr int AT_STAGES = 3;
+constexpr int AT_STAGE_BYTES = AT_CHUNK * 2 * ROW_BYTES;  // K + V: 32 KB
+constexpr int AT_SMEM = AT_STAGES * AT_STAGE_BYTES + 64;
 
 struct RowSpan {
   const bf16* k0;  // sinks
@@ -45,7 +49,7 @@ __device__ __forceinline__ void row_ptrs(const RowSpan& sp, int r, const uint4*&
 }
 
 template <int G>
-__global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnArgs a) {
   const int li = blockIdx.x, split = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
   const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
@@ -99,26 +103,80 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
     for (int k = 0; k < 8; ++k) acc[j][k] = 0.f;
   }
 
-  // warp-uniform loop: each half-warp takes 4 rows per iteration (8 x 16-B loads in flight per
-  // lane), then one block-wise online-softmax update for the 4 rows.
-  const int warp = tid >> 5, half = hw & 1;
-  constexpr int NWARP = AT_THREADS / 32;
-  constexpr int RB = 4;
-  for (int base = r_begin + warp * (2 * RB); base < r_end; base += 2 * RB * NWARP) {
+  // ---- rows stream through shared memory: 64-row chunks, AT_STAGES-deep ring, filled by TMA
+  // bulk copies (each piece of the attention set is contiguous: sinks, working set, ring (with
+  // one wrap), or the full cache); thread 0 is the producer, all warps consume every chunk.
+  extern __shared__ __align__(128) uint8_t at_smem[];
+  uint8_t* sKV = at_smem;  // [AT_STAGES][K 64x256 B | V 64x256 B]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(at_smem + AT_STAGES * AT_STAGE_BYTES);
+  // pieces in virtual-row order: (first virtual row, count, K base, V base)
+  int p_v0[4], p_n[4];
+  const bf16* p_k[4];
+  const bf16* p_vv[4];
+  int np = 0;
+  {
+    int v = 0;
+    auto add = [&](int cnt, const bf16* kb, const bf16* vb) {
+      if (cnt > 0) {
+        p_v0[np] = v;
+        p_n[np] = cnt;
+        p_k[np] = kb;
+        p_vv[np] = vb;
+        ++np;
+        v += cnt;
+      }
+    };
+    if (a.inst) {
+      add(sp.n0, sp.k0, sp.v0);
+      add(sp.n1, sp.k1, sp.v1);
+      const int nb = n_rows - sp.n0 - sp.n1;
+      const int h0 = sp.head % sp.cap;
+      const int first = nb < sp.cap - h0 ? nb : sp.cap - h0;
+      add(first, sp.k2 + (int64_t)h0 * D, sp.v2 + (int64_t)h0 * D);
+      add(nb - first, sp.k2, sp.v2);
+    } else {
+      add(sp.n0, sp.k0, sp.v0);
+    }
+  }
+  const int n_chunks = (r_end - r_begin + AT_CHUNK - 1) / AT_CHUNK;
+  auto issue = [&](int c) {
+    const int st = c % AT_STAGES;
+    const int c0 = r_begin + c * AT_CHUNK, c1 = min(r_end, c0 + AT_CHUNK);
+    uint8_t* dK = sKV + st * AT_STAGE_BYTES;
+    uint8_t* dV = dK + AT_CHUNK * ROW_BYTES;
+    ptx_mbar_expect_tx(&full_bar[st], (uint32_t)(c1 - c0) * 2 * ROW_BYTES);
+    for (int p = 0; p < np; ++p) {
+      const int lo = max(c0, p_v0[p]), hi = min(c1, p_v0[p] + p_n[p]);
+      if (lo >= hi) continue;
+      const uint32_t bytes = (uint32_t)(hi - lo) * ROW_BYTES;
+      ptx_bulk_g2s(dK + (lo - c0) * ROW_BYTES, p_k[p] + (int64_t)(lo - p_v0[p]) * D, bytes, &full_bar[st]);
+      ptx_bulk_g2s(dV + (lo - c0) * ROW_BYTES, p_vv[p] + (int64_t)(lo - p_v0[p]) * D, bytes, &full_bar[st]);
+    }
+  };
+  if (tid == 0) {
+    for (int i = 0; i < AT_STAGES; ++i) ptx_mbar_init(&full_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < n_chunks && c < AT_STAGES; ++c) issue(c);
+
+  const int warp = tid >> 5;
+  constexpr int RB = 4;  // rows per half-warp per chunk (16 half-warps x 4 = 64 rows)
+  for (int c = 0; c < n_chunks; ++c) {
+    const int st = c % AT_STAGES;
+    const int rows = min(AT_CHUNK, r_end - (r_begin + c * AT_CHUNK));
+    ptx_mbar_wait(&full_bar[st], (uint32_t)((c / AT_STAGES) & 1));
+    const uint8_t* sK = sKV + st * AT_STAGE_BYTES;
+    const uint8_t* sV = sK + AT_CHUNK * ROW_BYTES;
     uint4 ku[RB], vu[RB];
     bool valid[RB];
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
-      const int r = base + half + 2 * i;
-      valid[i] = r < r_end;
-      ku[i] = make_uint4(0, 0, 0, 0);
-      vu[i] = ku[i];
-      if (valid[i]) {
-        const uint4 *kp, *vp;
-        row_ptrs(sp, r, kp, vp);
-        ku[i] = __ldg(kp + sub);
-        vu[i] = __ldg(vp + sub);
-      }
+      const int r = hw + 16 * i;
+      valid[i] = r < rows;
+      ku[i] = valid[i] ? reinterpret_cast<const uint4*>(sK + r * ROW_BYTES)[sub] : make_uint4(0, 0, 0, 0);
+      vu[i] = valid[i] ? reinterpret_cast<const uint4*>(sV + r * ROW_BYTES)[sub] : make_uint4(0, 0, 0, 0);
     }
     float s[RB][G];
 #pragma unroll
@@ -152,7 +210,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
       float mb = m[j];
 #pragma unroll
       for (int i = 0; i < RB; ++i) mb = fmaxf(mb, s[i][j]);
-      if (mb == -INFINITY) continue;  // no valid row yet for this half-warp
+      if (mb == -INFINITY) continue;
       const float corr = exp2f(m[j] - mb);
       float p[RB], ps = 0.f;
 #pragma unroll
@@ -170,6 +228,8 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
       }
       m[j] = mb;
     }
+    __syncthreads();  // stage st fully consumed
+    if (tid == 0 && c + AT_STAGES < n_chunks) issue(c + AT_STAGES);
   }
 
   // ---- merge the two half-warps of each warp (lane ^ 16 holds the same dims), then the warps
@@ -190,14 +250,15 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
     m[j] = M;
   }
   constexpr int AT_W = AT_THREADS / 32;
-  __shared__ float s_m[AT_W][G], s_l[AT_W][G];
-  __shared__ float s_acc[AT_W][G][D];
+  __shared__ float s_m[AT_W][G], s_lw[AT_W][G];
+  // the stage ring is idle after the main loop: reuse it for the cross-warp merge
+  float (*s_acc)[G][D] = reinterpret_cast<float (*)[G][D]>(at_smem);
   if ((tid & 31) < 16) {
     if (sub == 0) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         s_m[warp][j] = m[j];
-        s_l[warp][j] = l[j];
+        s_lw[warp][j] = l[j];
       }
     }
 #pragma unroll
@@ -216,7 +277,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
     if (M != -INFINITY) {
       for (int w = 0; w < AT_W; ++w) {
         const float sc = exp2f(s_m[w][j] - M);
-        Lsum += s_l[w][j] * sc;
+        Lsum += s_lw[w][j] * sc;
         A += s_acc[w][j][e] * sc;
       }
     }
@@ -241,16 +302,23 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
   const float* P0 = a.part + (int64_t)li * gridDim.y * G * (D + 2);
   const int Y = gridDim.y;
   __shared__ float s_w[64][G];  // per-split weights exp2(m_y - M) / L
+  __shared__ float s_l[64][G];
+  // all (split, head) statistics loaded in parallel, then the G reductions over splits
+  for (int t = tid; t < Y * G; t += AT_THREADS) {
+    const int y = t / G, j = t % G;
+    s_w[y][j] = __ldcg(P0 + (y * G + j) * (D + 2) + D);
+    s_l[y][j] = __ldcg(P0 + (y * G + j) * (D + 2) + D + 1);
+  }
+  __syncthreads();
   if (tid < G) {
     const int j = tid;
     float M = -INFINITY;
-    for (int y = 0; y < Y; ++y) M = fmaxf(M, __ldcg(P0 + (y * G + j) * (D + 2) + D));
+    for (int y = 0; y < Y; ++y) M = fmaxf(M, s_w[y][j]);
     float Lsum = 0.f;
     for (int y = 0; y < Y; ++y) {
-      const float my = __ldcg(P0 + (y * G + j) * (D + 2) + D);
-      const float w = my == -INFINITY ? 0.f : exp2f(my - M);
+      const float w = s_w[y][j] == -INFINITY ? 0.f : exp2f(s_w[y][j] - M);
       s_w[y][j] = w;
-      Lsum += w * __ldcg(P0 + (y * G + j) * (D + 2) + D + 1);
+      Lsum += w * s_l[y][j];
     }
     const float inv = 1.f / Lsum;
     for (int y = 0; y < Y; ++y) s_w[y][j] *= inv;
@@ -270,11 +338,19 @@ __global__ void __launch_bounds__(AT_THREADS) attn_kernel(AttnArgs a) {
 
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.batch * a.hn, a.splits);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    attr = true;
+  }
   switch (a.g) {
-    case 1: attn_kernel<1><<<grid, AT_THREADS, 0, st>>>(a); break;
-    case 2: attn_kernel<2><<<grid, AT_THREADS, 0, st>>>(a); break;
-    case 4: attn_kernel<4><<<grid, AT_THREADS, 0, st>>>(a); break;
-    case 8: attn_kernel<8><<<grid, AT_THREADS, 0, st>>>(a); break;
+    case 1: attn_kernel<1><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
+    case 2: attn_kernel<2><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
+    case 4: attn_kernel<4><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
+    case 8: attn_kernel<8><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -20,6 +20,7 @@
 namespace lkv {
 
 constexpr int KM_CHUNK = 1024;
+constexpr int KM_TASK = 32;  // members per centroid-update task
 
 __device__ __forceinline__ const bf16* xrow(const KmArgs& a, int li, int i) {
   const int b = li / a.hn, h = li % a.hn;
@@ -119,25 +120,63 @@ __global__ void __launch_bounds__(256) km_hist_kernel(KmArgs a, int nchunk) {
   const int32_t* as = a.assign + (int64_t)li * a.Nmax;
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&hist[as[i]], 1);
   __syncthreads();
-  int32_t* cc = a.cc + ((int64_t)li * a.nchunk_max + c) * a.kmax;
-  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) cc[j] = hist[j];
+  // chunk counts are stored transposed, cc[inst][cluster][chunk], so each cluster's prefix over
+  // chunks is one contiguous vector for km_scan
+  int32_t* cc = a.cc + (int64_t)li * a.kmax * a.nchunk_max + c;
+  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) cc[(int64_t)j * a.nchunk_max] = hist[j];
 }
 
 // column scan of cc + cluster offsets; one 1024-thread CTA per instance
+__device__ int km_block_excl_scan(int v, int& total) {
+  __shared__ int s_w[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = lane < nw ? s_w[lane] : 0;
+    int wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < nw) s_w[lane] = wi - w;
+    if (lane == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  const int r = s_w[warp] + incl - v;
+  total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+// per-cluster prefix over chunks (contiguous rows of the transposed cc), counts, cluster offsets
+// (counting sort) and the update-task offsets (ceil(count / KM_TASK) tasks per cluster)
 __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
-  __shared__ int s_part[1024];
   __shared__ int s_empty;
-  int32_t* cc = a.cc + (int64_t)li * a.nchunk_max * a.kmax;
   int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
   int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
   if (threadIdx.x == 0) s_empty = 0;
   __syncthreads();
   for (int j = threadIdx.x; j < a.kc; j += blockDim.x) {
+    int32_t* row = a.cc + ((int64_t)li * a.kmax + j) * a.nchunk_max;
     int run = 0;
-    for (int c = 0; c < nchunk; ++c) {
-      const int v = cc[(int64_t)c * a.kmax + j];
-      cc[(int64_t)c * a.kmax + j] = run;
-      run += v;
+    int32_t* ccT = a.ccT + (int64_t)li * a.nchunk_max * a.kmax;
+    for (int c0 = 0; c0 < nchunk; c0 += 8) {
+      int v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (c0 + q < nchunk) ? row[c0 + q] : 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < nchunk) {
+          ccT[(int64_t)(c0 + q) * a.kmax + j] = run;
+          run += v[q];
+        }
     }
     cnt[j] = run;
     if (run == 0) s_empty = 1;
@@ -145,23 +184,23 @@ __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
   __syncthreads();
   const int per = (a.kc + blockDim.x - 1) / blockDim.x;
   const int j0 = threadIdx.x * per, j1 = min(a.kc, j0 + per);
-  int local = 0;
-  for (int j = j0; j < j1; ++j) local += cnt[j];
-  s_part[threadIdx.x] = local;
-  __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-    const int y = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
-    __syncthreads();
-    s_part[threadIdx.x] += y;
-    __syncthreads();
+  int local = 0, tloc = 0;
+  for (int j = j0; j < j1; ++j) {
+    local += cnt[j];
+    tloc += (cnt[j] + KM_TASK - 1) / KM_TASK;
   }
-  int run = s_part[threadIdx.x] - local;
+  int total, ttotal;
+  int run = km_block_excl_scan(local, total);
+  int trun = km_block_excl_scan(tloc, ttotal);
   for (int j = j0; j < j1; ++j) {
     off[j] = run;
     run += cnt[j];
+    toff[j] = trun;
+    trun += (cnt[j] + KM_TASK - 1) / KM_TASK;
   }
   if (threadIdx.x == 0) {
     off[a.kc] = a.N;
+    toff[a.kc] = ttotal;
     a.flags[li] = s_empty;
   }
   __syncthreads();
@@ -169,23 +208,202 @@ __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
 
 __global__ void __launch_bounds__(1024) km_scan_kernel(KmArgs a, int nchunk) { km_scan_block(a, blockIdx.x, nchunk); }
 
-// empty-cluster repair (reading R-AMB9), then recount; only instances with an empty cluster
+// column scan (many CTAs): warp per cluster, lanes over chunks: exclusive prefix of the cluster's
+// chunk counts -> chunk-major ccT[inst][chunk][cluster] (coalesced reads for the scatter), count
+__global__ void __launch_bounds__(256) km_colscan_kernel(KmArgs a, int nchunk, int only_dirty) {
+  const int li = blockIdx.y;
+  if (only_dirty && a.flags[li] != 2) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + warp;
+  if (j >= a.kc) return;
+  const int32_t* row = a.cc + ((int64_t)li * a.kmax + j) * a.nchunk_max;
+  int32_t* ccT = a.ccT + (int64_t)li * a.nchunk_max * a.kmax;
+  int carry = 0;
+  for (int c0 = 0; c0 < nchunk; c0 += 32) {
+    const int c = c0 + lane;
+    const int v = c < nchunk ? row[c] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (c < nchunk) ccT[(int64_t)c * a.kmax + j] = carry + incl - v;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) a.cnt[(int64_t)li * a.kmax + j] = carry;
+}
+
+// cluster offsets and update-task offsets from the counts (one CTA per instance)
+__global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dirty) {
+  const int li = blockIdx.x;
+  if (only_dirty && a.flags[li] != 2) return;
+  const int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
+  int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  const int per = (a.kc + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * per, j1 = min(a.kc, j0 + per);
+  int local = 0, tloc = 0, empty = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int c = cnt[j];
+    local += c;
+    tloc += (c + KM_TASK - 1) / KM_TASK;
+    empty |= c == 0;
+  }
+  int total, ttotal;
+  int run = km_block_excl_scan(local, total);
+  int trun = km_block_excl_scan(tloc, ttotal);
+  const int any_empty = __syncthreads_or(empty);
+  for (int j = j0; j < j1; ++j) {
+    off[j] = run;
+    run += cnt[j];
+    toff[j] = trun;
+    trun += (cnt[j] + KM_TASK - 1) / KM_TASK;
+  }
+  if (threadIdx.x == 0) {
+    off[a.kc] = a.N;
+    toff[a.kc] = ttotal;
+    a.flags[li] = any_empty;
+  }
+}
+
+// empty-cluster repair (reading R-AMB9), then recount; only instances with an empty cluster.
+// Sequential rule: for each empty id ascending, the donor is the key with the largest dmin (ties ->
+// lower index) among clusters that still have >= 2 members. Eligibility only decreases, so the
+// donors are the first eligible keys of ONE list sorted by (dmin desc, index asc). Exact fast
+// path: radix-select a dmin threshold admitting ~1.5E statically eligible keys, compact and
+// bitonic-sort them in shared memory, walk them once with cluster counts in shared memory.
+// If the walk runs out of candidates (many ineligible), the slow per-empty scan finishes the job.
+constexpr int RP_CAND = 2048;
 __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
   const int li = blockIdx.x;
   if (!a.flags[li]) return;
+  extern __shared__ int rp_smem[];
+  int* s_cnt = rp_smem;                                                   // [kc]
+  int* s_empty = s_cnt + a.kc;                                            // [kc]
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_empty + a.kc + (a.kc & 1 ? 0 : 0));  // [RP_CAND] (2*kc ints: 8-B aligned)
+  int* s_cl = reinterpret_cast<int*>(s_key + RP_CAND);                    // [RP_CAND]
+  __shared__ int s_hist[256];
+  __shared__ int s_n, s_E, s_filled, s_need;
+  __shared__ unsigned s_prefix;
   int32_t* as = a.assign + (int64_t)li * a.Nmax;
   float* dm = a.dmin + (int64_t)li * a.Nmax;
   int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
+  const int tid = threadIdx.x;
+
+  // counts to smem; ordered list of the empty cluster ids (block compaction)
+  const int per = (a.kc + blockDim.x - 1) / blockDim.x;
+  const int j0 = tid * per, j1 = min(a.kc, j0 + per);
+  int ne = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int c = cnt[j];
+    s_cnt[j] = c;
+    ne += c == 0;
+  }
+  int E;
+  int pos = km_block_excl_scan(ne, E);
+  for (int j = j0; j < j1; ++j)
+    if (s_cnt[j] == 0) s_empty[pos++] = j;
+  // dmin key of an eligible point: bits of max(dmin, 0) (monotone for non-negative floats)
+  auto dkey = [&](int i) -> unsigned {
+    const float d = dm[i];
+    if (d == -INFINITY) return 0u;  // already a donor
+    return __float_as_uint(fmaxf(d, 0.f)) + 1u;  // 0 is reserved for "not eligible"
+  };
+  // ---- threshold: the T-th largest eligible key, T = min(1.5E + 32, RP_CAND / 2)
+  const int T = min(E + E / 2 + 32, RP_CAND / 2);
+  if (tid == 0) {
+    s_prefix = 0u;
+    s_need = T;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    const unsigned hi_mask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    for (int i = tid; i < 256; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int i = tid; i < a.N; i += blockDim.x) {
+      const unsigned k = s_cnt[as[i]] >= 2 ? dkey(i) : 0u;
+      if (k != 0u && (k & hi_mask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // descending: find the bucket where the count from the top reaches need
+      int need = s_need, b = 255;
+      for (; b > 0; --b) {
+        if (s_hist[b] >= need) break;
+        need -= s_hist[b];
+      }
+      s_need = need;
+      s_prefix = prefix | ((unsigned)b << shift);
+    }
+    __syncthreads();
+  }
+  const unsigned thr = s_prefix;  // keys >= thr include the top-T (and ties)
+  // ---- compact candidates (key >= thr) and sort them by (key desc, index asc)
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  for (int i = tid; i < a.N; i += blockDim.x) {
+    const unsigned k = s_cnt[as[i]] >= 2 ? dkey(i) : 0u;
+    if (k != 0u && k >= thr) {
+      const int slot = atomicAdd(&s_n, 1);
+      if (slot < RP_CAND) s_key[slot] = ((unsigned long long)(~k) << 32) | (unsigned)i;
+    }
+  }
+  __syncthreads();
+  const int nc = s_n <= RP_CAND ? s_n : 0;  // overflow (massive ties): exact slow path only
+  int np2 = 1;
+  while (np2 < nc) np2 <<= 1;
+  for (int i = nc + tid; i < np2; i += blockDim.x) s_key[i] = ~0ull;
+  __syncthreads();
+  for (int k2 = 2; k2 <= np2; k2 <<= 1)
+    for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+      for (int i = tid; i < np2; i += blockDim.x) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const unsigned long long x = s_key[i], y = s_key[l];
+          const bool up = (i & k2) == 0;
+          if ((x > y) == up) {
+            s_key[i] = y;
+            s_key[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < nc; i += blockDim.x) s_cl[i] = as[(int)(s_key[i] & 0xFFFFFFFFu)];
+  __syncthreads();
+  // ---- one sequential walk (shared memory only)
+  if (tid == 0) {
+    int r = 0;
+    for (int c = 0; c < nc && r < E; ++c) {
+      const int cl = s_cl[c];
+      if (s_cnt[cl] < 2) continue;
+      const int i = (int)(s_key[c] & 0xFFFFFFFFu);
+      const int j = s_empty[r++];
+      s_cnt[cl] -= 1;
+      s_cnt[j] = 1;
+      as[i] = j;
+      dm[i] = -INFINITY;
+      atomicSub(&a.cc[((int64_t)li * a.kmax + cl) * a.nchunk_max + i / KM_CHUNK], 1);
+      atomicAdd(&a.cc[((int64_t)li * a.kmax + j) * a.nchunk_max + i / KM_CHUNK], 1);
+    }
+    s_filled = r;
+  }
+  __syncthreads();
+  for (int j = tid; j < a.kc; j += blockDim.x) cnt[j] = s_cnt[j];
+  __syncthreads();
+  // ---- fallback for whatever the candidate list could not fill (exact, slow)
   __shared__ float s_bv[32];
   __shared__ int s_bi[32];
-  __shared__ int s_donor;
-  for (int j = 0; j < a.kc; ++j) {
-    if (cnt[j] != 0) continue;  // uniform: every thread reads the same value
+  for (int r = s_filled; r < E; ++r) {
+    const int j = s_empty[r];
     float bv = -INFINITY;
     int bi = 0x7FFFFFFF;
-    for (int i = threadIdx.x; i < a.N; i += blockDim.x) {
-      const float v = dm[i];
-      if (v == -INFINITY || cnt[as[i]] < 2) continue;
+    for (int i = tid; i < a.N; i += blockDim.x) {
+      if (dm[i] == -INFINITY || cnt[as[i]] < 2) continue;
+      const float v = fmaxf(dm[i], 0.f);  // same order as the fast path (fp32 dmin may dip below 0)
       if (v > bv || (v == bv && i < bi)) {
         bv = v;
         bi = i;
@@ -199,12 +417,12 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
         bi = oi;
       }
     }
-    if ((threadIdx.x & 31) == 0) {
-      s_bv[threadIdx.x >> 5] = bv;
-      s_bi[threadIdx.x >> 5] = bi;
+    if ((tid & 31) == 0) {
+      s_bv[tid >> 5] = bv;
+      s_bi[tid >> 5] = bi;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       float v = -INFINITY;
       int d = 0x7FFFFFFF;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
@@ -212,41 +430,45 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
           v = s_bv[w];
           d = s_bi[w];
         }
-      s_donor = d;
       if (d != 0x7FFFFFFF) {
-        cnt[as[d]] -= 1;
+        const int from = as[d];
+        cnt[from] -= 1;
         as[d] = j;
         cnt[j] = 1;
         dm[d] = -INFINITY;
+        atomicSub(&a.cc[((int64_t)li * a.kmax + from) * a.nchunk_max + d / KM_CHUNK], 1);
+        atomicAdd(&a.cc[((int64_t)li * a.kmax + j) * a.nchunk_max + d / KM_CHUNK], 1);
       }
     }
     __syncthreads();
   }
-  // recount chunk histograms for this instance
-  int32_t* cc = a.cc + (int64_t)li * a.nchunk_max * a.kmax;
-  for (int64_t t = threadIdx.x; t < (int64_t)nchunk * a.kmax; t += blockDim.x) cc[t] = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < a.N; i += blockDim.x) atomicAdd(&cc[(int64_t)(i / KM_CHUNK) * a.kmax + as[i]], 1);
-  __threadfence_block();
-  __syncthreads();
-  km_scan_block(a, li, nchunk);
+  // chunk histograms were updated in place; the column scan + offsets rerun for this instance
+  if (tid == 0) a.flags[li] = 2;
 }
 
 // stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
 __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   extern __shared__ int base[];  // [kc] running offsets of this chunk
   const int li = blockIdx.y, c = blockIdx.x, lane = threadIdx.x;
-  const int32_t* cc = a.cc + ((int64_t)li * a.nchunk_max + c) * a.kmax;
+  const int32_t* ccT = a.ccT + ((int64_t)li * a.nchunk_max + c) * a.kmax;
   const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
-  for (int j = lane; j < a.kc; j += 32) base[j] = cc[j] + off[j];
+  for (int j = lane; j < a.kc; j += 32) base[j] = ccT[j] + off[j];
   __syncwarp();
   const int32_t* as = a.assign + (int64_t)li * a.Nmax;
   int32_t* perm = a.perm + (int64_t)li * a.Nmax;
   const int i0 = c * KM_CHUNK, i1 = min(a.N, i0 + KM_CHUNK);
-  for (int r0 = i0; r0 < i1; r0 += 32) {
-    const int i = r0 + lane;
+  // prefetch the chunk's assignments (32 per lane) so the rounds below only touch registers/smem
+  int cl_pre[KM_CHUNK / 32];
+#pragma unroll
+  for (int r = 0; r < KM_CHUNK / 32; ++r) {
+    const int i = i0 + r * 32 + lane;
+    cl_pre[r] = i < i1 ? as[i] : -1 - lane;
+  }
+#pragma unroll
+  for (int r = 0; r < KM_CHUNK / 32; ++r) {
+    const int i = i0 + r * 32 + lane;
     const bool valid = i < i1;
-    const int cl = valid ? as[i] : -1 - lane;
+    const int cl = cl_pre[r];
     const unsigned peers = __match_any_sync(0xffffffffu, cl);
     const int leader = __ffs(peers) - 1;
     const int rank = __popc(peers & ((1u << lane) - 1u));
@@ -260,49 +482,85 @@ __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   }
 }
 
-// centroid update: warp per cluster, sequential fp32 sum over members in position order
-__global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
-  const int li = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * 4 + warp;
-  if (j >= a.kc) return;
-  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
-  const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
-  const int m0 = off[j], m1 = off[j + 1];
-  float s[4] = {0.f, 0.f, 0.f, 0.f};
-  int m = m0;
-  for (; m + 4 <= m1; m += 4) {
-    uint2 u[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) u[q] = reinterpret_cast<const uint2*>(xrow(a, li, perm[m + q]))[lane];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      s[0] = __fadd_rn(s[0], __uint_as_float(u[q].x << 16));
-      s[1] = __fadd_rn(s[1], __uint_as_float(u[q].x & 0xFFFF0000u));
-      s[2] = __fadd_rn(s[2], __uint_as_float(u[q].y << 16));
-      s[3] = __fadd_rn(s[3], __uint_as_float(u[q].y & 0xFFFF0000u));
-    }
-  }
-  for (; m < m1; ++m) {
-    const uint2 u = reinterpret_cast<const uint2*>(xrow(a, li, perm[m]))[lane];
-    s[0] = __fadd_rn(s[0], __uint_as_float(u.x << 16));
-    s[1] = __fadd_rn(s[1], __uint_as_float(u.x & 0xFFFF0000u));
-    s[2] = __fadd_rn(s[2], __uint_as_float(u.y << 16));
-    s[3] = __fadd_rn(s[3], __uint_as_float(u.y & 0xFFFF0000u));
-  }
-  const float n = (float)(m1 - m0);
+// centroid update, task based: cluster j is cut into ceil(|j| / KM_TASK) tasks of consecutive
+// members (position order); a warp sums one task (lane = 4 dims, sequential fp32). Single-task
+// clusters are finalised in place; larger ones write partial sums that km_finalize adds in task
+// order (deterministic; bounded work per warp however large a cluster grows).
+__device__ __forceinline__ void km_write_centroid(const KmArgs& a, int li, int j, const float s[4], int n, int lane) {
   float* C = a.cent + ((int64_t)li * a.Umax + j) * D;
   uint16_t* Cb = reinterpret_cast<uint16_t*>(a.centb) + ((int64_t)li * a.Umax + j) * D;
   float ss = 0.f;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const float c = m1 > m0 ? __fdiv_rn(s[e], n) : C[lane * 4 + e];
+    const float c = __fdiv_rn(s[e], (float)n);
     C[lane * 4 + e] = c;
     Cb[lane * 4 + e] = f2bf_rne(c);
     ss = fmaf(c, c, ss);
   }
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if (lane == 0) a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+}
+
+__global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + warp;
+  const int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  if (t >= toff[a.kc]) return;
+  // cluster of task t: the last j with toff[j] <= t
+  int lo = 0, hi = a.kc - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (toff[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const int j = lo;
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
+  const int q = t - toff[j];
+  const int m0 = off[j] + q * KM_TASK, m1 = min(off[j + 1], m0 + KM_TASK);
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int m = m0; m < m1; m += 8) {
+    uint2 u[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (m + r < m1) u[r] = reinterpret_cast<const uint2*>(xrow(a, li, perm[m + r]))[lane];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (m + r < m1) {
+        s[0] = __fadd_rn(s[0], __uint_as_float(u[r].x << 16));
+        s[1] = __fadd_rn(s[1], __uint_as_float(u[r].x & 0xFFFF0000u));
+        s[2] = __fadd_rn(s[2], __uint_as_float(u[r].y << 16));
+        s[3] = __fadd_rn(s[3], __uint_as_float(u[r].y & 0xFFFF0000u));
+      }
+  }
+  const int ntask = toff[j + 1] - toff[j];
+  if (ntask == 1) {
+    km_write_centroid(a, li, j, s, off[j + 1] - off[j], lane);
+  } else {
+    float4* P = reinterpret_cast<float4*>(a.upart + ((int64_t)li * a.task_max + t) * D);
+    P[lane] = make_float4(s[0], s[1], s[2], s[3]);
+  }
+}
+
+__global__ void __launch_bounds__(128) km_finalize_kernel(KmArgs a) {
+  const int li = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 4 + warp;
+  if (j >= a.kc) return;
+  const int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  const int t0 = toff[j], t1 = toff[j + 1];
+  if (t1 - t0 <= 1) return;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int t = t0; t < t1; ++t) {
+    const float4 v = reinterpret_cast<const float4*>(a.upart + ((int64_t)li * a.task_max + t) * D)[lane];
+    s[0] = __fadd_rn(s[0], v.x);
+    s[1] = __fadd_rn(s[1], v.y);
+    s[2] = __fadd_rn(s[2], v.z);
+    s[3] = __fadd_rn(s[3], v.w);
+  }
+  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  km_write_centroid(a, li, j, s, off[j + 1] - off[j], lane);
 }
 
 // caller-supplied clustering: copy assignment and centroids in
@@ -384,8 +642,14 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st);  // k_kmeans_tc.
 
 static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool repair, cudaStream_t st) {
   km_hist_kernel<<<dim3(nchunk, ni), 256, sizeof(int) * a.kc, st>>>(a, nchunk);
-  km_scan_kernel<<<ni, 1024, 0, st>>>(a, nchunk);
-  if (repair) km_repair_kernel<<<ni, 1024, 0, st>>>(a, nchunk);
+  km_colscan_kernel<<<dim3((a.kc + 7) / 8, ni), 256, 0, st>>>(a, nchunk, 0);
+  km_offsets_kernel<<<ni, 1024, 0, st>>>(a, 0);
+  if (repair) {
+    const size_t rsm = sizeof(int) * (2 * a.kc) + RP_CAND * (sizeof(unsigned long long) + sizeof(int));
+    km_repair_kernel<<<ni, 1024, rsm, st>>>(a, nchunk);
+    km_colscan_kernel<<<dim3((a.kc + 7) / 8, ni), 256, 0, st>>>(a, nchunk, 1);
+    km_offsets_kernel<<<ni, 1024, 0, st>>>(a, 1);
+  }
   km_scatter_kernel<<<dim3(nchunk, ni), 32, sizeof(int) * a.kc, st>>>(a);
   return cudaGetLastError();
 }
@@ -404,6 +668,7 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
   if (!attr) {
     cudaFuncSetAttribute(km_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(km_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(km_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   const int nchunk = (a.N + KM_CHUNK - 1) / KM_CHUNK;
@@ -425,7 +690,8 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
       if (!done) km_assign_simt_kernel<<<dim3((a.N + 127) / 128, ni), 128, 0, st>>>(a);
       ++*(done ? tc_iters : simt_iters);
       if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
-      km_update_kernel<<<gk, 128, 0, st>>>(a);
+      km_update_kernel<<<dim3((a.task_max + 3) / 4, ni), 128, 0, st>>>(a);
+      km_finalize_kernel<<<gk, 128, 0, st>>>(a);
     }
   }
   km_offload_kernel<<<dim3((a.N + 7) / 8, ni), 128, 0, st>>>(a);

@@ -34,8 +34,8 @@ constexpr int KH = 64;             // bf16 elements per 128-B swizzle row
 constexpr int A_BYTES = BM * D * 2;       // 32 KB
 constexpr int B_BYTES = BN * D * 2;       // 64 KB
 constexpr int B_STAGES = 2;
-constexpr int THREADS = 256;
-constexpr int SMEM_BYTES = 2 * A_BYTES + B_STAGES * B_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 384;  // 4 non-epilogue warps + 8 epilogue warps
+constexpr int SMEM_BYTES = 2 * A_BYTES + B_STAGES * B_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BM * 4 + 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -141,9 +141,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], 1 + 4);  // MMA commit + the 4 epilogue warps (they read ||x||^2 from sA)
+      mbar_init(&a_empty[i], 1 + 8);  // MMA commit + the 8 epilogue warps (half of them read ||x||^2 from sA)
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);
+      mbar_init(&acc_empty[i], 8);
     }
     for (int i = 0; i < B_STAGES; ++i) {
       mbar_init(&b_full[i], 1);
@@ -222,8 +222,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: thread = key row = TMEM lane
+    // ---------------- epilogue: 8 warps; thread = key row = TMEM lane (warp % 4 selects the lane
+    // quarter), column half = (warp - 4) / 4; the two halves of a row merge through smem per item
+    const int e = warp - 4;
     const int q = warp & 3;
+    const int chalf = e >> 2;
     const int row = q * 32 + lane;
     int it = 0, acc = 0;
     uint32_t accphase = 0;
@@ -231,12 +234,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int inst = item / p.n_mblk, mb = item % p.n_mblk;
       const float* half = p.half + (int64_t)inst * p.hstride;
       float best = -INFINITY;
-      int bidx = 0;
-      // ||x||^2 from the swizzled A tile (row = TMEM lane), then release the A buffer
+      int bidx = 0x7FFFFFFF;
       const int ab = it & 1;
-      mbar_wait(&a_full[ab], (it >> 1) & 1);
       float xn = 0.f;
-      {
+      mbar_wait(&a_full[ab], (it >> 1) & 1);
+      if (chalf == 0) {
+        // ||x||^2 from the swizzled A tile (row = TMEM lane)
         const uint8_t* arow = sA + ab * A_BYTES;
 #pragma unroll
         for (int kh = 0; kh < 2; ++kh) {
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             float f[8];
             unpack8(u, f);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) xn = fmaf(f[e], f[e], xn);
+            for (int x = 0; x < 8; ++x) xn = fmaf(f[x], f[x], xn);
           }
         }
       }
@@ -256,22 +259,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int nt = 0; nt < p.n_ntile; ++nt) {
         mbar_wait(&acc_full[acc], accphase);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
-          uint32_t r[32];
-          TMEM_LD32(taddr + ch * 32, r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const int col0 = nt * BN + ch * 32;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + chalf * (BN / 2));
+        const int colbase = nt * BN + chalf * (BN / 2);
+        uint32_t r[2][32];
+        TMEM_LD32(taddr, r[0]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int ch = 0; ch < BN / 64; ++ch) {
+          // software pipeline: the next 32 columns are in flight while this chunk is reduced
+          if (ch + 1 < BN / 64) TMEM_LD32(taddr + (ch + 1) * 32, r[(ch + 1) & 1]);
+          const uint32_t* rc = r[ch & 1];
+          const int col0 = colbase + ch * 32;
           const float4* h4 = reinterpret_cast<const float4*>(half + col0);
           float v[32];
 #pragma unroll
           for (int c4 = 0; c4 < 8; ++c4) {
             const float4 hv = __ldg(h4 + c4);
-            v[c4 * 4 + 0] = __uint_as_float(r[c4 * 4 + 0]) - hv.x;
-            v[c4 * 4 + 1] = __uint_as_float(r[c4 * 4 + 1]) - hv.y;
-            v[c4 * 4 + 2] = __uint_as_float(r[c4 * 4 + 2]) - hv.z;
-            v[c4 * 4 + 3] = __uint_as_float(r[c4 * 4 + 3]) - hv.w;
+            v[c4 * 4 + 0] = __uint_as_float(rc[c4 * 4 + 0]) - hv.x;
+            v[c4 * 4 + 1] = __uint_as_float(rc[c4 * 4 + 1]) - hv.y;
+            v[c4 * 4 + 2] = __uint_as_float(rc[c4 * 4 + 2]) - hv.z;
+            v[c4 * 4 + 3] = __uint_as_float(rc[c4 * 4 + 3]) - hv.w;
           }
           float m01[16];
 #pragma unroll
@@ -289,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             best = m;
             bidx = col0 + idx;
           }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
         __syncwarp();
@@ -298,11 +306,28 @@ __global__ void __launch_bounds__(THREADS, 1)
           accphase ^= 1;
         }
       }
-      const int grow = mb * BM + row;
-      if (grow < p.N) {
-        p.assign[(int64_t)inst * p.Nmax + grow] = bidx;
-        p.dmin[(int64_t)inst * p.Nmax + grow] = fmaf(-2.f, best, xn);
+      // merge the two column halves of each row (strictly greater wins; ties -> lower index)
+      float* s_best = reinterpret_cast<float*>(tmem_slot + 4);
+      int* s_idx = reinterpret_cast<int*>(s_best + BM);
+      if (chalf == 1) {
+        s_best[row] = best;
+        s_idx[row] = bidx;
       }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (chalf == 0) {
+        const float ob = s_best[row];
+        const int oi = s_idx[row];
+        if (ob > best || (ob == best && oi < bidx)) {
+          best = ob;
+          bidx = oi;
+        }
+        const int grow = mb * BM + row;
+        if (grow < p.N) {
+          p.assign[(int64_t)inst * p.Nmax + grow] = bidx;
+          p.dmin[(int64_t)inst * p.Nmax + grow] = fmaf(-2.f, best, xn);
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
   }
   tc_fence_before();

@@ -174,7 +174,11 @@ struct KmArgs {
   int hstride;       // multiple of 256
   int32_t* assign;   // [ni][Nmax]
   float* dmin;       // [ni][Nmax]
-  int32_t* cc;       // [ni][nchunk][kmax]
+  int32_t* cc;       // [ni][kmax][nchunk_max] (transposed chunk histograms)
+  int32_t* ccT;      // [ni][nchunk_max][kmax] chunk-major exclusive prefixes (scatter bases)
+  int32_t* toff;     // [ni][kmax+1] update-task offsets
+  float* upart;      // [ni][task_max][D] partial sums of multi-task clusters
+  int task_max;      // kmax + ceil(Nmax / 32)
   int32_t* off;      // [ni][kmax+1]
   int32_t* cnt;      // [ni][kmax]
   int32_t* perm;     // [ni][Nmax]
@@ -209,6 +213,31 @@ __device__ __forceinline__ void unpack8(const uint4 u, float* f) {
   f[5] = __uint_as_float(u.z & 0xFFFF0000u);
   f[6] = __uint_as_float(u.w << 16);
   f[7] = __uint_as_float(u.w & 0xFFFF0000u);
+}
+// ---- mbarrier / bulk-copy (TMA engine) helpers
+__device__ __forceinline__ uint32_t ptx_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ptx_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ptx_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void ptx_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ptx_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ptx_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(ptx_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy on the TMA engine; completes `bytes` of transaction on `bar`
+__device__ __forceinline__ void ptx_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(ptx_smem_u32(bar))
+               : "memory");
 }
 // fp32 -> bf16 bits, round to nearest even (NaN-free inputs)
 __device__ __forceinline__ uint16_t f2bf_rne(float x) {
