@@ -63,6 +63,7 @@ struct louiskv_ctx {
   int32_t* d_km_flags = nullptr;
   int32_t* d_km_toff = nullptr;
   int32_t* d_km_ccT = nullptr;
+  uint16_t* d_km_bext = nullptr;
   float* d_km_upart = nullptr;
   int km_task_max = 0;
   StatsDev* d_stats = nullptr;
@@ -230,6 +231,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_km_flags, (size_t)nl);
   c->km_task_max = std::max(c->kmax, 1) + (int)((c->Nmax + 31) / 32);
   ok = ok && dalloc(c, &c->d_km_toff, (size_t)nl * (c->kmax + 1));
+  ok = ok && dalloc(c, &c->d_km_bext, (size_t)nl * c->Umax * 8);
   ok = ok && dalloc(c, &c->d_km_ccT, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
   ok = ok && dalloc(c, &c->d_km_upart, (size_t)nl * c->km_task_max * D);
   ok = ok && dalloc(c, &c->d_stats, 1);
@@ -331,6 +333,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.flags = c->d_km_flags;
   a.toff = c->d_km_toff;
   a.ccT = c->d_km_ccT;
+  a.bext = c->d_km_bext;
   a.upart = c->d_km_upart;
   a.task_max = c->km_task_max;
   a.Nmax = std::max<int64_t>(c->Nmax, 1);

@@ -22,6 +22,21 @@ namespace lkv {
 constexpr int KM_CHUNK = 1024;
 constexpr int KM_TASK = 32;  // members per centroid-update task
 
+// -½||c||² folded into the tensor-core GEMM as a 9th K-step: three bf16 parts whose sum equals the
+// fp32 half-norm to within fp32 rounding (h = hi + mid + lo exactly up to the last ~2^-24 of h)
+__device__ __forceinline__ void write_bext(const KmArgs& a, int li, int j, float h) {
+  const uint16_t hi = f2bf_rne(h);
+  const float r1 = h - bf2f(hi);
+  const uint16_t mid = f2bf_rne(r1);
+  const uint16_t lo = f2bf_rne(r1 - bf2f(mid));
+  uint4 v;
+  v.x = (uint32_t)(hi ^ 0x8000u) | ((uint32_t)(mid ^ 0x8000u) << 16);  // negated (sign flip)
+  v.y = (uint32_t)(lo ^ 0x8000u);
+  v.z = 0u;
+  v.w = 0u;
+  reinterpret_cast<uint4*>(a.bext)[(int64_t)li * a.Umax + j] = v;
+}
+
 __device__ __forceinline__ const bf16* xrow(const KmArgs& a, int li, int i) {
   const int b = li / a.hn, h = li % a.hn;
   return a.k + (int64_t)b * a.sb + (int64_t)(a.S + i) * a.st + (int64_t)h * a.sh;
@@ -51,13 +66,19 @@ __global__ void km_init_kernel(KmArgs a) {
     ss = fmaf(c[e], c[e], ss);
   }
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+  if (lane == 0) {
+    a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+    write_bext(a, li, j, 0.5f * ss);
+  }
 }
 
-// ---- +inf half-norms for the padded centroid columns [kc, hstride) (masked in the argmax)
+// ---- +inf half-norms (-inf GEMM extension) for the padded centroid columns [kc, hstride)
 __global__ void km_half_pad_kernel(KmArgs a) {
   const int li = blockIdx.y;
-  for (int j = a.kc + threadIdx.x; j < a.hstride; j += blockDim.x) a.half[(int64_t)li * a.hstride + j] = INFINITY;
+  for (int j = a.kc + threadIdx.x; j < a.hstride; j += blockDim.x) {
+    a.half[(int64_t)li * a.hstride + j] = INFINITY;
+    if (j < a.Umax) reinterpret_cast<uint4*>(a.bext)[(int64_t)li * a.Umax + j] = make_uint4(0xFF80u, 0u, 0u, 0u);
+  }
 }
 
 // ---- SIMT assignment (correctness reference path; the tcgen05 kernel is the fast path)
@@ -498,7 +519,10 @@ __device__ __forceinline__ void km_write_centroid(const KmArgs& a, int li, int j
     ss = fmaf(c, c, ss);
   }
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+  if (lane == 0) {
+    a.half[(int64_t)li * a.hstride + j] = 0.5f * ss;
+    write_bext(a, li, j, 0.5f * ss);
+  }
 }
 
 __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {

@@ -35,7 +35,11 @@ constexpr int A_BYTES = BM * D * 2;       // 32 KB
 constexpr int B_BYTES = BN * D * 2;       // 64 KB
 constexpr int B_STAGES = 2;
 constexpr int THREADS = 384;  // 4 non-epilogue warps + 8 epilogue warps
-constexpr int SMEM_BYTES = 2 * A_BYTES + B_STAGES * B_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BM * 4 + 16;
+constexpr int BX_BYTES = BN * 16;        // B extension block: 256 centroids x 8 bf16 (4 KB)
+constexpr int AX_BYTES = BM * 16;        // A extension block: 128 keys x 8 bf16 (1,1,1,0...) (2 KB)
+constexpr int ZERO_BYTES = BN * 16;      // the second (all-zero) core-matrix column of the 9th K-step
+constexpr int SMEM_BYTES = 2 * A_BYTES + B_STAGES * (B_BYTES + BX_BYTES) + AX_BYTES + ZERO_BYTES + 1024 /*align*/ +
+                           256 /*barriers*/ + 2 * BM * 4 + 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -82,6 +86,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
+// UMMA descriptor for the 9th K-step: K-major, SWIZZLE_NONE, core matrices (8 rows x 16 B) packed
+// at 128 B (SBO); the second 8-element K half sits LBO bytes further (the shared zero block)
+__device__ __forceinline__ uint64_t umma_desc_none(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;  // layout type 0 = SWIZZLE_NONE
+}
 // instruction descriptor kind::f16: D=F32, A=B=BF16, K-major both, N=256, M=128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
@@ -121,12 +135,15 @@ struct TcParams {
 
 __global__ void __launch_bounds__(THREADS, 1)
     kmeans_assign_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            TcParams p) {
+                            const __grid_constant__ CUtensorMap tmBx, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                              // [2][A_BYTES]
   uint8_t* sB = smem + 2 * A_BYTES;                // [B_STAGES][B_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + B_STAGES * B_BYTES);
+  uint8_t* sBx = sB + B_STAGES * B_BYTES;          // [B_STAGES][BX_BYTES]
+  uint8_t* sAx = sBx + B_STAGES * BX_BYTES;        // [AX_BYTES] constant (1,1,1,0,...) rows
+  uint8_t* sZero = sAx + AX_BYTES;                 // [ZERO_BYTES] zeros
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sZero + ZERO_BYTES);
   uint64_t* a_full = bars;           // [2]
   uint64_t* a_empty = bars + 2;      // [2]
   uint64_t* b_full = bars + 4;       // [B_STAGES]
@@ -137,6 +154,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = p.ni * p.n_mblk;
+  // constant operand blocks of the 9th K-step (generic-proxy stores, fenced for the async proxy)
+  for (int i = threadIdx.x; i < BM; i += blockDim.x)
+    reinterpret_cast<uint4*>(sAx)[i] = make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u);
+  for (int i = threadIdx.x; i < ZERO_BYTES / 16; i += blockDim.x) reinterpret_cast<uint4*>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -175,9 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_4d(sA + ab * A_BYTES + A_BYTES / 2, &tmA, &a_full[ab], KH, h, mb * BM, b);
         for (int nt = 0; nt < p.n_ntile; ++nt) {
           mbar_wait(&b_empty[bstage], bphase ^ 1);
-          mbar_expect_tx(&b_full[bstage], B_BYTES);
+          mbar_expect_tx(&b_full[bstage], B_BYTES + BX_BYTES);
           tma_load_3d(sB + bstage * B_BYTES, &tmB, &b_full[bstage], 0, nt * BN, inst);
           tma_load_3d(sB + bstage * B_BYTES + B_BYTES / 2, &tmB, &b_full[bstage], KH, nt * BN, inst);
+          tma_load_3d(sBx + bstage * BX_BYTES, &tmBx, &b_full[bstage], 0, nt * BN, inst);
           if (++bstage == B_STAGES) {
             bstage = 0;
             bphase ^= 1;
@@ -207,6 +230,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t kofb = (uint32_t)((k >> 2) * (BN * 128) + (k & 3) * 32);
             mma_bf16(tmem_d, umma_desc(a_base + koff), umma_desc(b_base + kofb), k > 0 ? 1u : 0u);
           }
+          {  // 9th K-step: + (1,1,1) . (-h_hi, -h_mid, -h_lo)  ==  - ½||c||²
+            const uint32_t ax = smem_u32(sAx), bx = smem_u32(sBx + bstage * BX_BYTES), z = smem_u32(sZero);
+            mma_bf16(tmem_d, umma_desc_none(ax, z - ax), umma_desc_none(bx, z - bx), 1u);
+          }
           mma_commit(&b_empty[bstage]);
           mma_commit(&acc_full[acc]);
           if (nt == p.n_ntile - 1) mma_commit(&a_empty[ab]);
@@ -232,7 +259,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t accphase = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       const int inst = item / p.n_mblk, mb = item % p.n_mblk;
-      const float* half = p.half + (int64_t)inst * p.hstride;
       float best = -INFINITY;
       int bidx = 0x7FFFFFFF;
       const int ab = it & 1;
@@ -270,16 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (ch + 1 < BN / 64) TMEM_LD32(taddr + (ch + 1) * 32, r[(ch + 1) & 1]);
           const uint32_t* rc = r[ch & 1];
           const int col0 = colbase + ch * 32;
-          const float4* h4 = reinterpret_cast<const float4*>(half + col0);
-          float v[32];
+          float v[32];  // the accumulator already holds x.c - ½||c||² (9th K-step)
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            const float4 hv = __ldg(h4 + c4);
-            v[c4 * 4 + 0] = __uint_as_float(rc[c4 * 4 + 0]) - hv.x;
-            v[c4 * 4 + 1] = __uint_as_float(rc[c4 * 4 + 1]) - hv.y;
-            v[c4 * 4 + 2] = __uint_as_float(rc[c4 * 4 + 2]) - hv.z;
-            v[c4 * 4 + 3] = __uint_as_float(rc[c4 * 4 + 3]) - hv.w;
-          }
+          for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(rc[c]);
           float m01[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) m01[i] = fmaxf(v[2 * i], v[2 * i + 1]);
@@ -419,6 +438,20 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st) {
       return cudaErrorNotSupported;
     }
   }
+  CUtensorMap tmBx;
+  {
+    cuuint64_t dims[3] = {8, (cuuint64_t)a.Umax, (cuuint64_t)ni};
+    cuuint64_t strides[2] = {16, (cuuint64_t)a.Umax * 16};
+    cuuint32_t box[3] = {8, tc::BN, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = enc(&tmBx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)a.bext, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      tc_debug("tensor map of the half-norm extension", (int)r);
+      return cudaErrorNotSupported;
+    }
+  }
   tc::TcParams p;
   p.ni = ni;
   p.N = a.N;
@@ -442,7 +475,7 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int items = ni * p.n_mblk;
   const int grid = items < sms ? items : sms;
-  tc::kmeans_assign_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tmA, tmB, p);
+  tc::kmeans_assign_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tmA, tmB, tmBx, p);
   return cudaGetLastError();
 }
 

@@ -172,6 +172,7 @@ struct KmArgs {
   // scratch
   float* half;       // [ni][hstride], entries [kc, hstride) = +inf (masked centroid columns)
   int hstride;       // multiple of 256
+  uint16_t* bext;    // [ni][Umax][8] bf16: (-h_hi, -h_mid, -h_lo, 0...) — the 9th GEMM K-step
   int32_t* assign;   // [ni][Nmax]
   float* dmin;       // [ni][Nmax]
   int32_t* cc;       // [ni][kmax][nchunk_max] (transposed chunk histograms)
