@@ -57,17 +57,34 @@ float lko_bf16_round(float x) {
 /* R1: cosine similarity and the semantic-boundary trigger.                   */
 /* P:101-106 [§4.1 eq. r_t = (1/H) Σ_h cosine(q_{t-1}^h, q_t^h)],             */
 /* P:301 [Alg. 1: is_new_segment = (t==1) ∨ (CosineSimilarity < r)].          */
-/* Recipe: fp64, e ascending, multiply then add (no fma), sqrt(na)*sqrt(nb),  */
-/* clamp to [-1,1]; zero norm -> 0.                                    */
+/* Recipe (fp64, fixed order, R1): the d elements are cut into 16   */
+/* contiguous chunks of ceil(d/16); each chunk is summed sequentially         */
+/* (multiply then add, no fma) for dot, ||a||², ||b||²; the 16 partial sums   */
+/* are combined by a balanced pairwise tree s[l] += s[l+8], +4, +2, +1.        */
+/* cos = dot / (sqrt(na)*sqrt(nb)), clamped to [-1,1]; zero norm -> 0. */
 /* ------------------------------------------------------------------------ */
+static double r1_tree16(double* s) {
+  for (int off = 8; off >= 1; off >>= 1)
+    for (int l = 0; l < off; ++l) s[l] = s[l] + s[l + off];
+  return s[0];
+}
+
 double lko_cosine_r1(const float* a, const float* b, int d) {
-  double dot = 0.0, na = 0.0, nb = 0.0;
-  for (int e = 0; e < d; ++e) {
-    double x = (double)a[e], y = (double)b[e];
-    dot = dot + x * y;
-    na = na + x * x;
-    nb = nb + y * y;
+  double pd[16], pa[16], pb[16];
+  const int chunk = (d + 15) / 16;
+  for (int l = 0; l < 16; ++l) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int e = l * chunk; e < (l + 1) * chunk && e < d; ++e) {
+      double x = (double)a[e], y = (double)b[e];
+      dot = dot + x * y;
+      na = na + x * x;
+      nb = nb + y * y;
+    }
+    pd[l] = dot;
+    pa[l] = na;
+    pb[l] = nb;
   }
+  double dot = r1_tree16(pd), na = r1_tree16(pa), nb = r1_tree16(pb);
   if (na == 0.0 || nb == 0.0) return 0.0;
   double c = dot / (sqrt(na) * sqrt(nb));
   if (c > 1.0) c = 1.0;

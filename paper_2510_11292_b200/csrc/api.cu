@@ -48,7 +48,6 @@ struct louiskv_ctx {
   // scratch
   float* d_se = nullptr;
   uint8_t* d_ssort = nullptr;
-  GatherJob* d_jobs = nullptr;
   RowSrc* d_rows = nullptr;
   float* d_part = nullptr;
   int* d_counters = nullptr;
@@ -117,6 +116,44 @@ bool dalloc(louiskv_ctx* c, T** p, size_t n) {
 bool is_full(const louiskv_ctx* c, int layer) { return (c->cfg.full_cache_layers >> layer) & 1ull; }
 
 int64_t inst_base(const louiskv_ctx* c, int layer) { return (int64_t)c->ridx[layer] * c->inst_per_layer; }
+
+RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t stride_b) {
+  const int64_t ib = inst_base(c, layer);
+  RetrieveArgs a{};
+  a.q_own = reinterpret_cast<const bf16*>(q);
+  a.stride_b = stride_b;
+  a.batch = c->batch;
+  a.hn = c->hn;
+  a.g = c->g;
+  a.Umax = c->Umax;
+  a.budget = c->Bud;
+  a.Hq = c->Hq;
+  a.h0 = c->h0;
+  a.Bmax = c->Bmax;
+  a.trigger_ref = c->cfg.trigger_ref;
+  a.tau = c->cfg.tau;
+  a.qref = c->d_qref + (size_t)layer * 2 * c->Bmax * c->Hq * D;
+  a.r = c->d_r + (size_t)layer * c->Bmax;
+  a.step = c->d_step + layer;
+  a.flag = c->d_flag + (size_t)layer * c->Bmax;
+  a.inst = c->d_inst + ib;
+  a.centb = c->d_centb + ib * c->Umax * D;
+  a.usize = c->d_usize + ib * c->Umax;
+  a.uoff = c->d_uoff + ib * c->Umax;
+  a.sel = c->d_sel + ib * c->Umax;
+  a.seloff = c->d_seloff + ib * c->Umax;
+  a.pool = c->d_pool + ib * c->pool_inst_bytes;
+  a.pool_inst_bytes = c->pool_inst_bytes;
+  a.ws = c->d_ws;
+  a.ws_buf_stride = c->ws_buf_stride;
+  a.ws_inst_stride = c->ws_inst_stride;
+  a.inst_global_base = ib;
+  a.scratch_e = c->d_se;
+  a.scratch_sort = c->d_ssort;
+  a.rows = c->d_rows;
+  a.stats = c->d_stats;
+  return a;
+}
 
 }  // namespace
 
@@ -213,11 +250,10 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_pool_pos, (size_t)ni * c->pool_rows_cap);
   ok = ok && dalloc(c, &c->d_flag, (size_t)c->L * c->Bmax);
   ok = ok && dalloc(c, &c->d_r, (size_t)c->L * c->Bmax);
-  ok = ok && dalloc(c, &c->d_qref, (size_t)c->L * c->Bmax * c->Hq * D);
+  ok = ok && dalloc(c, &c->d_qref, (size_t)c->L * 2 * c->Bmax * c->Hq * D);
   ok = ok && dalloc(c, &c->d_full, (size_t)c->n_f * nl * 2 * c->full_cap * D);
   ok = ok && dalloc(c, &c->d_se, (size_t)nl * g * c->Umax);
   ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 14);
-  ok = ok && dalloc(c, &c->d_jobs, (size_t)nl);
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
   ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
   ok = ok && dalloc(c, &c->d_counters, (size_t)nl);
@@ -279,7 +315,8 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   c->P[layer] = P;
   c->t[layer] = 0;
   c->stage[layer] = 0;
-  LKV_LAUNCH(c, cudaMemsetAsync(c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, 0, sizeof(bf16) * c->Bmax * c->Hq * D, st),
+  LKV_LAUNCH(c, cudaMemsetAsync(c->d_qref + (size_t)layer * 2 * c->Bmax * c->Hq * D, 0,
+                                 sizeof(bf16) * 2 * c->Bmax * c->Hq * D, st),
              "memset q_ref");
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_flag + (size_t)layer * c->Bmax, 0, c->Bmax, st), "memset flag");
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_step + layer, 0, sizeof(int), st), "memset step");
@@ -390,24 +427,22 @@ louiskv_status louiskv_should_retrieve(louiskv_ctx* c, int32_t layer, const void
   if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "should_retrieve: max_output_len reached");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int t = c->t[layer] + 1;
-  uint8_t* flag = c->d_flag + (size_t)layer * c->Bmax;
-  double* r = c->d_r + (size_t)layer * c->Bmax;
   if (is_full(c, layer)) {
-    LKV_LAUNCH(c, launch_copy_flags(nullptr, nullptr, flag, r, d_flag_out, d_r_out, c->batch, c->d_step + layer, st),
-               "flags");
-  } else if (c->cfg.boundary_mode == LOUISKV_BOUNDARY_SHARED && layer != c->cfg.shared_layer) {
-    const int sl = c->cfg.shared_layer;
-    if (c->t[sl] < t) return fail(c, LOUISKV_ERR_STATE, "SHARED: designated layer not yet called this step");
-    LKV_LAUNCH(c,
-               launch_copy_flags(c->d_flag + (size_t)sl * c->Bmax, c->d_r + (size_t)sl * c->Bmax, flag, r, d_flag_out,
-                                 d_r_out, c->batch, c->d_step + layer, st),
-               "flags");
+    // full-cache layers never retrieve; the step counter advances in append_output
+    if (d_flag_out) LKV_LAUNCH(c, cudaMemsetAsync(d_flag_out, 0, c->batch, st), "flags");
+    if (d_r_out) LKV_LAUNCH(c, cudaMemsetAsync(d_r_out, 0, sizeof(double) * c->batch, st), "r");
   } else {
-    LKV_LAUNCH(c,
-               launch_trigger(reinterpret_cast<const bf16*>(q_all), stride_b, c->batch, c->Hq,
-                              c->d_qref + (size_t)layer * c->Bmax * c->Hq * D, flag, r, d_flag_out, d_r_out,
-                              c->d_step + layer, c->cfg.tau, c->cfg.trigger_ref, st),
-               "trigger");
+    RetrieveArgs a = retrieve_args(c, layer, q_all, stride_b);
+    a.flag_out = d_flag_out;
+    a.r_out = d_r_out;
+    if (c->cfg.boundary_mode == LOUISKV_BOUNDARY_SHARED && layer != c->cfg.shared_layer) {
+      const int sl = c->cfg.shared_layer;
+      if (c->t[sl] < t) return fail(c, LOUISKV_ERR_STATE, "SHARED: designated layer not yet called this step");
+      a.shared_copy = 1;
+      a.flag_src = c->d_flag + (size_t)sl * c->Bmax;
+      a.r_src = c->d_r + (size_t)sl * c->Bmax;
+    }
+    LKV_LAUNCH(c, launch_trigger_logits(a, st), "trigger+logits");
   }
   c->t[layer] = t;
   c->stage[layer] = 1;
@@ -421,35 +456,9 @@ louiskv_status louiskv_retrieve(louiskv_ctx* c, int32_t layer, const void* q_own
   c->stage[layer] = 2;
   if (is_full(c, layer)) return LOUISKV_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t ib = inst_base(c, layer);
-  RetrieveArgs a{};
-  a.q_own = reinterpret_cast<const bf16*>(q_own);
-  a.stride_b = stride_b;
-  a.batch = c->batch;
-  a.hn = c->hn;
-  a.g = c->g;
-  a.Umax = c->Umax;
-  a.budget = c->Bud;
-  a.flag = c->d_flag + (size_t)layer * c->Bmax;
-  a.inst = c->d_inst + ib;
-  a.centb = c->d_centb + ib * c->Umax * D;
-  a.usize = c->d_usize + ib * c->Umax;
-  a.uoff = c->d_uoff + ib * c->Umax;
-  a.sel = c->d_sel + ib * c->Umax;
-  a.seloff = c->d_seloff + ib * c->Umax;
-  a.pool = c->d_pool + ib * c->pool_inst_bytes;
-  a.pool_inst_bytes = c->pool_inst_bytes;
-  a.ws = c->d_ws;
-  a.ws_buf_stride = c->ws_buf_stride;
-  a.ws_inst_stride = c->ws_inst_stride;
-  a.inst_global_base = ib;
-  a.scratch_e = c->d_se;
-  a.scratch_sort = c->d_ssort;
-  a.jobs = c->d_jobs;
-  a.rows = c->d_rows;
-  a.stats = c->d_stats;
-  LKV_LAUNCH(c, launch_score_select(a, st), "score_select");
-  LKV_LAUNCH(c, launch_gather(c->d_jobs, c->d_rows, c->batch * c->hn, std::max(c->Bud, 1), st), "gather");
+  RetrieveArgs a = retrieve_args(c, layer, q_own, stride_b);
+  a.budget = std::max(c->Bud, 0);
+  LKV_LAUNCH(c, launch_select_gather(a, st), "select+gather");
   return LOUISKV_OK;
 }
 
@@ -463,11 +472,11 @@ louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* 
 
   if (is_full(c, layer)) {
     LKV_LAUNCH(c,
-               launch_full_append(reinterpret_cast<const bf16*>(k_t), reinterpret_cast<const bf16*>(v_t), stride_b,
-                                  c->batch, c->hn,
-                                  c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D,
-                                  c->full_cap, c->P[layer], c->d_step + layer, c->d_error, st),
-               "full append");
+               launch_full_step(reinterpret_cast<const bf16*>(k_t), reinterpret_cast<const bf16*>(v_t), stride_b,
+                                c->batch, c->hn,
+                                c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D,
+                                c->full_cap, c->P[layer], c->d_step + layer, c->d_error, st),
+               "full step");
   } else {
     const int64_t ib = inst_base(c, layer);
     AppendArgs a{};
@@ -541,8 +550,12 @@ louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_
     a.ring_cap = c->ring_cap;
     max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
   }
-  // split-K: aim for ~2 waves of CTAs over 148 SMs, >= 64 rows per split
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((296 + n_ctas - 1) / n_ctas, max_rows / 64));
+  // split-K: ~2 CTAs per SM when the rows allow it; a split never ends with a tiny tail chunk
+  // (rows per split rounded to whole 64-row pipeline chunks)
+  const int64_t want = (296 + n_ctas - 1) / n_ctas;
+  const int64_t chunks = (max_rows + 63) / 64;
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
+  if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));
   a.splits = std::min(splits, c->max_splits);
   LKV_LAUNCH(c, launch_attn(a, st), "attn");
   return LOUISKV_OK;

@@ -106,20 +106,27 @@ __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   if (tid == 0) *S = s;
 }
 
-__global__ void full_append_kernel(const bf16* k_t, const bf16* v_t, int64_t stride_b, int hn, bf16* full,
-                                   int64_t full_cap, int64_t P, const int* step, int* error) {
-  const int li = blockIdx.x, b = li / hn, h = li % hn;
-  const int tid = threadIdx.x;  // 32 threads
-  const int64_t pos = P + *step - 1;
+// full-cache layer: append (k_t, v_t) at row P + t - 1 of every (b, head) and commit the
+// layer's step counter; one CTA so the read of t and its commit cannot race.
+__global__ void __launch_bounds__(256) full_step_kernel(const bf16* k_t, const bf16* v_t, int64_t stride_b, int n,
+                                                        int hn, bf16* full, int64_t full_cap, int64_t P, int* step,
+                                                        int* error) {
+  const int t = *step + 1;
+  const int64_t pos = P + t - 1;
   if (pos >= full_cap) {
-    if (tid == 0) *error = 1;
-    return;
+    if (threadIdx.x == 0) *error = 1;
+  } else {
+    for (int i = threadIdx.x; i < n * 32; i += blockDim.x) {
+      const int li = i >> 5, lane = i & 31, b = li / hn, h = li % hn;
+      bf16* K = full + (int64_t)li * 2 * full_cap * D;
+      bf16* V = K + full_cap * D;
+      const bf16* src = (lane < 16 ? k_t : v_t) + (int64_t)b * stride_b + (int64_t)h * D;
+      bf16* dst = (lane < 16 ? K : V) + pos * D;
+      reinterpret_cast<uint4*>(dst)[lane & 15] = reinterpret_cast<const uint4*>(src)[lane & 15];
+    }
   }
-  bf16* K = full + (int64_t)li * 2 * full_cap * D;
-  bf16* V = K + full_cap * D;
-  const bf16* src = (tid < 16 ? k_t : v_t) + (int64_t)b * stride_b + (int64_t)h * D;
-  bf16* dst = (tid < 16 ? K : V) + pos * D;
-  reinterpret_cast<uint4*>(dst)[tid & 15] = reinterpret_cast<const uint4*>(src)[tid & 15];
+  __syncthreads();
+  if (threadIdx.x == 0) *step = t;
 }
 
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st) {
@@ -127,9 +134,9 @@ cudaError_t launch_append(const AppendArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_full_append(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
-                               int64_t full_cap, int64_t P, const int* step, int* error, cudaStream_t st) {
-  full_append_kernel<<<batch * hn, 32, 0, st>>>(k_t, v_t, stride_b, hn, full, full_cap, P, step, error);
+cudaError_t launch_full_step(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
+                             int64_t full_cap, int64_t P, int* step, int* error, cudaStream_t st) {
+  full_step_kernel<<<1, 256, 0, st>>>(k_t, v_t, stride_b, batch * hn, hn, full, full_cap, P, step, error);
   return cudaGetLastError();
 }
 

@@ -46,19 +46,101 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
   return ((unsigned long long)hi << 32) | lo;
 }
 
-// ---- logits (recipe R2 step 1): one thread per unit, all g heads; spread over many CTAs
+// ---- should_retrieve: semantic-boundary trigger (recipe R1) fused with the
+// logits of the flagged instances (recipe R2 step 1). Grid (unit slices, b*hn). Every CTA recomputes
+// r_t of its sequence with the same fixed-order recipe (bit-identical), so no grid-wide dependency
+// is needed; the (slice 0, head 0) CTA publishes flag/r and writes the next q_ref buffer
+// (double-buffered by step parity so concurrent CTAs keep reading the old one).
+constexpr int TL_THREADS = 128;
 template <int G>
-__global__ void __launch_bounds__(128) logits_kernel(RetrieveArgs a) {
+__global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a) {
   const int li = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
-  if (!a.flag[b]) return;
-  const int n = a.inst[li].n_units;
-  if ((int)blockIdx.x * 128 >= n) return;
-  __shared__ float sq[G][D];
-  const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)h * G * D;
-  for (int i = threadIdx.x; i < G * D; i += 128) sq[i / D][i % D] = bf2f(qb[i]);
+  const int tid = threadIdx.x;
+  const int t = *a.step + 1;
+  const int par = t & 1;
+  __shared__ double s_cos[64];
+  __shared__ int s_flag;
+  __shared__ double s_r;
+  const uint16_t* qc = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b;
+  const uint16_t* qr_old = reinterpret_cast<const uint16_t*>(a.qref) + ((int64_t)(par ^ 1) * a.Bmax + b) * a.Hq * D;
+  if (a.shared_copy) {
+    if (tid == 0) {
+      s_flag = a.flag_src[b];
+      s_r = a.r_src[b];
+    }
+  } else {
+    // 16 lanes per head: lane l sums elements [8l, 8l+8) sequentially, then a fixed xor tree.
+    // Warp-uniform loop (two heads per warp); lanes past the last head shuffle zeros.
+    const int l16 = tid & 15, warp = tid >> 5, lane = tid & 31;
+    for (int hb = warp * 2; hb < a.Hq; hb += (TL_THREADS / 32) * 2) {
+      const int hh = hb + (lane >> 4);
+      const bool act = hh < a.Hq;
+      uint4 ua = make_uint4(0, 0, 0, 0), uc = ua;
+      if (act) {
+        ua = reinterpret_cast<const uint4*>(qr_old + hh * D)[l16];
+        uc = reinterpret_cast<const uint4*>(qc + hh * D)[l16];
+      }
+      float fa[8], fc[8];
+      unpack8(ua, fa);
+      unpack8(uc, fc);
+      double dot = 0.0, na = 0.0, nb = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double x = (double)fa[e], y = (double)fc[e];
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+      }
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) {
+        dot = __dadd_rn(dot, __shfl_xor_sync(0xffffffffu, dot, off));
+        na = __dadd_rn(na, __shfl_xor_sync(0xffffffffu, na, off));
+        nb = __dadd_rn(nb, __shfl_xor_sync(0xffffffffu, nb, off));
+      }
+      if (act && l16 == 0) {
+        double cs = 0.0;
+        if (na != 0.0 && nb != 0.0) {
+          cs = __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
+          cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
+        }
+        s_cos[hh] = cs;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int hh = 0; hh < a.Hq; ++hh) sum = __dadd_rn(sum, s_cos[hh]);
+      const double rr = __ddiv_rn(sum, (double)a.Hq);
+      s_r = rr;
+      s_flag = (t == 1) || (rr < a.tau);
+    }
+  }
   __syncthreads();
-  const int u = blockIdx.x * 128 + threadIdx.x;
+  const int flag = s_flag;
+  if (blockIdx.x == 0 && h == 0) {
+    if (tid == 0) {
+      a.flag[b] = (uint8_t)flag;
+      a.r[b] = s_r;
+      if (a.flag_out) a.flag_out[b] = (uint8_t)flag;
+      if (a.r_out) a.r_out[b] = s_r;
+    }
+    if (!a.shared_copy) {
+      // q_ref for step t+1: q_t (PREV_STEP, or a retrieval step) else the old reference
+      const uint4* src = reinterpret_cast<const uint4*>((a.trigger_ref == LOUISKV_TRIG_PREV_STEP || flag) ? qc : qr_old);
+      uint4* dst = reinterpret_cast<uint4*>(a.qref + ((int64_t)par * a.Bmax + b) * a.Hq * D);
+      for (int i = tid; i < a.Hq * D / 8; i += TL_THREADS) dst[i] = src[i];
+    }
+  }
+  if (!flag) return;
+  // ---- logits of the owned KV head's g query heads against this slice of units
+  const int n = a.inst[li].n_units;
+  if ((int)blockIdx.x * TL_THREADS >= n) return;
+  __shared__ float sq[G][D];
+  const uint16_t* qb = qc + (int64_t)(a.h0 + h) * G * D;
+  for (int i = tid; i < G * D; i += TL_THREADS) sq[i / D][i % D] = bf2f(qb[i]);
+  __syncthreads();
+  const int u = blockIdx.x * TL_THREADS + tid;
   if (u >= n) return;
   const uint4* row = reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D);
   uint4 cr[D / 8];
@@ -117,10 +199,9 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
   const int li = blockIdx.x;
   const int b = li / a.hn;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (!a.flag[b]) {
-    if (tid == 0) a.jobs[li].n_rows = 0;
-    return;
-  }
+  // commit the layer's device step counter (read by should_retrieve's kernel, then by append/attn)
+  if (li == 0 && tid == 0) *a.step = *a.step + 1;
+  if (!a.flag[b]) return;
   InstState* S = a.inst + li;
   const int n = S->n_units;
 
@@ -385,74 +466,70 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
   if (tid == 0) {
     atomicAdd(&a.stats->units_scored, (unsigned long long)n);
     if (li % a.hn == 0) atomicAdd(&a.stats->retrievals, 1ull);
-    a.jobs[li] = GatherJob{total, 0, nxtK, nxtV};
     S->ws_cur = nxt;
     S->ws_rows = total;
   }
-}
-
-constexpr int GA_THREADS = 256;
-constexpr int GA_ROWS_PER_PASS = GA_THREADS / 16;
-
-__global__ void __launch_bounds__(GA_THREADS) gather_kernel(const GatherJob* __restrict__ jobs,
-                                                            const RowSrc* __restrict__ rows, int budget) {
-  const int li = blockIdx.x;
-  const GatherJob J = jobs[li];
-  if (J.n_rows <= 0) return;
-  const RowSrc* R = rows + (int64_t)li * budget;
-  const int sub = threadIdx.x & 15;
-  int r = blockIdx.y * GA_ROWS_PER_PASS + (threadIdx.x >> 4);
-  const int stride = gridDim.y * GA_ROWS_PER_PASS;
-  uint4* dK = reinterpret_cast<uint4*>(J.dstK);
-  uint4* dV = reinterpret_cast<uint4*>(J.dstV);
-  // two rows in flight per thread per iteration (4 x 16 B loads outstanding)
-  for (; r < J.n_rows; r += 2 * stride) {
-    const int r2 = r + stride;
-    RowSrc s0 = R[r];
-    uint4 k0 = s0.k[sub], v0 = s0.v[sub];
-    uint4 k1, v1;
-    if (r2 < J.n_rows) {
-      RowSrc s1 = R[r2];
-      k1 = s1.k[sub];
-      v1 = s1.v[sub];
-    }
-    dK[(int64_t)r * (D / 8) + sub] = k0;
-    dV[(int64_t)r * (D / 8) + sub] = v0;
-    if (r2 < J.n_rows) {
-      dK[(int64_t)r2 * (D / 8) + sub] = k1;
-      dV[(int64_t)r2 * (D / 8) + sub] = v1;
+  __syncthreads();
+  // ---- gather (P:126 row-granular transfer): 16 lanes x 16 B per row, 2 rows in flight per thread;
+  // new units read zero-copy from the pinned host pool, kept units device-to-device
+  {
+    const int sub = tid & 15;
+    constexpr int RPP = SS_THREADS / 16;  // rows per pass
+    uint4* dK = reinterpret_cast<uint4*>(nxtK);
+    uint4* dV = reinterpret_cast<uint4*>(nxtV);
+    for (int r = tid >> 4; r < total; r += 2 * RPP) {
+      const int r2 = r + RPP;
+      const RowSrc s0 = rows[r];
+      const uint4 k0 = s0.k[sub], v0 = s0.v[sub];
+      uint4 k1 = k0, v1 = v0;
+      if (r2 < total) {
+        const RowSrc s1 = rows[r2];
+        k1 = s1.k[sub];
+        v1 = s1.v[sub];
+      }
+      dK[(int64_t)r * (D / 8) + sub] = k0;
+      dV[(int64_t)r * (D / 8) + sub] = v0;
+      if (r2 < total) {
+        dK[(int64_t)r2 * (D / 8) + sub] = k1;
+        dV[(int64_t)r2 * (D / 8) + sub] = v1;
+      }
     }
   }
 }
 
 template <int G>
-static cudaError_t launch_retrieve_g(const RetrieveArgs& a, cudaStream_t st) {
-  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
-  const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32) + 14ull * cap;
+static void set_attrs_once() {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(select_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  logits_kernel<G><<<dim3((a.Umax + 127) / 128, a.batch * a.hn), 128, 0, st>>>(a);
-  select_kernel<G><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a);
+}
+
+cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st) {
+  if (a.Hq > 64) return cudaErrorInvalidValue;
+  const dim3 grid((a.Umax + TL_THREADS - 1) / TL_THREADS, a.batch * a.hn);
+  switch (a.g) {
+    case 1: trig_logits_kernel<1><<<grid, TL_THREADS, 0, st>>>(a); break;
+    case 2: trig_logits_kernel<2><<<grid, TL_THREADS, 0, st>>>(a); break;
+    case 4: trig_logits_kernel<4><<<grid, TL_THREADS, 0, st>>>(a); break;
+    case 8: trig_logits_kernel<8><<<grid, TL_THREADS, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_score_select(const RetrieveArgs& a, cudaStream_t st) {
+cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st) {
+  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
+  const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32) + 14ull * cap;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
   switch (a.g) {
-    case 1: return launch_retrieve_g<1>(a, st);
-    case 2: return launch_retrieve_g<2>(a, st);
-    case 4: return launch_retrieve_g<4>(a, st);
-    case 8: return launch_retrieve_g<8>(a, st);
+    case 1: set_attrs_once<1>(); select_kernel<1><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
+    case 2: set_attrs_once<2>(); select_kernel<2><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
+    case 4: set_attrs_once<4>(); select_kernel<4><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
+    case 8: set_attrs_once<8>(); select_kernel<8><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
-}
-
-cudaError_t launch_gather(const GatherJob* jobs, const RowSrc* rows, int n_inst, int budget, cudaStream_t st) {
-  const int gy = budget >= 64 ? budget / 64 : 1;
-  gather_kernel<<<dim3(n_inst, gy), GA_THREADS, 0, st>>>(jobs, rows, budget);
   return cudaGetLastError();
 }
 

@@ -37,13 +37,6 @@ struct InstState {
   int32_t pad;
 };
 
-// One gather job per active instance (written by score_select, read by gather).
-struct GatherJob {
-  int32_t n_rows;
-  int32_t pad;
-  bf16* dstK;
-  bf16* dstV;
-};
 struct RowSrc {
   const uint4* k;
   const uint4* v;
@@ -55,21 +48,22 @@ struct StatsDev {
 };
 
 // ---------------------------------------------------------------- kernel launchers
-// trigger (k_trigger.cu)
-// Both kernels run as a single CTA and own the per-layer device step counter: they read
-// t = step[layer] + 1 and commit step[layer] = t at the end (graph-replay safe).
-cudaError_t launch_trigger(const bf16* q_all, int64_t stride_b, int batch, int Hq, bf16* q_ref, uint8_t* flag,
-                           double* r, uint8_t* flag_out, double* r_out, int* step, double tau, int trigger_ref,
-                           cudaStream_t st);
-cudaError_t launch_copy_flags(const uint8_t* src_flag, const double* src_r, uint8_t* flag, double* r,
-                              uint8_t* flag_out, double* r_out, int batch, int* step, cudaStream_t st);
-
 // retrieve (k_retrieve.cu)
 struct RetrieveArgs {
-  const bf16* q_own;
+  const bf16* q_own;         // (select) owned heads; (trigger+logits) = q_all
   int64_t stride_b;
   int batch, hn, g, Umax, budget;
-  const uint8_t* flag;       // [batch] of this layer
+  // trigger (fused into the logits kernel launched by should_retrieve)
+  int Hq, h0, Bmax, trigger_ref, shared_copy;
+  double tau;
+  bf16* qref;                // layer base [2][Bmax][Hq][D], read buffer (t-1)&1, write t&1
+  const uint8_t* flag_src;   // SHARED mode: designated layer's flags / r
+  const double* r_src;
+  double* r;                 // [batch] of this layer
+  uint8_t* flag_out;         // optional caller outputs
+  double* r_out;
+  int* step;                 // device step counter of this layer (read by both, committed by select)
+  uint8_t* flag;             // [batch] of this layer
   InstState* inst;           // layer base, [batch*hn]
   const bf16* centb;         // layer base [batch*hn][Umax][D]
   const int32_t* usize;      // [batch*hn][Umax]
@@ -84,12 +78,13 @@ struct RetrieveArgs {
   int64_t inst_global_base;  // global instance index of this layer's first instance
   float* scratch_e;          // [batch*hn][g][Umax]
   uint8_t* scratch_sort;     // [batch*hn][Umax * 14] sort buffers when n exceeds the smem capacity
-  GatherJob* jobs;           // [batch*hn]
   RowSrc* rows;              // [batch*hn][B]
   StatsDev* stats;
 };
-cudaError_t launch_score_select(const RetrieveArgs& a, cudaStream_t st);
-cudaError_t launch_gather(const GatherJob* jobs, const RowSrc* rows, int n_inst, int budget, cudaStream_t st);
+// should_retrieve on a retrieval layer: r_t / flag (recipe R1) + logits of flagged instances
+cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st);
+// retrieve: select (sort + greedy) + working-set layout + gather; commits the step counter
+cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st);
 
 // append (k_append.cu)
 struct AppendArgs {
@@ -115,8 +110,9 @@ struct AppendArgs {
   StatsDev* stats;
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);
-cudaError_t launch_full_append(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
-                               int64_t full_cap, int64_t P, const int* step, int* error, cudaStream_t st);
+// full-cache layer step: append (k_t, v_t) at P + t - 1 and commit the step counter (one CTA)
+cudaError_t launch_full_step(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
+                             int64_t full_cap, int64_t P, int* step, int* error, cudaStream_t st);
 
 // attention (k_attn.cu)
 struct AttnArgs {
