@@ -16,6 +16,7 @@
 namespace lkv {
 
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.x;
   const int b = li / a.hn;
   const int tid = threadIdx.x;
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
 __global__ void __launch_bounds__(256) full_step_kernel(const bf16* k_t, const bf16* v_t, int64_t stride_b, int n,
                                                         int hn, bf16* full, int64_t full_cap, int64_t P, int* step,
                                                         int* error) {
+  pdl_wait_trigger();
   const int t = *step + 1;
   const int64_t pos = P + t - 1;
   if (pos >= full_cap) {
@@ -130,13 +132,13 @@ __global__ void __launch_bounds__(256) full_step_kernel(const bf16* k_t, const b
 }
 
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st) {
-  append_kernel<<<a.batch * a.hn, 128, 0, st>>>(a);
+  launch_k(append_kernel, dim3(a.batch * a.hn), dim3(128), 0, st, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_full_step(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
                              int64_t full_cap, int64_t P, int* step, int* error, cudaStream_t st) {
-  full_step_kernel<<<1, 256, 0, st>>>(k_t, v_t, stride_b, batch * hn, hn, full, full_cap, P, step, error);
+  launch_k(full_step_kernel, dim3(1), dim3(256), 0, st, k_t, v_t, stride_b, batch * hn, hn, full, full_cap, P, step, error);
   return cudaGetLastError();
 }
 

@@ -50,6 +50,7 @@ __device__ __forceinline__ void row_ptrs(const RowSpan& sp, int r, const uint4*&
 
 template <int G>
 __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.x, split = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
   const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
@@ -347,10 +348,10 @@ cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
     attr = true;
   }
   switch (a.g) {
-    case 1: attn_kernel<1><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
-    case 2: attn_kernel<2><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
-    case 4: attn_kernel<4><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
-    case 8: attn_kernel<8><<<grid, AT_THREADS, AT_SMEM, st>>>(a); break;
+    case 1: launch_k(attn_kernel<1>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
+    case 2: launch_k(attn_kernel<2>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
+    case 4: launch_k(attn_kernel<4>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
+    case 8: launch_k(attn_kernel<8>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -48,6 +48,7 @@ __device__ __forceinline__ const bf16* vrow(const KmArgs& a, int li, int i) {
 
 // ---- init: C_j = x_{floor(j N / k)}; bf16 copy; ½||C_j||²  (warp per cluster)
 __global__ void km_init_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 4 + warp;
@@ -74,6 +75,7 @@ __global__ void km_init_kernel(KmArgs a) {
 
 // ---- +inf half-norms (-inf GEMM extension) for the padded centroid columns [kc, hstride)
 __global__ void km_half_pad_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   for (int j = a.kc + threadIdx.x; j < a.hstride; j += blockDim.x) {
     a.half[(int64_t)li * a.hstride + j] = INFINITY;
@@ -84,6 +86,7 @@ __global__ void km_half_pad_kernel(KmArgs a) {
 // ---- SIMT assignment (correctness reference path; the tcgen05 kernel is the fast path)
 constexpr int AS_TILE = 32;
 __global__ void __launch_bounds__(128) km_assign_simt_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int i = blockIdx.x * 128 + threadIdx.x;
   __shared__ uint32_t sc[AS_TILE][D / 2];
@@ -133,6 +136,7 @@ __global__ void __launch_bounds__(128) km_assign_simt_kernel(KmArgs a) {
 
 // ---- per-chunk histogram
 __global__ void __launch_bounds__(256) km_hist_kernel(KmArgs a, int nchunk) {
+  pdl_wait_trigger();
   extern __shared__ int hist[];
   const int li = blockIdx.y, c = blockIdx.x;
   for (int j = threadIdx.x; j < a.kc; j += blockDim.x) hist[j] = 0;
@@ -227,11 +231,13 @@ __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) km_scan_kernel(KmArgs a, int nchunk) { km_scan_block(a, blockIdx.x, nchunk); }
+__global__ void __launch_bounds__(1024) km_scan_kernel(KmArgs a, int nchunk) {
+  pdl_wait_trigger(); km_scan_block(a, blockIdx.x, nchunk); }
 
 // column scan (many CTAs): warp per cluster, lanes over chunks: exclusive prefix of the cluster's
 // chunk counts -> chunk-major ccT[inst][chunk][cluster] (coalesced reads for the scatter), count
 __global__ void __launch_bounds__(256) km_colscan_kernel(KmArgs a, int nchunk, int only_dirty) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   if (only_dirty && a.flags[li] != 2) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(256) km_colscan_kernel(KmArgs a, int nchunk, i
 
 // cluster offsets and update-task offsets from the counts (one CTA per instance)
 __global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dirty) {
+  pdl_wait_trigger();
   const int li = blockIdx.x;
   if (only_dirty && a.flags[li] != 2) return;
   const int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
@@ -297,6 +304,7 @@ __global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dir
 // If the walk runs out of candidates (many ineligible), the slow per-empty scan finishes the job.
 constexpr int RP_CAND = 2048;
 __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
+  pdl_wait_trigger();
   const int li = blockIdx.x;
   if (!a.flags[li]) return;
   extern __shared__ int rp_smem[];
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
 
 // stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
 __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
+  pdl_wait_trigger();
   extern __shared__ int base[];  // [kc] running offsets of this chunk
   const int li = blockIdx.y, c = blockIdx.x, lane = threadIdx.x;
   const int32_t* ccT = a.ccT + ((int64_t)li * a.nchunk_max + c) * a.kmax;
@@ -526,6 +535,7 @@ __device__ __forceinline__ void km_write_centroid(const KmArgs& a, int li, int j
 }
 
 __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 4 + warp;
@@ -568,6 +578,7 @@ __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
 }
 
 __global__ void __launch_bounds__(128) km_finalize_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 4 + warp;
@@ -589,6 +600,7 @@ __global__ void __launch_bounds__(128) km_finalize_kernel(KmArgs a) {
 
 // caller-supplied clustering: copy assignment and centroids in
 __global__ void km_ext_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.N; t += (int64_t)gridDim.x * blockDim.x)
     a.assign[(int64_t)li * a.Nmax + t] = a.ext_assign[(int64_t)li * a.N + t];
@@ -602,6 +614,7 @@ __global__ void km_ext_kernel(KmArgs a) {
 
 // offload: pool row r (cluster-major order) <- key perm[r]; unit-major spans [K rows | V rows]
 __global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int r = blockIdx.x * 8 + (threadIdx.x >> 4), sub = threadIdx.x & 15;
   if (r >= a.N) return;
@@ -618,6 +631,7 @@ __global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a) {
 
 // unit table + instance reset after clustering
 __global__ void km_units_kernel(KmArgs a, int P) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
@@ -641,6 +655,7 @@ __global__ void km_units_kernel(KmArgs a, int P) {
 
 // sinks [0, S) stay on the device
 __global__ void km_sinks_kernel(KmArgs a, int s_eff) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
   const int r = blockIdx.x * 8 + (threadIdx.x >> 4), sub = threadIdx.x & 15;
@@ -654,6 +669,7 @@ __global__ void km_sinks_kernel(KmArgs a, int s_eff) {
 }
 
 __global__ void reset_insts_kernel(InstState* inst, int n, int P, int s_eff) {
+  pdl_wait_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   InstState s{};
@@ -665,16 +681,16 @@ __global__ void reset_insts_kernel(InstState* inst, int n, int P, int s_eff) {
 cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st);  // k_kmeans_tc.cu
 
 static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool repair, cudaStream_t st) {
-  km_hist_kernel<<<dim3(nchunk, ni), 256, sizeof(int) * a.kc, st>>>(a, nchunk);
-  km_colscan_kernel<<<dim3((a.kc + 7) / 8, ni), 256, 0, st>>>(a, nchunk, 0);
-  km_offsets_kernel<<<ni, 1024, 0, st>>>(a, 0);
+  launch_k(km_hist_kernel, dim3(dim3(nchunk, ni)), dim3(256), sizeof(int) * a.kc, st, a, nchunk);
+  launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 0);
+  launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 0);
   if (repair) {
     const size_t rsm = sizeof(int) * (2 * a.kc) + RP_CAND * (sizeof(unsigned long long) + sizeof(int));
-    km_repair_kernel<<<ni, 1024, rsm, st>>>(a, nchunk);
-    km_colscan_kernel<<<dim3((a.kc + 7) / 8, ni), 256, 0, st>>>(a, nchunk, 1);
-    km_offsets_kernel<<<ni, 1024, 0, st>>>(a, 1);
+    launch_k(km_repair_kernel, dim3(ni), dim3(1024), rsm, st, a, nchunk);
+    launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 1);
+    launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);
   }
-  km_scatter_kernel<<<dim3(nchunk, ni), 32, sizeof(int) * a.kc, st>>>(a);
+  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), sizeof(int) * a.kc, st, a);
   return cudaGetLastError();
 }
 
@@ -683,9 +699,9 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
   const int P = a.S + a.N;
   const int s_eff = min(a.S_cap, P);
   cudaError_t e;
-  if (s_eff > 0) km_sinks_kernel<<<dim3((s_eff + 7) / 8, ni), 128, 0, st>>>(a, s_eff);
+  if (s_eff > 0) launch_k(km_sinks_kernel, dim3(dim3((s_eff + 7) / 8, ni)), dim3(128), 0, st, a, s_eff);
   if (a.N <= 0 || a.kc <= 0) {
-    reset_insts_kernel<<<(ni + 127) / 128, 128, 0, st>>>(a.inst, ni, P, s_eff);
+    launch_k(reset_insts_kernel, dim3((ni + 127) / 128), dim3(128), 0, st, a.inst, ni, P, s_eff);
     return cudaGetLastError();
   }
   static bool attr = false;
@@ -698,11 +714,11 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
   const int nchunk = (a.N + KM_CHUNK - 1) / KM_CHUNK;
   const dim3 gk((a.kc + 3) / 4, ni);
   if (a.ext_assign) {
-    km_ext_kernel<<<dim3(64, ni), 256, 0, st>>>(a);
+    launch_k(km_ext_kernel, dim3(dim3(64, ni)), dim3(256), 0, st, a);
     if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
   } else {
-    km_init_kernel<<<gk, 128, 0, st>>>(a);
-    km_half_pad_kernel<<<dim3(1, ni), 256, 0, st>>>(a);
+    launch_k(km_init_kernel, dim3(gk), dim3(128), 0, st, a);
+    launch_k(km_half_pad_kernel, dim3(dim3(1, ni)), dim3(256), 0, st, a);
     for (int it = 0; it < a.iters; ++it) {
       bool done = false;
       if (a.impl == LOUISKV_KMEANS_TC && kmeans_tc_available()) {
@@ -711,20 +727,21 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
         else if (e != cudaErrorNotSupported) return e;
         else cudaGetLastError();
       }
-      if (!done) km_assign_simt_kernel<<<dim3((a.N + 127) / 128, ni), 128, 0, st>>>(a);
+      if (!done) launch_k(km_assign_simt_kernel, dim3(dim3((a.N + 127) / 128, ni)), dim3(128), 0, st, a);
       ++*(done ? tc_iters : simt_iters);
       if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
-      km_update_kernel<<<dim3((a.task_max + 3) / 4, ni), 128, 0, st>>>(a);
-      km_finalize_kernel<<<gk, 128, 0, st>>>(a);
+      launch_k(km_update_kernel, dim3(dim3((a.task_max + 3) / 4, ni)), dim3(128), 0, st, a);
+      launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
     }
   }
-  km_offload_kernel<<<dim3((a.N + 7) / 8, ni), 128, 0, st>>>(a);
-  km_units_kernel<<<dim3((a.kc + 255) / 256, ni), 256, 0, st>>>(a, P);
+  launch_k(km_offload_kernel, dim3(dim3((a.N + 7) / 8, ni)), dim3(128), 0, st, a);
+  launch_k(km_units_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, P);
   return cudaGetLastError();
 }
 
 __global__ void full_prompt_kernel(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int hn,
                                    int64_t P, bf16* full, int64_t full_cap) {
+  pdl_wait_trigger();
   const int li = blockIdx.y, b = li / hn, h = li % hn;
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 4);
   const int sub = threadIdx.x & 15;
@@ -738,13 +755,13 @@ __global__ void full_prompt_kernel(const bf16* k, const bf16* v, int64_t sb, int
 cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int batch, int hn,
                                int64_t P, bf16* full, int64_t full_cap, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
-  full_prompt_kernel<<<dim3((unsigned)((P + 7) / 8), batch * hn), 128, 0, st>>>(k, v, sb, st_, sh, hn, P, full,
+  launch_k(full_prompt_kernel, dim3(dim3((unsigned)((P + 7) / 8), batch * hn)), dim3(128), 0, st, k, v, sb, st_, sh, hn, P, full,
                                                                                 full_cap);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st) {
-  reset_insts_kernel<<<(n + 127) / 128, 128, 0, st>>>(inst, n, P, s_eff);
+  launch_k(reset_insts_kernel, dim3((n + 127) / 128), dim3(128), 0, st, inst, n, P, s_eff);
   return cudaGetLastError();
 }
 

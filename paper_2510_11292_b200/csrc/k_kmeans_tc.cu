@@ -136,6 +136,7 @@ struct TcParams {
 __global__ void __launch_bounds__(THREADS, 1)
     kmeans_assign_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             const __grid_constant__ CUtensorMap tmBx, TcParams p) {
+  pdl_wait_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                              // [2][A_BYTES]
@@ -475,7 +476,7 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int items = ni * p.n_mblk;
   const int grid = items < sms ? items : sms;
-  tc::kmeans_assign_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(tmA, tmB, tmBx, p);
+  launch_k(tc::kmeans_assign_tc_kernel, dim3(grid), dim3(tc::THREADS), tc::SMEM_BYTES, st, tmA, tmB, tmBx, p);
   return cudaGetLastError();
 }
 

@@ -54,6 +54,7 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
 constexpr int TL_THREADS = 128;
 template <int G>
 __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
   const int tid = threadIdx.x;
@@ -196,6 +197,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 // ---- group scores, sort, budgeted greedy, working-set layout: one CTA per flagged instance
 template <int G>
 __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
+  pdl_wait_trigger();
   const int li = blockIdx.x;
   const int b = li / a.hn;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -510,10 +512,10 @@ cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st) {
   if (a.Hq > 64) return cudaErrorInvalidValue;
   const dim3 grid((a.Umax + TL_THREADS - 1) / TL_THREADS, a.batch * a.hn);
   switch (a.g) {
-    case 1: trig_logits_kernel<1><<<grid, TL_THREADS, 0, st>>>(a); break;
-    case 2: trig_logits_kernel<2><<<grid, TL_THREADS, 0, st>>>(a); break;
-    case 4: trig_logits_kernel<4><<<grid, TL_THREADS, 0, st>>>(a); break;
-    case 8: trig_logits_kernel<8><<<grid, TL_THREADS, 0, st>>>(a); break;
+    case 1: launch_k(trig_logits_kernel<1>, dim3(grid), dim3(TL_THREADS), 0, st, a); break;
+    case 2: launch_k(trig_logits_kernel<2>, dim3(grid), dim3(TL_THREADS), 0, st, a); break;
+    case 4: launch_k(trig_logits_kernel<4>, dim3(grid), dim3(TL_THREADS), 0, st, a); break;
+    case 8: launch_k(trig_logits_kernel<8>, dim3(grid), dim3(TL_THREADS), 0, st, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -524,10 +526,10 @@ cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st) {
   const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32) + 14ull * cap;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   switch (a.g) {
-    case 1: set_attrs_once<1>(); select_kernel<1><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
-    case 2: set_attrs_once<2>(); select_kernel<2><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
-    case 4: set_attrs_once<4>(); select_kernel<4><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
-    case 8: set_attrs_once<8>(); select_kernel<8><<<a.batch * a.hn, SS_THREADS, smem, st>>>(a); break;
+    case 1: set_attrs_once<1>(); launch_k(select_kernel<1>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 2: set_attrs_once<2>(); launch_k(select_kernel<2>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 4: set_attrs_once<4>(); launch_k(select_kernel<4>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 8: set_attrs_once<8>(); launch_k(select_kernel<8>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "louiskv.h"
@@ -195,6 +196,24 @@ cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStr
 
 bool kmeans_tc_available();
 
+// Launch with the programmatic-stream-serialization attribute (PDL); captured into CUDA graphs as
+// programmatic edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 }  // namespace lkv
 
 // ---------------------------------------------------------------- device helpers
@@ -211,6 +230,16 @@ __device__ __forceinline__ void unpack8(const uint4 u, float* f) {
   f[6] = __uint_as_float(u.w << 16);
   f[7] = __uint_as_float(u.w & 0xFFFF0000u);
 }
+// ---- programmatic dependent launch: every kernel waits for its predecessor grid (memory visible)
+// before touching shared state, then lets its dependent grid launch early (the launch latency of the
+// next kernel overlaps this one; the dependent still waits at its own griddepcontrol.wait)
+__device__ __forceinline__ void pdl_wait_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef LKV_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // ---- mbarrier / bulk-copy (TMA engine) helpers
 __device__ __forceinline__ uint32_t ptx_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void ptx_mbar_init(uint64_t* bar, uint32_t count) {
