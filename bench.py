@@ -270,10 +270,16 @@ def main():
             ctx.retrieve(l, q_in[l])
             if events is not None:
                 events[4 * l + 2].record()
-            ctx.append_output(l, k_in[l], v_in[l])
-            if events is not None:
-                events[4 * l + 3].record()
-            ctx.sparse_attn(l, q_in[l], out[l])
+            if l in full:
+                # full-cache layer: separate calls so the attention launch is isolated by the events
+                ctx.append_output(l, k_in[l], v_in[l])
+                if events is not None:
+                    events[4 * l + 3].record()
+                ctx.sparse_attn(l, q_in[l], out[l])
+            else:
+                if events is not None:
+                    events[4 * l + 3].record()
+                ctx.append_attn(l, k_in[l], v_in[l], q_in[l], out[l])
         if events is not None:
             events[4 * L].record()
 
@@ -294,7 +300,8 @@ def main():
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=cap_stream):
         issue_step()
-    launches_per_step = sum(3 if l in full else 5 for l in range(L))
+    # retrieval layer: trigger+logits, select+gather, clustered append+attention; full layer: step, attention
+    launches_per_step = sum(2 if l in full else 3 for l in range(L))
 
     for _ in range(W):
         load(step_idx)
@@ -346,9 +353,10 @@ def main():
     graph2 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph2, stream=cap_stream):
         issue_step(evs)
-    phase = {"trigger": 0.0, "retrieve": 0.0, "append": 0.0, "attn_sparse": 0.0, "attn_full": 0.0}
+    # phases (ms per step): should_retrieve = trigger + logits, retrieve = select + gather,
+    # append_attn = clustered append + attention (retrieval layers) / full-cache step + attention
+    phase = {"should_retrieve": 0.0, "retrieve": 0.0, "append_attn_sparse": 0.0, "append_attn_full": 0.0}
     attn_full_launch_ms, n_full_launch = 0.0, 0
-    attn_sparse_launch = []
     retr_step_ms = []
     st_c = ctx.stats()
     for i in range(A):
@@ -360,18 +368,15 @@ def main():
         for l in range(L):
             t_trig = evs[4 * l].elapsed_time(evs[4 * l + 1])
             t_ret = evs[4 * l + 1].elapsed_time(evs[4 * l + 2])
-            t_app = evs[4 * l + 2].elapsed_time(evs[4 * l + 3])
             t_att = evs[4 * l + 3].elapsed_time(evs[4 * l + 4])
-            phase["trigger"] += t_trig
-            phase["append"] += t_app
+            phase["should_retrieve"] += t_trig
             if l in full:
-                phase["attn_full"] += t_att
+                phase["append_attn_full"] += t_att
                 attn_full_launch_ms += t_att
                 n_full_launch += 1
             else:
                 phase["retrieve"] += t_ret
-                phase["attn_sparse"] += t_att
-                attn_sparse_launch.append(t_att)
+                phase["append_attn_sparse"] += t_att
                 rs += t_ret
         retr_step_ms.append(rs)
     st_d = ctx.stats()
@@ -408,7 +413,7 @@ def main():
                      "achieved": att_full_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": att_full_gbs / hbm_peak,
                      "traffic": None, "bytes_per_launch": full_bytes, "ms_per_launch": attn_full_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
-                     "share_of_step": phase["attn_full"] / step_ms_attr}
+                     "share_of_step": phase["append_attn_full"] / step_ms_attr}
     roofline_gather = {"kernel": "score_select + gather (retrieve)", "bound": "host_link",
                        "achieved": gather_gbs, "peak": host_link_gbs, "unit": "GB/s",
                        "frac": gather_gbs / host_link_gbs if host_link_gbs else None,

@@ -154,6 +154,15 @@ louiskv_status louiskv_append_output(louiskv_ctx* ctx, int32_t layer, const void
 louiskv_status louiskv_sparse_attn(louiskv_ctx* ctx, int32_t layer, const void* q_own, int64_t stride_b,
                                    void* out, float* out_f32, void* stream);
 
+/* Fused equivalent of louiskv_append_output followed by louiskv_sparse_attn (identical results):
+ * on a retrieval layer one clustered launch (8 CTAs per (b, owned head); rank 0 runs the
+ * seal/append/evict of store_cache, the cluster barrier publishes the local buffer, all ranks
+ * attend their split, rank 0 merges the partials through distributed shared memory). On a
+ * full-cache layer it issues the two calls. Arguments as in the two calls. Errors: as there. */
+louiskv_status louiskv_append_attn(louiskv_ctx* ctx, int32_t layer, const void* k_t, const void* v_t,
+                                   int64_t stride_kv, const void* q_own, int64_t stride_q, void* out,
+                                   float* out_f32, void* stream);
+
 /* ---- introspection (synchronous: they synchronise the device) ---- */
 /* Current working-set unit ids of (layer, b, owned head h), ascending. */
 louiskv_status louiskv_get_selection(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,

@@ -29,6 +29,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE"
 # ABI symbols declared in include/louiskv.h (checked by tests/test_abi.py)
 SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louiskv_set_prompt_units",
            "louiskv_should_retrieve", "louiskv_retrieve", "louiskv_append_output", "louiskv_sparse_attn",
+           "louiskv_append_attn",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
            "louiskv_get_stats", "louiskv_last_error", "louiskv_version"]
 
@@ -80,6 +81,7 @@ def lib():
         L.louiskv_retrieve.argtypes = [vp, i32, vp, i64, vp]
         L.louiskv_append_output.argtypes = [vp, i32, vp, vp, i64, vp]
         L.louiskv_sparse_attn.argtypes = [vp, i32, vp, i64, vp, vp, vp]
+        L.louiskv_append_attn.argtypes = [vp, i32, vp, vp, i64, vp, i64, vp, vp, vp]
         L.louiskv_get_selection.argtypes = [vp, i32, i32, i32, vp, i32, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_units.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_unit_positions.argtypes = [vp, i32, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64)]
@@ -191,6 +193,12 @@ class Context:
     def sparse_attn(self, layer, q_own, out, out_f32=None, stream=None):
         self._chk(self._L.louiskv_sparse_attn(self.h, layer, _ptr(q_own), q_own.stride(0), _ptr(out), _ptr(out_f32),
                                               _stream(stream)))
+
+    def append_attn(self, layer, k_t, v_t, q_own, out, out_f32=None, stream=None):
+        """Fused append_output + sparse_attn (one clustered launch on retrieval layers)."""
+        assert k_t.stride(0) == v_t.stride(0)
+        self._chk(self._L.louiskv_append_attn(self.h, layer, _ptr(k_t), _ptr(v_t), k_t.stride(0), _ptr(q_own),
+                                              q_own.stride(0), _ptr(out), _ptr(out_f32), _stream(stream)))
 
     # --- introspection ------------------------------------------------------
     def get_selection(self, layer, b, h):

@@ -155,6 +155,81 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   return a;
 }
 
+AppendArgs append_args(louiskv_ctx* c, int layer, const void* k_t, const void* v_t, int64_t stride_b) {
+  const int64_t ib = inst_base(c, layer);
+  AppendArgs a{};
+  a.k_t = reinterpret_cast<const bf16*>(k_t);
+  a.v_t = reinterpret_cast<const bf16*>(v_t);
+  a.stride_b = stride_b;
+  a.batch = c->batch;
+  a.hn = c->hn;
+  a.step = c->d_step + layer;
+  a.W = c->W;
+  a.max_open = c->max_open;
+  a.ring_cap = c->ring_cap;
+  a.Umax = c->Umax;
+  a.flag = c->d_flag + (size_t)layer * c->Bmax;
+  a.inst = c->d_inst + ib;
+  a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
+  a.fifo = c->d_fifo + ib * c->ring_cap;
+  a.cent = c->d_cent + ib * c->Umax * D;
+  a.centb = c->d_centb + ib * c->Umax * D;
+  a.usize = c->d_usize + ib * c->Umax;
+  a.uoff = c->d_uoff + ib * c->Umax;
+  a.ufirst = c->d_ufirst + ib * c->Umax;
+  a.sel = c->d_sel + ib * c->Umax;
+  a.pool_pos = c->d_pool_pos + ib * c->pool_rows_cap;
+  a.pool_rows_cap = c->pool_rows_cap;
+  a.pool = c->d_pool + ib * c->pool_inst_bytes;
+  a.pool_inst_bytes = c->pool_inst_bytes;
+  a.stats = c->d_stats;
+  return a;
+}
+
+AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_b, void* out, float* out_f32) {
+  AttnArgs a{};
+  a.q_own = reinterpret_cast<const bf16*>(q_own);
+  a.stride_b = stride_b;
+  a.batch = c->batch;
+  a.hn = c->hn;
+  a.g = c->g;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  a.out = reinterpret_cast<bf16*>(out);
+  a.out_f32 = out_f32;
+  a.part = c->d_part;
+  a.counters = c->d_counters;
+  const int n_ctas = c->batch * c->hn;
+  int64_t max_rows;
+  if (is_full(c, layer)) {
+    a.full = c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D;
+    a.full_cap = c->full_cap;
+    a.full_P = c->P[layer];
+    a.step = c->d_step + layer;
+    max_rows = c->P[layer] + c->t[layer];
+  } else {
+    const int64_t ib = inst_base(c, layer);
+    a.inst = c->d_inst + ib;
+    a.sinks = c->d_sinks + ib * 2 * std::max(c->S, 1) * D;
+    a.S = std::max(c->S, 1);
+    a.ws = c->d_ws;
+    a.ws_buf_stride = c->ws_buf_stride;
+    a.ws_inst_stride = c->ws_inst_stride;
+    a.inst_global_base = ib;
+    a.B = std::max(c->Bud, 1);
+    a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
+    a.ring_cap = c->ring_cap;
+    max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
+  }
+  // split-K: ~2 CTAs per SM when the rows allow it; a split never ends with a tiny tail chunk
+  // (rows per split rounded to whole 64-row pipeline chunks)
+  const int64_t want = (296 + n_ctas - 1) / n_ctas;
+  const int64_t chunks = (max_rows + 63) / 64;
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
+  if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));
+  a.splits = std::min(splits, c->max_splits);
+  return a;
+}
+
 }  // namespace
 
 extern "C" {
@@ -478,33 +553,7 @@ louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* 
                                 c->full_cap, c->P[layer], c->d_step + layer, c->d_error, st),
                "full step");
   } else {
-    const int64_t ib = inst_base(c, layer);
-    AppendArgs a{};
-    a.k_t = reinterpret_cast<const bf16*>(k_t);
-    a.v_t = reinterpret_cast<const bf16*>(v_t);
-    a.stride_b = stride_b;
-    a.batch = c->batch;
-    a.hn = c->hn;
-    a.step = c->d_step + layer;
-    a.W = c->W;
-    a.max_open = c->max_open;
-    a.ring_cap = c->ring_cap;
-    a.Umax = c->Umax;
-    a.flag = c->d_flag + (size_t)layer * c->Bmax;
-    a.inst = c->d_inst + ib;
-    a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
-    a.fifo = c->d_fifo + ib * c->ring_cap;
-    a.cent = c->d_cent + ib * c->Umax * D;
-    a.centb = c->d_centb + ib * c->Umax * D;
-    a.usize = c->d_usize + ib * c->Umax;
-    a.uoff = c->d_uoff + ib * c->Umax;
-    a.ufirst = c->d_ufirst + ib * c->Umax;
-    a.sel = c->d_sel + ib * c->Umax;
-    a.pool_pos = c->d_pool_pos + ib * c->pool_rows_cap;
-    a.pool_rows_cap = c->pool_rows_cap;
-    a.pool = c->d_pool + ib * c->pool_inst_bytes;
-    a.pool_inst_bytes = c->pool_inst_bytes;
-    a.stats = c->d_stats;
+    AppendArgs a = append_args(c, layer, k_t, v_t, stride_b);
     LKV_LAUNCH(c, launch_append(a, st), "append");
   }
   c->stage[layer] = 3;
@@ -517,47 +566,30 @@ louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_
   if (layer < 0 || layer >= c->L || !q_own || !out) return fail(c, LOUISKV_ERR_INVALID_ARG, "sparse_attn: bad args");
   if (c->stage[layer] != 3) return fail(c, LOUISKV_ERR_STATE, "sparse_attn must follow append_output");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  AttnArgs a{};
-  a.q_own = reinterpret_cast<const bf16*>(q_own);
-  a.stride_b = stride_b;
-  a.batch = c->batch;
-  a.hn = c->hn;
-  a.g = c->g;
-  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-  a.out = reinterpret_cast<bf16*>(out);
-  a.out_f32 = out_f32;
-  a.part = c->d_part;
-  a.counters = c->d_counters;
-  const int n_ctas = c->batch * c->hn;
-  int64_t max_rows;
-  if (is_full(c, layer)) {
-    a.full = c->d_full + (size_t)c->fidx[layer] * c->inst_per_layer * 2 * c->full_cap * D;
-    a.full_cap = c->full_cap;
-    a.full_P = c->P[layer];
-    a.step = c->d_step + layer;
-    max_rows = c->P[layer] + c->t[layer];
-  } else {
-    const int64_t ib = inst_base(c, layer);
-    a.inst = c->d_inst + ib;
-    a.sinks = c->d_sinks + ib * 2 * std::max(c->S, 1) * D;
-    a.S = std::max(c->S, 1);
-    a.ws = c->d_ws;
-    a.ws_buf_stride = c->ws_buf_stride;
-    a.ws_inst_stride = c->ws_inst_stride;
-    a.inst_global_base = ib;
-    a.B = std::max(c->Bud, 1);
-    a.ring = c->d_ring + ib * 2 * c->ring_cap * D;
-    a.ring_cap = c->ring_cap;
-    max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
-  }
-  // split-K: ~2 CTAs per SM when the rows allow it; a split never ends with a tiny tail chunk
-  // (rows per split rounded to whole 64-row pipeline chunks)
-  const int64_t want = (296 + n_ctas - 1) / n_ctas;
-  const int64_t chunks = (max_rows + 63) / 64;
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
-  if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));
-  a.splits = std::min(splits, c->max_splits);
+  AttnArgs a = attn_args(c, layer, q_own, stride_b, out, out_f32);
   LKV_LAUNCH(c, launch_attn(a, st), "attn");
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_append_attn(louiskv_ctx* c, int32_t layer, const void* k_t, const void* v_t,
+                                  int64_t stride_kv, const void* q_own, int64_t stride_q, void* out, float* out_f32,
+                                  void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !k_t || !v_t || !q_own || !out)
+    return fail(c, LOUISKV_ERR_INVALID_ARG, "append_attn: bad args");
+  if (is_full(c, layer)) {
+    louiskv_status s = louiskv_append_output(c, layer, k_t, v_t, stride_kv, stream);
+    if (s != LOUISKV_OK) return s;
+    return louiskv_sparse_attn(c, layer, q_own, stride_q, out, out_f32, stream);
+  }
+  if (c->stage[layer] != 1 && c->stage[layer] != 2)
+    return fail(c, LOUISKV_ERR_STATE, "append_attn must follow should_retrieve/retrieve");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  AttnArgs a = attn_args(c, layer, q_own, stride_q, out, out_f32);
+  a.fused = 1;
+  a.app = append_args(c, layer, k_t, v_t, stride_kv);
+  LKV_LAUNCH(c, launch_attn(a, st), "append+attn");
+  c->stage[layer] = 3;
   return LOUISKV_OK;
 }
 

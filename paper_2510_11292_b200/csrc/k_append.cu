@@ -11,100 +11,13 @@
 //      index), and the K/V rows written to the pinned host pool (zero-copy stores over the host
 //      link, "Offload (K_seg, V_seg) to CPU memory pool").
 // The open segment is never evicted.
-#include "lkv_internal.cuh"
+#include "lkv_append_dev.cuh"
 
 namespace lkv {
 
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   pdl_wait_trigger();
-  const int li = blockIdx.x;
-  const int b = li / a.hn;
-  const int tid = threadIdx.x;
-  InstState* S = a.inst + li;
-  const int flag = a.flag ? a.flag[b] : 0;
-  const int dec = *a.step - 1;  // decode index of this token (device step counter)
-  const int cap = a.ring_cap;
-  int2* fifo = a.fifo + (int64_t)li * cap;
-  bf16* ringK = a.ring + (int64_t)li * 2 * cap * D;
-  bf16* ringV = ringK + (int64_t)cap * D;
-
-  __shared__ InstState s;
-  if (tid == 0) {
-    s = *S;
-    if ((flag && s.open_len > 0) || s.open_len >= a.max_open) {
-      fifo[(s.fifo_head + s.fifo_count) % cap] = make_int2(s.open_start, s.open_len);
-      s.fifo_count++;
-      s.open_len = 0;
-    }
-    if (s.open_len == 0) s.open_start = dec;
-    if (s.buffered == 0) s.ring_head = dec;
-    s.open_len++;
-    s.buffered++;
-  }
-  // append the token's K and V rows
-  const int slot = dec % cap;
-  if (tid < 16) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.k_t + (int64_t)b * a.stride_b + (int64_t)(li % a.hn) * D);
-    reinterpret_cast<uint4*>(ringK + (int64_t)slot * D)[tid] = src[tid];
-  } else if (tid < 32) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.v_t + (int64_t)b * a.stride_b + (int64_t)(li % a.hn) * D);
-    reinterpret_cast<uint4*>(ringV + (int64_t)slot * D)[tid - 16] = src[tid - 16];
-  }
-  __syncthreads();
-
-  float* cent = a.cent + (int64_t)li * a.Umax * D;
-  uint16_t* centb = reinterpret_cast<uint16_t*>(a.centb) + (int64_t)li * a.Umax * D;
-  uint8_t* pool = a.pool + (int64_t)li * a.pool_inst_bytes;
-  int32_t* ppos = a.pool_pos + (int64_t)li * a.pool_rows_cap;
-  while (s.buffered > a.W && s.fifo_count > 0 && !s.error) {
-    const int2 seg = fifo[s.fifo_head];
-    const int start = seg.x, len = seg.y;
-    const int uid = s.n_units;
-    const int64_t prow = s.pool_rows;
-    if (uid >= a.Umax || prow + len > a.pool_rows_cap) {
-      __syncthreads();
-      if (tid == 0) s.error = 1;
-      __syncthreads();
-      break;
-    }
-    // centroid: sequential fp32 sum in time order, then one RN division (recipe)
-    {
-      float sum = 0.0f;
-      const uint16_t* rk = reinterpret_cast<const uint16_t*>(ringK);
-      for (int i = 0; i < len; ++i) sum = __fadd_rn(sum, bf2f(rk[(int64_t)((start + i) % cap) * D + tid]));
-      const float c = __fdiv_rn(sum, (float)len);
-      cent[(int64_t)uid * D + tid] = c;
-      centb[(int64_t)uid * D + tid] = f2bf_rne(c);
-    }
-    // offload rows: unit-major span [K rows | V rows] at pool row offset prow
-    uint4* dst = reinterpret_cast<uint4*>(pool + prow * POOL_ROW_BYTES);
-    for (int c = tid; c < 2 * len * 16; c += blockDim.x) {
-      const int isV = c >= len * 16;
-      const int cc = isV ? c - len * 16 : c;
-      const int i = cc >> 4, sub = cc & 15;
-      const bf16* src = (isV ? ringV : ringK) + (int64_t)((start + i) % cap) * D;
-      dst[(int64_t)(isV ? len + i : i) * 16 + sub] = reinterpret_cast<const uint4*>(src)[sub];
-    }
-    for (int i = tid; i < len; i += blockDim.x) ppos[prow + i] = s.prompt_len + start + i;
-    __syncthreads();
-    if (tid == 0) {
-      a.usize[(int64_t)li * a.Umax + uid] = len;
-      a.uoff[(int64_t)li * a.Umax + uid] = prow;
-      a.ufirst[(int64_t)li * a.Umax + uid] = s.prompt_len + start;
-      a.sel[(int64_t)li * a.Umax + uid] = 0;
-      s.n_units++;
-      s.pool_rows += len;
-      s.buffered -= len;
-      s.ring_head += len;
-      s.fifo_head = (s.fifo_head + 1) % cap;
-      s.fifo_count--;
-      atomicAdd(&a.stats->segments_evicted, 1ull);
-      atomicAdd(&a.stats->bytes_d2h, (unsigned long long)len * POOL_ROW_BYTES);
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  if (tid == 0) *S = s;
+  append_one(a, blockIdx.x);
 }
 
 // full-cache layer: append (k_t, v_t) at row P + t - 1 of every (b, head) and commit the

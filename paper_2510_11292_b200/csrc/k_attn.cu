@@ -7,7 +7,11 @@
 // (16 lanes x 8 dims) walks rows with an online softmax in the log2 domain; half-warps merge
 // through shared memory; splits merge in a fixed order by the last CTA to finish (atomic
 // ticket), so the result is deterministic. HBM-bound: 512 B of K+V per row.
-#include "lkv_internal.cuh"
+#include <cooperative_groups.h>
+
+#include "lkv_append_dev.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace lkv {
 
@@ -17,6 +21,7 @@ constexpr int AT_CHUNK = 64;           // rows per pipeline stage
 constexpr int AT_STAGES = 3;
 constexpr int AT_STAGE_BYTES = AT_CHUNK * 2 * ROW_BYTES;  // K + V: 32 KB
 constexpr int AT_SMEM = AT_STAGES * AT_STAGE_BYTES + 64;
+constexpr int AT_CL = 8;  // cluster size of the fused append+attention launch (one cluster per instance)
 
 struct RowSpan {
   const bf16* k0;  // sinks
@@ -48,10 +53,27 @@ __device__ __forceinline__ void row_ptrs(const RowSpan& sp, int r, const uint4*&
   vp = reinterpret_cast<const uint4*>(sp.v2 + (int64_t)slot * D);
 }
 
-template <int G>
+template <int G, bool FUSED>
 __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnArgs a) {
   pdl_wait_trigger();
-  const int li = blockIdx.x, split = blockIdx.y;
+  int li, split, nsplit;
+  if constexpr (FUSED) {
+    // one 8-CTA cluster per instance: rank 0 runs kvm.store_cache(k_t, v_t) (seal / append / evict),
+    // the cluster barrier publishes the new local-buffer state to the other ranks
+    li = blockIdx.x / AT_CL;
+    split = blockIdx.x % AT_CL;
+    nsplit = AT_CL;
+    if (split == 0) {
+      append_one(a.app, li);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    cg::this_cluster().sync();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  } else {
+    li = blockIdx.x;
+    split = blockIdx.y;
+    nsplit = gridDim.y;
+  }
   const int b = li / a.hn, h = li % a.hn;
   const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
 
@@ -82,8 +104,8 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
     sp.head = 0;
     sp.cap = 1;
   }
-  const int r_begin = (int)((int64_t)n_rows * split / gridDim.y);
-  const int r_end = (int)((int64_t)n_rows * (split + 1) / gridDim.y);
+  const int r_begin = (int)((int64_t)n_rows * split / nsplit);
+  const int r_end = (int)((int64_t)n_rows * (split + 1) / nsplit);
 
   // query fragment: this lane's 8 dims for each of the G heads, pre-scaled into log2 domain
   float q[G][8];
@@ -269,7 +291,9 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
   }
   __syncthreads();
 
-  float* part = a.part + ((int64_t)li * gridDim.y + split) * G * (D + 2);
+  // per-CTA partial: global scratch (split merge by the last CTA) or own smem (cluster merge)
+  float* part = FUSED ? reinterpret_cast<float*>(at_smem + AT_W * G * D * sizeof(float))
+                      : a.part + ((int64_t)li * nsplit + split) * G * (D + 2);
   for (int idx = tid; idx < G * D; idx += AT_THREADS) {
     const int j = idx / D, e = idx % D;
     float M = -INFINITY;
@@ -289,19 +313,60 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
     }
   }
 
+  if constexpr (FUSED) {
+    // ---- rank 0 merges the AT_CL partials through distributed shared memory, in rank order
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (split == 0) {
+      __shared__ float f_w[AT_CL][G];
+      __shared__ float f_l[AT_CL][G];
+      for (int t = tid; t < AT_CL * G; t += AT_THREADS) {
+        const int y = t / G, j = t % G;
+        const float* py = cl.map_shared_rank(part, y);
+        f_w[y][j] = py[j * (D + 2) + D];
+        f_l[y][j] = py[j * (D + 2) + D + 1];
+      }
+      __syncthreads();
+      if (tid < G) {
+        const int j = tid;
+        float M = -INFINITY;
+        for (int y = 0; y < AT_CL; ++y) M = fmaxf(M, f_w[y][j]);
+        float Lsum = 0.f;
+        for (int y = 0; y < AT_CL; ++y) {
+          const float w = f_w[y][j] == -INFINITY ? 0.f : exp2f(f_w[y][j] - M);
+          f_w[y][j] = w;
+          Lsum += w * f_l[y][j];
+        }
+        const float inv = 1.f / Lsum;
+        for (int y = 0; y < AT_CL; ++y) f_w[y][j] *= inv;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < G * D; idx += AT_THREADS) {
+        const int j = idx / D, e = idx % D;
+        float A = 0.f;
+#pragma unroll
+        for (int y = 0; y < AT_CL; ++y) A = fmaf(f_w[y][j], cl.map_shared_rank(part, y)[j * (D + 2) + e], A);
+        const int64_t oi = ((int64_t)(b * a.hn + h) * G + j) * D + e;
+        a.out[oi] = __float2bfloat16_rn(A);
+        if (a.out_f32) a.out_f32[oi] = A;
+      }
+    }
+    cl.sync();  // keep every rank's shared memory alive until rank 0 has read it
+    return;
+  }
   // ---- last CTA of this instance merges the splits in split order
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
   if (tid == 0) {
     const int ticket = atomicAdd(&a.counters[li], 1);
-    s_last = (ticket == (int)gridDim.y - 1);
+    s_last = (ticket == nsplit - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const float* P0 = a.part + (int64_t)li * gridDim.y * G * (D + 2);
-  const int Y = gridDim.y;
+  const float* P0 = a.part + (int64_t)li * nsplit * G * (D + 2);
+  const int Y = nsplit;
   __shared__ float s_w[64][G];  // per-split weights exp2(m_y - M) / L
   __shared__ float s_l[64][G];
   // all (split, head) statistics loaded in parallel, then the G reductions over splits
@@ -337,24 +402,40 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
   if (tid == 0) a.counters[li] = 0;
 }
 
-cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
-  dim3 grid(a.batch * a.hn, a.splits);
+template <int G>
+static cudaError_t launch_attn_g(const AttnArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    cudaFuncSetAttribute(attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
     attr = true;
   }
+  if (!a.fused) return launch_k(attn_kernel<G, false>, dim3(a.batch * a.hn, a.splits), dim3(AT_THREADS), AT_SMEM, st, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.batch * a.hn * AT_CL);
+  cfg.blockDim = dim3(AT_THREADS);
+  cfg.dynamicSmemBytes = AT_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = AT_CL;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, attn_kernel<G, true>, a);
+}
+
+cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st) {
   switch (a.g) {
-    case 1: launch_k(attn_kernel<1>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
-    case 2: launch_k(attn_kernel<2>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
-    case 4: launch_k(attn_kernel<4>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
-    case 8: launch_k(attn_kernel<8>, dim3(grid), dim3(AT_THREADS), AT_SMEM, st, a); break;
+    case 1: return launch_attn_g<1>(a, st);
+    case 2: return launch_attn_g<2>(a, st);
+    case 4: return launch_attn_g<4>(a, st);
+    case 8: return launch_attn_g<8>(a, st);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace lkv

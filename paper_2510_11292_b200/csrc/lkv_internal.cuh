@@ -142,6 +142,9 @@ struct AttnArgs {
   float* part;            // [batch*hn][splits][g][D+2]
   int* counters;          // [batch*hn]
   int splits;
+  // fused append + attention (clustered launch, sparse layers)
+  int fused;
+  AppendArgs app;
 };
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
 

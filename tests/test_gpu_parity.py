@@ -31,7 +31,7 @@ def small_cfg(**kw):
 
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
-                check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True):
+                check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step."""
     lkv = _lkv()
     hn = cfg.num_kv_heads - kv_head_begin if kv_head_count is None else kv_head_count
@@ -69,8 +69,11 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
             vt = inp.v[t, l][:, h0:h0 + hn]
             ctx.should_retrieve(l, qa, flag_d, r_d)
             ctx.retrieve(l, qo)
-            ctx.append_output(l, kt.contiguous(), vt.contiguous())
-            ctx.sparse_attn(l, qo, out, out32)
+            if fused:
+                ctx.append_attn(l, kt.contiguous(), vt.contiguous(), qo, out, out32)
+            else:
+                ctx.append_output(l, kt.contiguous(), vt.contiguous())
+                ctx.sparse_attn(l, qo, out, out32)
             f_o, r_o = ep.should_retrieve(l, np32(qa))
             ep.retrieve(l, np32(qo))
             ep.append_output(l, np32(kt), np32(vt))
@@ -125,11 +128,11 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
 
 
 # ------------------------------------------------------------------ episodes
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_episode_oracle_clustering_small(seed):
+@pytest.mark.parametrize("seed,fused", [(0, False), (1, False), (2, False), (0, True), (1, True)])
+def test_episode_oracle_clustering_small(seed, fused):
     cfg = small_cfg()
     inp = make_inputs(cfg, cfg.decode_steps, seed)
-    worst, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn))
+    worst, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused)
     assert n_flags > 5 and st["segments_evicted"] > 0 and st["units_reused"] > 0
 
 
@@ -139,7 +142,7 @@ def test_episode_c1_shape():
     for hq in (1, 4):
         cfg = C1.replace(num_q_heads=hq)
         inp = make_inputs(cfg, cfg.decode_steps, 0)
-        run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn))
+        run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=(hq == 4))
 
 
 def test_episode_last_retrieval_and_shared_modes():
@@ -159,6 +162,7 @@ def test_episode_degenerate_tau_budget_force_seal():
     assert st["retrievals"] == cfg.batch * 2
     cfg = small_cfg(decode_steps=30, tau=-1.0, window_tokens=6)     # force-seal at max_open=3
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3)
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3, fused=True)
 
 
 def test_superset_budget_equals_full_attention():
@@ -334,7 +338,7 @@ def test_c2_layer_full_size_sampled():
     cfg = C2.replace(num_layers=2, full_cache_layers=(0,), decode_steps=24)
     inp = make_inputs(cfg, 24, 0)
     worst, n_flags, st = run_episode(cfg, inp, 24, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
-                                     compare_ws=False)
+                                     compare_ws=False, fused=True)
     assert n_flags >= 3
 
 
