@@ -49,6 +49,7 @@ struct louiskv_ctx {
   float* d_se = nullptr;
   uint8_t* d_ssort = nullptr;
   RowSrc* d_rows = nullptr;
+  GatherJob* d_jobs = nullptr;  // [L][Bmax*hn]
   float* d_part = nullptr;
   int* d_counters = nullptr;
   int max_splits = 64;
@@ -151,6 +152,7 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   a.scratch_e = c->d_se;
   a.scratch_sort = c->d_ssort;
   a.rows = c->d_rows;
+  a.jobs = c->d_jobs + (size_t)layer * c->inst_per_layer;
   a.stats = c->d_stats;
   return a;
 }
@@ -183,6 +185,9 @@ AppendArgs append_args(louiskv_ctx* c, int layer, const void* k_t, const void* v
   a.pool = c->d_pool + ib * c->pool_inst_bytes;
   a.pool_inst_bytes = c->pool_inst_bytes;
   a.stats = c->d_stats;
+  a.jobs = c->d_jobs + (size_t)layer * c->inst_per_layer;
+  a.rows = c->d_rows;
+  a.budget = std::max(c->Bud, 1);
   return a;
 }
 
@@ -330,6 +335,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_se, (size_t)nl * g * c->Umax);
   ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 14);
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
+  ok = ok && dalloc(c, &c->d_jobs, (size_t)c->L * nl);
   ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
   ok = ok && dalloc(c, &c->d_counters, (size_t)nl);
   ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * (((std::max(c->kmax, 1) + 255) / 256) * 256));
@@ -395,6 +401,8 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
              "memset q_ref");
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_flag + (size_t)layer * c->Bmax, 0, c->Bmax, st), "memset flag");
   LKV_LAUNCH(c, cudaMemsetAsync(c->d_step + layer, 0, sizeof(int), st), "memset step");
+  LKV_LAUNCH(c, cudaMemsetAsync(c->d_jobs + (size_t)layer * c->inst_per_layer, 0, sizeof(GatherJob) * c->inst_per_layer, st),
+             "memset jobs");
   if (is_full(c, layer)) {
     if (h_assign) return fail(c, LOUISKV_ERR_INVALID_ARG, "set_prompt_units on a full-cache layer");
     LKV_LAUNCH(c,

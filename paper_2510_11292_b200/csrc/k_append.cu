@@ -20,6 +20,21 @@ __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   append_one(a, blockIdx.x);
 }
 
+// standalone gather of the pending jobs (unfused API path): grid (instances, row slices)
+__global__ void __launch_bounds__(256) gather_kernel(AppendArgs a) {
+  pdl_wait_trigger();
+  const int li = blockIdx.x;
+  const GatherJob J = a.jobs[li];
+  const int per = (J.n_rows + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * per, r1 = min(J.n_rows, r0 + per);
+  if (r0 < r1) gather_rows(a, li, J, r0, r1);
+}
+
+__global__ void clear_jobs_kernel(GatherJob* jobs, int n) {
+  pdl_wait_trigger();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) jobs[i].n_rows = 0;
+}
+
 // full-cache layer: append (k_t, v_t) at row P + t - 1 of every (b, head) and commit the
 // layer's step counter; one CTA so the read of t and its commit cannot race.
 __global__ void __launch_bounds__(256) full_step_kernel(const bf16* k_t, const bf16* v_t, int64_t stride_b, int n,
@@ -45,6 +60,9 @@ __global__ void __launch_bounds__(256) full_step_kernel(const bf16* k_t, const b
 }
 
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st) {
+  const int gy = a.budget >= 64 ? a.budget / 64 : 1;
+  launch_k(gather_kernel, dim3(a.batch * a.hn, gy), dim3(256), 0, st, a);
+  launch_k(clear_jobs_kernel, dim3(1), dim3(256), 0, st, a.jobs, a.batch * a.hn);
   launch_k(append_kernel, dim3(a.batch * a.hn), dim3(128), 0, st, a);
   return cudaGetLastError();
 }

@@ -63,12 +63,19 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
     li = blockIdx.x / AT_CL;
     split = blockIdx.x % AT_CL;
     nsplit = AT_CL;
-    if (split == 0) {
-      append_one(a.app, li);
-      asm volatile("fence.proxy.async.global;" ::: "memory");
+    {  // every rank copies 1/AT_CL of the pending gather job (selected rows -> working set)
+      const GatherJob J = a.app.jobs[li];
+      if (J.n_rows > 0) {
+        const int per = (J.n_rows + AT_CL - 1) / AT_CL;
+        const int r0 = split * per, r1 = min(J.n_rows, r0 + per);
+        if (r0 < r1) gather_rows(a.app, li, J, r0, r1);
+      }
     }
+    if (split == 0) append_one(a.app, li);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     cg::this_cluster().sync();
     asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (split == 0 && threadIdx.x == 0) a.app.jobs[li].n_rows = 0;
   } else {
     li = blockIdx.x;
     split = blockIdx.y;

@@ -51,7 +51,7 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
 // r_t of its sequence with the same fixed-order recipe (bit-identical), so no grid-wide dependency
 // is needed; the (slice 0, head 0) CTA publishes flag/r and writes the next q_ref buffer
 // (double-buffered by step parity so concurrent CTAs keep reading the old one).
-constexpr int TL_THREADS = 128;
+constexpr int TL_THREADS = 256;
 template <int G>
 __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a) {
   pdl_wait_trigger();
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // commit the layer's device step counter (read by should_retrieve's kernel, then by append/attn)
   if (li == 0 && tid == 0) *a.step = *a.step + 1;
-  if (!a.flag[b]) return;
+  if (!a.flag[b]) return;  // (jobs of unflagged instances were cleared by their consumer)
   InstState* S = a.inst + li;
   const int n = S->n_units;
 
@@ -471,32 +471,7 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
     S->ws_cur = nxt;
     S->ws_rows = total;
   }
-  __syncthreads();
-  // ---- gather (P:126 row-granular transfer): 16 lanes x 16 B per row, 2 rows in flight per thread;
-  // new units read zero-copy from the pinned host pool, kept units device-to-device
-  {
-    const int sub = tid & 15;
-    constexpr int RPP = SS_THREADS / 16;  // rows per pass
-    uint4* dK = reinterpret_cast<uint4*>(nxtK);
-    uint4* dV = reinterpret_cast<uint4*>(nxtV);
-    for (int r = tid >> 4; r < total; r += 2 * RPP) {
-      const int r2 = r + RPP;
-      const RowSrc s0 = rows[r];
-      const uint4 k0 = s0.k[sub], v0 = s0.v[sub];
-      uint4 k1 = k0, v1 = v0;
-      if (r2 < total) {
-        const RowSrc s1 = rows[r2];
-        k1 = s1.k[sub];
-        v1 = s1.v[sub];
-      }
-      dK[(int64_t)r * (D / 8) + sub] = k0;
-      dV[(int64_t)r * (D / 8) + sub] = v0;
-      if (r2 < total) {
-        dK[(int64_t)r2 * (D / 8) + sub] = k1;
-        dV[(int64_t)r2 * (D / 8) + sub] = v1;
-      }
-    }
-  }
+  if (tid == 0) a.jobs[li] = GatherJob{total, 0, nxtK, nxtV};
 }
 
 template <int G>

@@ -5,6 +5,34 @@
 
 namespace lkv {
 
+// Row-granular gather of instance li's pending job, rows [r0, r1) by this CTA: 16 lanes x 16 B
+// per row, two rows in flight per thread; new units are read zero-copy from the pinned host pool,
+// kept units device-to-device.
+__device__ __forceinline__ void gather_rows(const AppendArgs& a, int li, const GatherJob& J, int r0, int r1) {
+  const RowSrc* R = a.rows + (int64_t)li * a.budget;
+  const int sub = threadIdx.x & 15;
+  const int rpp = blockDim.x >> 4;
+  uint4* dK = reinterpret_cast<uint4*>(J.dstK);
+  uint4* dV = reinterpret_cast<uint4*>(J.dstV);
+  for (int r = r0 + (threadIdx.x >> 4); r < r1; r += 2 * rpp) {
+    const int r2 = r + rpp;
+    const RowSrc s0 = R[r];
+    const uint4 k0 = s0.k[sub], v0 = s0.v[sub];
+    uint4 k1 = k0, v1 = v0;
+    if (r2 < r1) {
+      const RowSrc s1 = R[r2];
+      k1 = s1.k[sub];
+      v1 = s1.v[sub];
+    }
+    dK[(int64_t)r * (D / 8) + sub] = k0;
+    dV[(int64_t)r * (D / 8) + sub] = v0;
+    if (r2 < r1) {
+      dK[(int64_t)r2 * (D / 8) + sub] = k1;
+      dV[(int64_t)r2 * (D / 8) + sub] = v1;
+    }
+  }
+}
+
 // Called by every thread of one CTA (blockDim >= 128: thread e < 128 owns dimension e of the
 // centroid); leaves the post-append state in global memory.
 __device__ __forceinline__ void append_one(const AppendArgs& a, const int li) {

@@ -38,6 +38,14 @@ struct InstState {
   int32_t pad;
 };
 
+// Gather job of one instance: written by select (retrieve), consumed by the gather of append_output
+// or by the clustered append+attention kernel, which clear it.
+struct GatherJob {
+  int32_t n_rows;
+  int32_t pad;
+  bf16* dstK;
+  bf16* dstV;
+};
 struct RowSrc {
   const uint4* k;
   const uint4* v;
@@ -65,6 +73,7 @@ struct RetrieveArgs {
   double* r_out;
   int* step;                 // device step counter of this layer (read by both, committed by select)
   uint8_t* flag;             // [batch] of this layer
+  GatherJob* jobs;           // [batch*hn] per-layer gather jobs
   InstState* inst;           // layer base, [batch*hn]
   const bf16* centb;         // layer base [batch*hn][Umax][D]
   const int32_t* usize;      // [batch*hn][Umax]
@@ -89,6 +98,9 @@ cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st);
 
 // append (k_append.cu)
 struct AppendArgs {
+  GatherJob* jobs;      // [batch*hn] pending gathers of this layer (consumed here)
+  const RowSrc* rows;   // [batch*hn][budget]
+  int budget;
   const bf16* k_t;
   const bf16* v_t;
   int64_t stride_b;
@@ -110,7 +122,7 @@ struct AppendArgs {
   int64_t pool_inst_bytes;
   StatsDev* stats;
 };
-cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);
+cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);  // gather kernel + append kernel
 // full-cache layer step: append (k_t, v_t) at P + t - 1 and commit the step counter (one CTA)
 cudaError_t launch_full_step(const bf16* k_t, const bf16* v_t, int64_t stride_b, int batch, int hn, bf16* full,
                              int64_t full_cap, int64_t P, int* step, int* error, cudaStream_t st);

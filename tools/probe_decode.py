@@ -15,6 +15,6 @@ q, k, v, _ = synth.decode_stream(cfg, T, 0, "cuda", plants)
 out = torch.empty((cfg.num_layers, 1, 32, 128), dtype=torch.bfloat16, device="cuda")
 for t in range(T):
     for l in range(cfg.num_layers):
-        ctx.should_retrieve(l, q[t, l]); ctx.retrieve(l, q[t, l]); ctx.append_output(l, k[t, l], v[t, l]); ctx.sparse_attn(l, q[t, l], out[l])
+        ctx.should_retrieve(l, q[t, l]); ctx.retrieve(l, q[t, l]); ctx.append_attn(l, k[t, l], v[t, l], q[t, l], out[l])
 torch.cuda.synchronize()
 print(ctx.stats())
