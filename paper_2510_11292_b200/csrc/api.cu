@@ -333,7 +333,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_qref, (size_t)c->L * 2 * c->Bmax * c->Hq * D);
   ok = ok && dalloc(c, &c->d_full, (size_t)c->n_f * nl * 2 * c->full_cap * D);
   ok = ok && dalloc(c, &c->d_se, (size_t)nl * g * c->Umax);
-  ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 14);
+  ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 26);
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
   ok = ok && dalloc(c, &c->d_jobs, (size_t)c->L * nl);
   ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));

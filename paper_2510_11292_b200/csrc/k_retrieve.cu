@@ -21,9 +21,9 @@
 
 namespace lkv {
 
-constexpr int SS_THREADS = 512;
+constexpr int SS_THREADS = 1024;
 constexpr int SS_WARPS = SS_THREADS / 32;
-constexpr int SORT_CAP = 12288;  // units whose sort buffers live in shared memory (else global scratch)
+constexpr int SORT_CAP = 12288;  // units whose keys/sizes live in shared memory (else global scratch)
 
 __device__ __forceinline__ float exp_r3(float x, const float* c) {
   const float log2e = __double2float_rn(1.4426950408889634074);
@@ -195,37 +195,31 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
 }
 
 // ---- group scores, sort, budgeted greedy, working-set layout: one CTA per flagged instance
-template <int G>
-__global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
-  pdl_wait_trigger();
-  const int li = blockIdx.x;
-  const int b = li / a.hn;
+// SMB: the sort buffers live in shared memory (explicit LDS/STS); else in this instance's global scratch
+template <int G, bool SMB>
+__device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li, const int n) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // commit the layer's device step counter (read by should_retrieve's kernel, then by append/attn)
-  if (li == 0 && tid == 0) *a.step = *a.step + 1;
-  if (!a.flag[b]) return;  // (jobs of unflagged instances were cleared by their consumer)
   InstState* S = a.inst + li;
-  const int n = S->n_units;
 
   __shared__ float s_coef[7];
   __shared__ float s_red[SS_WARPS][G];
   __shared__ float s_m[G];
   __shared__ unsigned long long s_z[G];
   __shared__ float s_Z[G];
-  __shared__ int s_cnt[SS_WARPS][256];
   __shared__ int s_warp[SS_WARPS + 1];
-  extern __shared__ uint32_t s_dyn[];
+  extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* s_taken = s_dyn;  // bitmap [ceil(Umax/32)]
-  // sort buffers (shared memory when n <= SORT_CAP, else this instance's global scratch)
-  uint8_t* sb = reinterpret_cast<uint8_t*>(s_dyn + (a.Umax + 31) / 32);
-  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
-  if (n > cap) sb = a.scratch_sort + (int64_t)li * a.Umax * 14;
-  const int m_ = n > cap ? a.Umax : cap;
-  uint32_t* kA = reinterpret_cast<uint32_t*>(sb);
-  uint32_t* kB = kA + m_;
-  uint16_t* vA = reinterpret_cast<uint16_t*>(kB + m_);
-  uint16_t* vB = vA + m_;
-  uint16_t* s_sz = vB + m_;
+  // sort keys (~bits(A) << 16 | id) padded to a power of two, and unit sizes (by id): shared memory
+  // when they fit, else this instance's global scratch
+  unsigned long long* KEYS;
+  uint16_t* s_sz;
+  if constexpr (SMB) {
+    KEYS = reinterpret_cast<unsigned long long*>(s_dyn + (((a.Umax + 31) / 32 + 1) & ~1));
+    s_sz = reinterpret_cast<uint16_t*>(KEYS + SORT_CAP);
+  } else {
+    KEYS = reinterpret_cast<unsigned long long*>(a.scratch_sort + (int64_t)li * a.Umax * 26);
+    s_sz = reinterpret_cast<uint16_t*>(KEYS + 3 * a.Umax);
+  }
 
   if (tid == 0) {
     double p = 1.0, fact = 1.0;
@@ -293,111 +287,132 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
 #pragma unroll
     for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[(int64_t)j * a.Umax + u], s_Z[j]));
     A = __fdiv_rn(A, (float)G);
-    kA[u] = ~__float_as_uint(A);
-    vA[u] = (uint16_t)u;
+    KEYS[u] = ((unsigned long long)(~__float_as_uint(A)) << 16) | (unsigned)u;  // (A desc, id asc)
     const int sz = usize[u];
     s_sz[u] = (uint16_t)(sz > 0xFFFF ? 0xFFFF : sz);
   }
   __syncthreads();
 
-  // ---- stable LSD radix sort of (key, id), 4 passes of 8 bits; warp w owns a contiguous chunk
+  // ---- budgeted greedy skip-and-continue in (A desc, id asc) order, exact:
+  // (1) size-weighted radix select of the first-skip pivot K* = the smallest key whose running size
+  //     sum exceeds B (6 passes of 8-bit digits over the 48-bit keys; warp-aggregated histograms);
+  //     every key < K* is taken, K* is skipped, rem1 = B - (sizes below K*);
+  // (2) after K* only units with size <= rem1 can still be taken (the budget never grows): they are
+  //     compacted, bitonic-sorted (a small set) and walked by one warp until the budget is spent.
   {
-    const int chunk = (((n + 31) / 32 + SS_WARPS - 1) / SS_WARPS) * 32;
-    const int c0 = warp * chunk, c1 = min(n, c0 + chunk);
-    uint32_t *kin = kA, *kout = kB;
-    uint16_t *vin = vA, *vout = vB;
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 8 * pass;
-      for (int i = tid; i < SS_WARPS * 256; i += SS_THREADS) (&s_cnt[0][0])[i] = 0;
-      __syncthreads();
-      for (int r0 = c0; r0 < c1; r0 += 32) {
-        const int i = r0 + lane;
-        const int d = i < c1 ? (int)((kin[i] >> shift) & 255u) : 256 + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (i < c1 && lane == __ffs(peers) - 1) s_cnt[warp][d] += __popc(peers);
-        __syncwarp();
-      }
-      __syncthreads();
-      // exclusive offsets in (digit, warp) order: thread t owns digit t/2, warps (t%2)*8 .. +8
-      {
-        const int d = tid >> 1, w0 = (tid & 1) * (SS_WARPS / 2);
-        int v[SS_WARPS / 2], loc = 0;
-#pragma unroll
-        for (int w = 0; w < SS_WARPS / 2; ++w) {
-          v[w] = s_cnt[w0 + w][d];
-          loc += v[w];
-        }
-        int total;
-        int run = block_excl_scan(loc, s_warp, total);
-#pragma unroll
-        for (int w = 0; w < SS_WARPS / 2; ++w) {
-          s_cnt[w0 + w][d] = run;
-          run += v[w];
-        }
-      }
-      __syncthreads();
-      for (int r0 = c0; r0 < c1; r0 += 32) {
-        const int i = r0 + lane;
-        const bool valid = i < c1;
-        const uint32_t k = valid ? kin[i] : 0u;
-        const int d = valid ? (int)((k >> shift) & 255u) : 256 + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (valid) base = s_cnt[warp][d];
-        __syncwarp();
-        if (valid) {
-          const int pos = base + __popc(peers & ((1u << lane) - 1u));
-          kout[pos] = k;
-          vout[pos] = vin[i];
-          if (lane == leader) s_cnt[warp][d] = base + __popc(peers);
-        }
-        __syncwarp();
-      }
-      __syncthreads();
-      uint32_t* tk = kin;
-      kin = kout;
-      kout = tk;
-      uint16_t* tv = vin;
-      vin = vout;
-      vout = tv;
+    __shared__ int s_hist[256];
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_need, s_all;
+    if (tid == 0) {
+      s_prefix = 0ull;
+      s_need = a.budget;
+      s_all = 0;
     }
-    // after 4 passes the sorted data is back in (kA, vA)
-  }
-
-  // ---- greedy skip-and-continue in sorted order (single warp): take u iff size_u <= remaining
-  if (warp == 0) {
-    int rem = a.budget;
-    for (int c = 0; c < n && rem > 0; c += 32) {
-      const int i = c + lane;
-      int u = 0, sz = 0x7FFFFFFF;
-      if (i < n) {
-        u = vA[i];
-        sz = s_sz[u];
+    __syncthreads();
+    for (int pass = 0; pass < 6; ++pass) {
+      const int shift = 40 - 8 * pass;
+      const unsigned long long hi_mask = (pass == 0) ? 0ull : (~0ull << (shift + 8)) & 0xFFFFFFFFFFFFull;
+      for (int i = tid; i < 256; i += SS_THREADS) s_hist[i] = 0;
+      __syncthreads();
+      const unsigned long long prefix = s_prefix;
+      for (int u0 = warp * 32; u0 < n; u0 += SS_THREADS) {
+        const int u = u0 + lane;
+        int bk = -1, sz = 0;
+        if (u < n) {
+          const unsigned long long k = KEYS[u];
+          if ((k & hi_mask) == prefix) {
+            bk = (int)((k >> shift) & 255);
+            sz = s_sz[u];
+          }
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, bk);
+        const unsigned sum = __reduce_add_sync(peers, (unsigned)sz);
+        if (bk >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bk], (int)sum);
       }
-      bool pending = i < n;
-      while (true) {
-        const bool cand = pending && sz <= rem;
-        const unsigned cm = __ballot_sync(0xffffffffu, cand);
-        if (cm == 0u) break;
-        int incl = cand ? sz : 0;
+      __syncthreads();
+      if (warp == 0) {
+        int v[8], ls = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[i] = s_hist[lane * 8 + i];
+          ls += v[i];
+        }
+        int incl = ls;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += y;
         }
-        const unsigned over = __ballot_sync(0xffffffffu, cand && incl > rem);
-        if (over == 0u) {
-          if (cand) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
-          rem -= __shfl_sync(0xffffffffu, incl, 31);
-          break;
+        const int excl = incl - ls;
+        const int need = s_need;
+        const unsigned hit = __ballot_sync(0xffffffffu, incl > need);
+        if (hit == 0u) {
+          if (lane == 0) s_all = 1;  // (pass 0 sees everything) the whole set fits the budget
+        } else {
+          const int first = __ffs(hit) - 1;
+          if (lane == first) {
+            int cum = excl, bk = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (cum + v[i] > need) {
+                bk = i;
+                break;
+              }
+              cum += v[i];
+            }
+            s_need = need - cum;
+            s_prefix = prefix | ((unsigned long long)(lane * 8 + bk) << shift);
+          }
         }
-        const int first = __ffs(over) - 1;
-        const int before = __shfl_sync(0xffffffffu, incl, first > 0 ? first - 1 : 0);
-        if (cand && lane < first) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
-        rem -= first > 0 ? before : 0;
-        pending = pending && lane > first;
       }
+      __syncthreads();
+      if (s_all) break;
+    }
+    const bool all = s_all != 0;
+    const unsigned long long pivot = all ? ~0ull : s_prefix;
+    const int rem1 = all ? 0 : s_need;
+    // prefix run: every key below the pivot is taken
+    const int per = (n + SS_THREADS - 1) / SS_THREADS;
+    const int u0 = tid * per, u1 = min(n, u0 + per);
+    for (int u = u0; u < u1; ++u)
+      if (KEYS[u] < pivot) atomicOr(&s_taken[u >> 5], 1u << (u & 31));
+    // tail: the greedy's next take is the smallest key after the last taken one among the units
+    // that still fit; one block-wide min-reduction per take (few: each take lowers the budget,
+    // which starts below the pivot's size)
+    __shared__ unsigned long long s_kmin[SS_WARPS];
+    __shared__ unsigned long long s_last;
+    if (tid == 0) s_last = pivot;
+    int rem = rem1;
+    while (rem > 0) {
+      __syncthreads();
+      const unsigned long long last = s_last;
+      unsigned long long best = ~0ull;
+      for (int u = u0; u < u1; ++u) {
+        const unsigned long long k = KEYS[u];
+        if (k > last && k < best && s_sz[u] <= rem) best = k;
+      }
+#pragma unroll
+      for (int o2 = 16; o2; o2 >>= 1) {
+        const unsigned long long y = shfl_xor_u64(best, o2);
+        best = y < best ? y : best;
+      }
+      if (lane == 0) s_kmin[warp] = best;
+      __syncthreads();
+      if (warp == 0) {
+        unsigned long long v = s_kmin[lane];
+#pragma unroll
+        for (int o2 = 16; o2; o2 >>= 1) {
+          const unsigned long long y = shfl_xor_u64(v, o2);
+          v = y < v ? y : v;
+        }
+        if (lane == 0) s_last = v;
+      }
+      __syncthreads();
+      const unsigned long long kt = s_last;
+      if (kt == ~0ull) break;  // nothing else fits
+      const int ut = (int)(kt & 0xFFFFull);
+      rem -= s_sz[ut];
+      if (tid == 0) atomicOr(&s_taken[ut >> 5], 1u << (ut & 31));
     }
   }
   __syncthreads();
@@ -475,6 +490,22 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
 }
 
 template <int G>
+__global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
+  pdl_wait_trigger();
+  const int li = blockIdx.x;
+  const int b = li / a.hn;
+  // commit the layer's device step counter (read by should_retrieve's kernel, then by append/attn)
+  if (li == 0 && threadIdx.x == 0) *a.step = *a.step + 1;
+  if (!a.flag[b]) return;  // (jobs of unflagged instances were cleared by their consumer)
+  const int n = a.inst[li].n_units;
+  const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
+  if (n <= cap)
+    select_body<G, true>(a, li, n);
+  else
+    select_body<G, false>(a, li, n);
+}
+
+template <int G>
 static void set_attrs_once() {
   static bool attr = false;
   if (!attr) {
@@ -498,7 +529,8 @@ cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st) {
 
 cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st) {
   const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
-  const size_t smem = sizeof(uint32_t) * ((a.Umax + 31) / 32) + 14ull * cap;
+  const size_t smem =
+      sizeof(uint32_t) * ((((a.Umax + 31) / 32) + 1) & ~1) + 8ull * SORT_CAP + 2ull * cap;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   switch (a.g) {
     case 1: set_attrs_once<1>(); launch_k(select_kernel<1>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
