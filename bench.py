@@ -260,28 +260,17 @@ def main():
     v_in = torch.empty((L, b, Hkv, d), dtype=torch.bfloat16, device=dev)
     out = torch.empty((L, b, Hq, d), dtype=torch.bfloat16, device=dev)
 
+    flags = torch.zeros((L, b), dtype=torch.uint8, device=dev)
+
     def issue_step(events=None):
+        # one louiskv_decode_layer call per layer: trigger -> retrieve -> store_cache -> attention
+        # (one clustered launch on a retrieval layer; step kernel + attention on a full-cache layer)
         for l in range(L):
             if events is not None:
-                events[4 * l].record()
-            ctx.should_retrieve(l, q_in[l])
-            if events is not None:
-                events[4 * l + 1].record()
-            ctx.retrieve(l, q_in[l])
-            if events is not None:
-                events[4 * l + 2].record()
-            if l in full:
-                # full-cache layer: separate calls so the attention launch is isolated by the events
-                ctx.append_output(l, k_in[l], v_in[l])
-                if events is not None:
-                    events[4 * l + 3].record()
-                ctx.sparse_attn(l, q_in[l], out[l])
-            else:
-                if events is not None:
-                    events[4 * l + 3].record()
-                ctx.append_attn(l, k_in[l], v_in[l], q_in[l], out[l])
+                events[l].record()
+            ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], flag_out=flags[l])
         if events is not None:
-            events[4 * L].record()
+            events[L].record()
 
     step_idx = 0
 
@@ -300,8 +289,8 @@ def main():
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=cap_stream):
         issue_step()
-    # retrieval layer: trigger+logits, select+gather, clustered append+attention; full layer: step, attention
-    launches_per_step = sum(2 if l in full else 3 for l in range(L))
+    # retrieval layer: one clustered launch; full-cache layer: step kernel + attention
+    launches_per_step = sum(2 if l in full else 1 for l in range(L))
 
     for _ in range(W):
         load(step_idx)
@@ -348,39 +337,34 @@ def main():
            "h2d_bytes_per_step": int(qh[0].numel() + kh[0].numel() + vh[0].numel()) * 2,
            "d2h_bytes_per_step": int(oh[0].numel()) * 2, "ms_per_step": e2e_ms / K}
 
-    # ---------------- attribution pass: graph with event nodes between the ABI calls
-    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4 * L + 1)]
+    # ---------------- attribution pass: graph with event nodes between the per-layer calls; every
+    # retrieval-layer launch is classified by its trigger decision (flags read back per step)
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(L + 1)]
     graph2 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph2, stream=cap_stream):
         issue_step(evs)
-    # phases (ms per step): should_retrieve = trigger + logits, retrieve = select + gather,
-    # append_attn = clustered append + attention (retrieval layers) / full-cache step + attention
-    phase = {"should_retrieve": 0.0, "retrieve": 0.0, "append_attn_sparse": 0.0, "append_attn_full": 0.0}
-    attn_full_launch_ms, n_full_launch = 0.0, 0
-    retr_step_ms = []
+    t_unf, t_flg, t_full = [], [], []
     st_c = ctx.stats()
     for i in range(A):
         load(step_idx)
         graph2.replay()
         step_idx += 1
         torch.cuda.synchronize()
-        rs = 0.0
+        fl = flags.cpu().numpy()
         for l in range(L):
-            t_trig = evs[4 * l].elapsed_time(evs[4 * l + 1])
-            t_ret = evs[4 * l + 1].elapsed_time(evs[4 * l + 2])
-            t_att = evs[4 * l + 3].elapsed_time(evs[4 * l + 4])
-            phase["should_retrieve"] += t_trig
+            dt = evs[l].elapsed_time(evs[l + 1])
             if l in full:
-                phase["append_attn_full"] += t_att
-                attn_full_launch_ms += t_att
-                n_full_launch += 1
+                t_full.append(dt)
+            elif fl[l].any():
+                t_flg.append(dt)
             else:
-                phase["retrieve"] += t_ret
-                phase["append_attn_sparse"] += t_att
-                rs += t_ret
-        retr_step_ms.append(rs)
+                t_unf.append(dt)
     st_d = ctx.stats()
-    phase = {k_: v_ / A for k_, v_ in phase.items()}  # ms per step
+    mean = lambda xs: sum(xs) / len(xs) if xs else 0.0
+    phase = {"retrieval_layers_unflagged": sum(t_unf) / A, "retrieval_layers_flagged": sum(t_flg) / A,
+             "full_cache_layers": sum(t_full) / A}  # ms per step
+    layer_us = {"retrieval_unflagged": mean(t_unf) * 1e3, "retrieval_flagged": mean(t_flg) * 1e3,
+                "full_cache": mean(t_full) * 1e3, "n_flagged": len(t_flg), "n_unflagged": len(t_unf)}
 
     # ---------------- host-link peak (pinned H2D copy) and HBM / tensor peaks
     hl = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
@@ -398,28 +382,57 @@ def main():
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
-    # dominant kernel: full-cache attention (HBM) vs retrieval gather (host link)
+    # ---- per-launch algorithmic bytes. Full-cache launch: K+V rows of P+t tokens. Retrieval-layer
+    # launch: the attended rows (sinks + working set + local buffer; buffered = t - evicted tokens),
+    # plus on a flagged launch the centroid reads (n_units x 256 B) and the working-set rebuild
+    # (rows written 512 B each; host rows cross the link, kept rows are re-read from HBM).
     P = cfg.prompt_len
     t_mid = step_idx - A // 2
-    full_bytes = b * Hkv * (P + t_mid) * 2 * d * 2  # K+V bf16 rows read per full-cache launch
-    attn_full_ms = attn_full_launch_ms / max(n_full_launch, 1)
-    att_full_gbs = full_bytes / (attn_full_ms / 1e3) / 1e9
+    full_bytes = b * Hkv * (P + t_mid) * 2 * d * 2
+    att_rows, n_units = 0, 0
+    kc = -(-(P - cfg.sink_tokens) // cfg.avg_cluster_size)
+    for l in range(L):
+        if l in full:
+            continue
+        for bb in range(b):
+            for hh in range(Hkv):
+                _, sizes, _ = ctx.get_units(l, bb, hh)
+                nws = len(ctx.get_working_set(l, bb, hh)[0])
+                att_rows += min(cfg.sink_tokens, P) + nws + (step_idx - int(sizes[kc:].sum()))
+                n_units += len(sizes)
+    n_rl = L - len(full)
+    unf_bytes = att_rows / n_rl * 512
     h2d_bytes = st_d["bytes_h2d"] - st_c["bytes_h2d"]
-    retr_ms_total = sum(retr_step_ms)
-    gather_gbs = h2d_bytes / (retr_ms_total / 1e3) / 1e9 if retr_ms_total > 0 else 0.0
+    flg_launches = max(len(t_flg), 1)
+    ws_rows_flg = b * Hkv * cfg.budget_tokens  # rows rebuilt per flagged launch (upper bound: B per instance)
+    flg_bytes = unf_bytes + n_units / n_rl * 256 + ws_rows_flg * 512 + (ws_rows_flg * 512 - h2d_bytes / flg_launches)
+    ret_ms = (sum(t_unf) + sum(t_flg)) / max(len(t_unf) + len(t_flg), 1)
+    ret_bytes = (unf_bytes * len(t_unf) + flg_bytes * len(t_flg)) / max(len(t_unf) + len(t_flg), 1)
+    ret_gbs = ret_bytes / (ret_ms / 1e3) / 1e9
     step_ms_attr = sum(phase.values())
-    dominant = max(phase.items(), key=lambda kv: kv[1])[0]
-    roofline_attn = {"kernel": "attn_kernel (full-cache layers, split-K flash-decode)", "bound": "hbm",
-                     "achieved": att_full_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": att_full_gbs / hbm_peak,
-                     "traffic": None, "bytes_per_launch": full_bytes, "ms_per_launch": attn_full_ms,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
-                     "share_of_step": phase["append_attn_full"] / step_ms_attr}
-    roofline_gather = {"kernel": "score_select + gather (retrieve)", "bound": "host_link",
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"
+    roofline_layer = {"kernel": "layer_kernel (retrieval layers: trigger + score/select + gather + append + attention)",
+                      "bound": "hbm", "achieved": ret_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ret_gbs / hbm_peak,
+                      "traffic": None, "bytes_per_launch": ret_bytes, "ms_per_launch": ret_ms,
+                      "peak_source": peak_src,
+                      "share_of_step": (phase["retrieval_layers_unflagged"] + phase["retrieval_layers_flagged"]) / step_ms_attr}
+    attn_full_ms = mean(t_full)
+    att_full_gbs = full_bytes / (attn_full_ms / 1e3) / 1e9
+    roofline_attn = {"kernel": "full_step_kernel + attn_kernel (full-cache layers, split-K flash-decode)",
+                     "bound": "hbm", "achieved": att_full_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": att_full_gbs / hbm_peak, "traffic": None, "bytes_per_launch": full_bytes,
+                     "ms_per_launch": attn_full_ms, "peak_source": peak_src,
+                     "share_of_step": phase["full_cache_layers"] / step_ms_attr}
+    flag_extra_ms = sum(t_flg) - len(t_flg) * mean(t_unf)
+    gather_gbs = h2d_bytes / (flag_extra_ms / 1e3) / 1e9 if flag_extra_ms > 0 else 0.0
+    roofline_gather = {"kernel": "layer_kernel flagged-launch excess (score/select + host gather)", "bound": "host_link",
                        "achieved": gather_gbs, "peak": host_link_gbs, "unit": "GB/s",
                        "frac": gather_gbs / host_link_gbs if host_link_gbs else None,
-                       "traffic": h2d_bytes / max(A, 1), "share_of_step": phase["retrieve"] / step_ms_attr,
+                       "traffic": h2d_bytes / max(A, 1),
+                       "share_of_step": phase["retrieval_layers_flagged"] / step_ms_attr,
                        "peak_source": "pinned 256 MiB cudaMemcpy H2D measured in this run"}
-    roofline = roofline_gather if dominant == "retrieve" else roofline_attn
+    roofline = roofline_layer
+    retr_ms_total = flag_extra_ms
 
     retrievals = st_b["retrievals"] - st_a["retrievals"]
     n_ret_layers = L - len(full)
@@ -438,15 +451,16 @@ def main():
         "gpu_launches": launches_per_step * K,
         "clocks": clk,
         "roofline": roofline,
-        "roofline_attention": roofline_attn,
+        "roofline_full_cache": roofline_attn,
         "roofline_gather": roofline_gather,
         "phases_ms_per_step": phase,
+        "layer_us": layer_us,
         "kmeans_keys_per_s": km_keys / (km_ms / 1e3) if km_ms > 0 else None,
         "kmeans": {"ms_total": km_ms, "keys": km_keys, "iters": cfg.kmeans_iters,
                    "impl": "tcgen05" if args.kmeans_impl == 0 else "simt", "full_cache_copy_ms": full_ms,
                    "prompt_offload_bytes": st0["bytes_d2h"]},
         "retrieve_us_per_step": {"per_flagged_layer_call": (retr_ms_total * 1e3 / max(1, st_d['retrievals'] - st_c['retrievals'])),
-                                 "amortized_per_step": phase["retrieve"] * 1e3},
+                                 "amortized_per_step": flag_extra_ms * 1e3 / max(A, 1)},
         "retrievals_per_step": retrievals / K / max(n_ret_layers, 1) / b,
         "stats_timed": {k_: st_b[k_] - st_a[k_] for k_ in st_b},
         "host_link_h2d_gbs": host_link_gbs,

@@ -163,6 +163,21 @@ louiskv_status louiskv_append_attn(louiskv_ctx* ctx, int32_t layer, const void* 
                                    int64_t stride_kv, const void* q_own, int64_t stride_q, void* out,
                                    float* out_f32, void* stream);
 
+/* One whole decode step of one layer (Algorithm 1: trigger, retrieve when flagged,
+ * store_cache, attention), identical in results to should_retrieve -> retrieve ->
+ * append_output -> sparse_attn with q_own = q_all + kv_head_begin*g*d (same stride). On a
+ * retrieval layer it is ONE clustered launch (8 CTAs per (b, owned head)): every rank recomputes
+ * r_t (recipe R1), the flagged instances score and select with their units split over the 8
+ * ranks (histograms and minima exchanged through distributed shared memory), the ranks gather
+ * the new working set, rank 0 appends, all ranks attend one split each. Instances with more than
+ * 16384 units, and full-cache layers, issue the multi-kernel sequence instead. Arguments: q_all
+ * as in should_retrieve (stride_q), k_t/v_t as in append_output (stride_kv), out/out_f32 as in
+ * sparse_attn, d_flag_out/d_r_out optional device outputs as in should_retrieve.
+ * Errors: INVALID_ARG, STATE (as should_retrieve), CUDA. */
+louiskv_status louiskv_decode_layer(louiskv_ctx* ctx, int32_t layer, const void* q_all, int64_t stride_q,
+                                    const void* k_t, const void* v_t, int64_t stride_kv, void* out,
+                                    float* out_f32, uint8_t* d_flag_out, double* d_r_out, void* stream);
+
 /* ---- introspection (synchronous: they synchronise the device) ---- */
 /* Current working-set unit ids of (layer, b, owned head h), ascending. */
 louiskv_status louiskv_get_selection(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,

@@ -16,7 +16,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblouiskv.so")
+LIB_PATH = os.environ.get("LOUISKV_LIB", os.path.join(HERE, "liblouiskv.so"))  # (override: profiling build)
 
 OK, ERR_INVALID_ARG, ERR_STATE, ERR_CAPACITY, ERR_OOM_DEVICE, ERR_OOM_HOST, ERR_CUDA, ERR_NOT_IMPLEMENTED = range(8)
 TRIG_PREV_STEP, TRIG_LAST_RETRIEVAL = 0, 1
@@ -29,7 +29,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE"
 # ABI symbols declared in include/louiskv.h (checked by tests/test_abi.py)
 SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louiskv_set_prompt_units",
            "louiskv_should_retrieve", "louiskv_retrieve", "louiskv_append_output", "louiskv_sparse_attn",
-           "louiskv_append_attn",
+           "louiskv_append_attn", "louiskv_decode_layer",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
            "louiskv_get_stats", "louiskv_last_error", "louiskv_version"]
 
@@ -82,6 +82,7 @@ def lib():
         L.louiskv_append_output.argtypes = [vp, i32, vp, vp, i64, vp]
         L.louiskv_sparse_attn.argtypes = [vp, i32, vp, i64, vp, vp, vp]
         L.louiskv_append_attn.argtypes = [vp, i32, vp, vp, i64, vp, i64, vp, vp, vp]
+        L.louiskv_decode_layer.argtypes = [vp, i32, vp, i64, vp, vp, i64, vp, vp, vp, vp, vp]
         L.louiskv_get_selection.argtypes = [vp, i32, i32, i32, vp, i32, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_units.argtypes = [vp, i32, i32, i32, i32, vp, vp, vp, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_unit_positions.argtypes = [vp, i32, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64)]
@@ -199,6 +200,14 @@ class Context:
         assert k_t.stride(0) == v_t.stride(0)
         self._chk(self._L.louiskv_append_attn(self.h, layer, _ptr(k_t), _ptr(v_t), k_t.stride(0), _ptr(q_own),
                                               q_own.stride(0), _ptr(out), _ptr(out_f32), _stream(stream)))
+
+    def decode_layer(self, layer, q_all, k_t, v_t, out, out_f32=None, flag_out=None, r_out=None, stream=None):
+        """One whole decode step of one layer (trigger, retrieve, store_cache, attention); one
+        clustered launch on retrieval layers. q_all: [batch, Hq, d] (all heads)."""
+        assert k_t.stride(0) == v_t.stride(0)
+        self._chk(self._L.louiskv_decode_layer(self.h, layer, _ptr(q_all), q_all.stride(0), _ptr(k_t), _ptr(v_t),
+                                               k_t.stride(0), _ptr(out), _ptr(out_f32), _ptr(flag_out),
+                                               _ptr(r_out), _stream(stream)))
 
     # --- introspection ------------------------------------------------------
     def get_selection(self, layer, b, h):

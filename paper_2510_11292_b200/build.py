@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
          "-Xptxas", "-v", "-cudart", "static"]
-SOURCES = ["api.cu", "k_retrieve.cu", "k_append.cu", "k_attn.cu", "k_kmeans.cu", "k_kmeans_tc.cu"]
+SOURCES = ["api.cu", "k_retrieve.cu", "k_append.cu", "k_attn.cu", "k_layer.cu", "k_kmeans.cu", "k_kmeans_tc.cu"]
 
 
 def _stale(target, deps):
@@ -24,29 +24,34 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(verbose: bool = False, force: bool = False, prof: bool = False) -> str:
+    """prof=True: a separate liblouiskv_prof.so with per-phase %globaltimer stamps (-DLKV_PROF) for
+    tools/probe_phases.py; never loaded by the tests or the bench."""
+    objdir = os.path.join(HERE, "build_prof" if prof else "build")
+    lib = LIB.replace(".so", "_prof.so") if prof else LIB
+    flags = FLAGS + (["-DLKV_PROF"] if prof else [])
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, "lkv_internal.cuh"), os.path.join(INCLUDE, "louiskv.h")]
+    headers = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
+    headers.append(os.path.join(INCLUDE, "louiskv.h"))
     objs = []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+            cmd = [NVCC] + ARCH + flags + ["-c", src, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed for {s}")
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB + ".tmp"] + objs
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib + ".tmp"] + objs
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, prof="--prof" in sys.argv))

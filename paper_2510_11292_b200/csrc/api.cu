@@ -135,7 +135,6 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   a.tau = c->cfg.tau;
   a.qref = c->d_qref + (size_t)layer * 2 * c->Bmax * c->Hq * D;
   a.r = c->d_r + (size_t)layer * c->Bmax;
-  a.step = c->d_step + layer;
   a.flag = c->d_flag + (size_t)layer * c->Bmax;
   a.inst = c->d_inst + ib;
   a.centb = c->d_centb + ib * c->Umax * D;
@@ -165,7 +164,6 @@ AppendArgs append_args(louiskv_ctx* c, int layer, const void* k_t, const void* v
   a.stride_b = stride_b;
   a.batch = c->batch;
   a.hn = c->hn;
-  a.step = c->d_step + layer;
   a.W = c->W;
   a.max_open = c->max_open;
   a.ring_cap = c->ring_cap;
@@ -597,6 +595,47 @@ louiskv_status louiskv_append_attn(louiskv_ctx* c, int32_t layer, const void* k_
   a.fused = 1;
   a.app = append_args(c, layer, k_t, v_t, stride_kv);
   LKV_LAUNCH(c, launch_attn(a, st), "append+attn");
+  c->stage[layer] = 3;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q_all, int64_t stride_q,
+                                    const void* k_t, const void* v_t, int64_t stride_kv, void* out, float* out_f32,
+                                    uint8_t* d_flag_out, double* d_r_out, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (layer < 0 || layer >= c->L || !q_all || !k_t || !v_t || !out)
+    return fail(c, LOUISKV_ERR_INVALID_ARG, "decode_layer: bad args");
+  const void* q_own = reinterpret_cast<const bf16*>(q_all) + (int64_t)c->h0 * c->g * D;
+  if (is_full(c, layer)) {  // full-cache layer: the step kernel + the attention
+    louiskv_status s = louiskv_should_retrieve(c, layer, q_all, stride_q, d_flag_out, d_r_out, stream);
+    if (s == LOUISKV_OK) s = louiskv_retrieve(c, layer, q_own, stride_q, stream);
+    if (s == LOUISKV_OK) s = louiskv_append_attn(c, layer, k_t, v_t, stride_kv, q_own, stride_q, out, out_f32, stream);
+    return s;
+  }
+  if (c->P[layer] < 0) return fail(c, LOUISKV_ERR_STATE, "decode_layer before cluster_prompt");
+  if (c->stage[layer] != 0 && c->stage[layer] != 3)
+    return fail(c, LOUISKV_ERR_STATE, "decode_layer: previous step incomplete");
+  if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "decode_layer: max_output_len reached");
+  const int t = c->t[layer] + 1;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LayerArgs la{};
+  la.r = retrieve_args(c, layer, q_all, stride_q);
+  la.r.budget = std::max(c->Bud, 0);
+  la.r.flag_out = d_flag_out;
+  la.r.r_out = d_r_out;
+  if (c->cfg.boundary_mode == LOUISKV_BOUNDARY_SHARED && layer != c->cfg.shared_layer) {
+    const int sl = c->cfg.shared_layer;
+    if (c->t[sl] < t) return fail(c, LOUISKV_ERR_STATE, "SHARED: designated layer not yet called this step");
+    la.r.shared_copy = 1;
+    la.r.flag_src = c->d_flag + (size_t)sl * c->Bmax;
+    la.r.r_src = c->d_r + (size_t)sl * c->Bmax;
+  }
+  la.at = attn_args(c, layer, q_own, stride_q, out, out_f32);
+  la.at.fused = 1;
+  la.at.app = append_args(c, layer, k_t, v_t, stride_kv);
+  la.layer = layer;
+  LKV_LAUNCH(c, launch_layer(la, st), "decode_layer");
+  c->t[layer] = t;
   c->stage[layer] = 3;
   return LOUISKV_OK;
 }

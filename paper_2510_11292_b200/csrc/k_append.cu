@@ -17,7 +17,7 @@ namespace lkv {
 
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   pdl_wait_trigger();
-  append_one(a, blockIdx.x);
+  append_one(a, blockIdx.x, a.flag ? a.flag[blockIdx.x / a.hn] : 0);
 }
 
 // standalone gather of the pending jobs (unfused API path): grid (instances, row slices)

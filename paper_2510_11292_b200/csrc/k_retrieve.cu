@@ -17,34 +17,13 @@
 //      host pool; one RowSrc per destination row for the gather kernel.
 // gather_kernel: copies the rows (256 B K + 256 B V) with 16-B vector loads; host rows are
 //   read zero-copy over the host link ("directly transfer specific rows").
-#include "lkv_internal.cuh"
+#include "lkv_score_dev.cuh"
 
 namespace lkv {
 
 constexpr int SS_THREADS = 1024;
 constexpr int SS_WARPS = SS_THREADS / 32;
 constexpr int SORT_CAP = 12288;  // units whose keys/sizes live in shared memory (else global scratch)
-
-__device__ __forceinline__ float exp_r3(float x, const float* c) {
-  const float log2e = __double2float_rn(1.4426950408889634074);
-  float t = __fmul_rn(x, log2e);
-  if (t < -126.0f) return 0.0f;
-  float n = rintf(t);
-  float f = __fsub_rn(t, n);
-  float p = c[6];
-#pragma unroll
-  for (int i = 5; i >= 0; --i) p = __fmaf_rn(p, f, c[i]);
-  int ni = (int)n;
-  float scale = __int_as_float((ni + 127) << 23);
-  return __fmul_rn(p, scale);
-}
-
-__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
-  unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
-  lo = __shfl_xor_sync(0xffffffffu, lo, m);
-  hi = __shfl_xor_sync(0xffffffffu, hi, m);
-  return ((unsigned long long)hi << 32) | lo;
-}
 
 // ---- should_retrieve: semantic-boundary trigger (recipe R1) fused with the
 // logits of the flagged instances (recipe R2 step 1). Grid (unit slices, b*hn). Every CTA recomputes
@@ -58,7 +37,7 @@ __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a)
   const int li = blockIdx.y;
   const int b = li / a.hn, h = li % a.hn;
   const int tid = threadIdx.x;
-  const int t = *a.step + 1;
+  const int t = a.inst[li].step + 1;  // this instance's decode step (committed by its append)
   const int par = t & 1;
   __shared__ double s_cos[64];
   __shared__ int s_flag;
@@ -71,48 +50,10 @@ __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a)
       s_r = a.r_src[b];
     }
   } else {
-    // 16 lanes per head: lane l sums elements [8l, 8l+8) sequentially, then a fixed xor tree.
-    // Warp-uniform loop (two heads per warp); lanes past the last head shuffle zeros.
-    const int l16 = tid & 15, warp = tid >> 5, lane = tid & 31;
-    for (int hb = warp * 2; hb < a.Hq; hb += (TL_THREADS / 32) * 2) {
-      const int hh = hb + (lane >> 4);
-      const bool act = hh < a.Hq;
-      uint4 ua = make_uint4(0, 0, 0, 0), uc = ua;
-      if (act) {
-        ua = reinterpret_cast<const uint4*>(qr_old + hh * D)[l16];
-        uc = reinterpret_cast<const uint4*>(qc + hh * D)[l16];
-      }
-      float fa[8], fc[8];
-      unpack8(ua, fa);
-      unpack8(uc, fc);
-      double dot = 0.0, na = 0.0, nb = 0.0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const double x = (double)fa[e], y = (double)fc[e];
-        dot = __dadd_rn(dot, __dmul_rn(x, y));
-        na = __dadd_rn(na, __dmul_rn(x, x));
-        nb = __dadd_rn(nb, __dmul_rn(y, y));
-      }
-#pragma unroll
-      for (int off = 8; off >= 1; off >>= 1) {
-        dot = __dadd_rn(dot, __shfl_xor_sync(0xffffffffu, dot, off));
-        na = __dadd_rn(na, __shfl_xor_sync(0xffffffffu, na, off));
-        nb = __dadd_rn(nb, __shfl_xor_sync(0xffffffffu, nb, off));
-      }
-      if (act && l16 == 0) {
-        double cs = 0.0;
-        if (na != 0.0 && nb != 0.0) {
-          cs = __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
-          cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
-        }
-        s_cos[hh] = cs;
-      }
-    }
+    trigger_cosines<TL_THREADS>(qc, qr_old, a.Hq, s_cos);
     __syncthreads();
     if (tid == 0) {
-      double sum = 0.0;
-      for (int hh = 0; hh < a.Hq; ++hh) sum = __dadd_rn(sum, s_cos[hh]);
-      const double rr = __ddiv_rn(sum, (double)a.Hq);
+      const double rr = trigger_mean(s_cos, a.Hq);
       s_r = rr;
       s_flag = (t == 1) || (rr < a.tau);
     }
@@ -143,26 +84,11 @@ __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a)
   __syncthreads();
   const int u = blockIdx.x * TL_THREADS + tid;
   if (u >= n) return;
-  const uint4* row = reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D);
-  uint4 cr[D / 8];
-#pragma unroll
-  for (int c8 = 0; c8 < D / 8; ++c8) cr[c8] = __ldg(row + c8);
-  float acc[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) acc[j] = 0.0f;
-#pragma unroll
-  for (int c8 = 0; c8 < D / 8; ++c8) {
-    float cf[8];
-    unpack8(cr[c8], cf);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-#pragma unroll
-      for (int j = 0; j < G; ++j) acc[j] = __fmaf_rn(sq[j][c8 * 8 + k], cf[k], acc[j]);
-  }
-  const float inv_sqrt_d = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn((double)D)));
+  float l[G];
+  logits_row<G>(sq, reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D), l);
   float* E = a.scratch_e + (int64_t)li * G * a.Umax;
 #pragma unroll
-  for (int j = 0; j < G; ++j) E[(int64_t)j * a.Umax + u] = __fmul_rn(acc[j], inv_sqrt_d);
+  for (int j = 0; j < G; ++j) E[(int64_t)j * a.Umax + u] = l[j];
 }
 
 // block-wide exclusive scan of one int per thread (512 threads); returns the exclusive prefix
@@ -221,17 +147,7 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
     s_sz = reinterpret_cast<uint16_t*>(KEYS + 3 * a.Umax);
   }
 
-  if (tid == 0) {
-    double p = 1.0, fact = 1.0;
-    const double ln2 = 0.6931471805599453094;
-    for (int i = 0; i <= 6; ++i) {
-      if (i > 0) {
-        p = __dmul_rn(p, ln2);
-        fact = __dmul_rn(fact, (double)i);
-      }
-      s_coef[i] = __double2float_rn(__ddiv_rn(p, fact));
-    }
-  }
+  if (tid == 0) r3_coefs(s_coef);
   for (int i = tid; i < (a.Umax + 31) / 32; i += SS_THREADS) s_taken[i] = 0u;
   if (tid < G) s_z[tid] = 0ull;
   float* E = a.scratch_e + (int64_t)li * G * a.Umax;
@@ -494,8 +410,6 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
   pdl_wait_trigger();
   const int li = blockIdx.x;
   const int b = li / a.hn;
-  // commit the layer's device step counter (read by should_retrieve's kernel, then by append/attn)
-  if (li == 0 && threadIdx.x == 0) *a.step = *a.step + 1;
   if (!a.flag[b]) return;  // (jobs of unflagged instances were cleared by their consumer)
   const int n = a.inst[li].n_units;
   const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;

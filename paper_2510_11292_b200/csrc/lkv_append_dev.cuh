@@ -34,21 +34,24 @@ __device__ __forceinline__ void gather_rows(const AppendArgs& a, int li, const G
 }
 
 // Called by every thread of one CTA (blockDim >= 128: thread e < 128 owns dimension e of the
-// centroid); leaves the post-append state in global memory.
-__device__ __forceinline__ void append_one(const AppendArgs& a, const int li) {
+// centroid); `flag` = this step's trigger decision. The token's decode index is the instance's
+// completed-step count, which this call commits (+1); leaves the post-append state in global memory.
+__device__ __forceinline__ void append_one(const AppendArgs& a, const int li, const int flag) {
   const int b = li / a.hn;
   const int tid = threadIdx.x;
   InstState* S = a.inst + li;
-  const int flag = a.flag ? a.flag[b] : 0;
-  const int dec = *a.step - 1;  // decode index of this token (device step counter)
   const int cap = a.ring_cap;
   int2* fifo = a.fifo + (int64_t)li * cap;
   bf16* ringK = a.ring + (int64_t)li * 2 * cap * D;
   bf16* ringV = ringK + (int64_t)cap * D;
 
   __shared__ InstState s;  // (function-scope shared: one instance per CTA)
+  __shared__ int s_dec;
   if (tid == 0) {
     s = *S;
+    const int dec = s.step;  // decode index (0-based) of this token
+    s_dec = dec;
+    s.step = dec + 1;
     if ((flag && s.open_len > 0) || s.open_len >= a.max_open) {
       fifo[(s.fifo_head + s.fifo_count) % cap] = make_int2(s.open_start, s.open_len);
       s.fifo_count++;
@@ -59,8 +62,9 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li) {
     s.open_len++;
     s.buffered++;
   }
+  __syncthreads();
   // append the token's K and V rows
-  const int slot = dec % cap;
+  const int slot = s_dec % cap;
   if (tid < 16) {
     const uint4* src = reinterpret_cast<const uint4*>(a.k_t + (int64_t)b * a.stride_b + (int64_t)(li % a.hn) * D);
     reinterpret_cast<uint4*>(ringK + (int64_t)slot * D)[tid] = src[tid];

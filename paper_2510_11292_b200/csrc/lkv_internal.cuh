@@ -35,7 +35,7 @@ struct InstState {
   int32_t error;          // capacity overflow (sticky)
   int32_t prompt_len;     // P
   int32_t s_eff;          // min(S, P)
-  int32_t pad;
+  int32_t step;           // decode steps completed (read by the trigger, committed by the append)
 };
 
 // Gather job of one instance: written by select (retrieve), consumed by the gather of append_output
@@ -71,7 +71,6 @@ struct RetrieveArgs {
   double* r;                 // [batch] of this layer
   uint8_t* flag_out;         // optional caller outputs
   double* r_out;
-  int* step;                 // device step counter of this layer (read by both, committed by select)
   uint8_t* flag;             // [batch] of this layer
   GatherJob* jobs;           // [batch*hn] per-layer gather jobs
   InstState* inst;           // layer base, [batch*hn]
@@ -93,7 +92,7 @@ struct RetrieveArgs {
 };
 // should_retrieve on a retrieval layer: r_t / flag (recipe R1) + logits of flagged instances
 cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st);
-// retrieve: select (sort + greedy) + working-set layout + gather; commits the step counter
+// retrieve: select (sort + greedy) + working-set layout -> gather job
 cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st);
 
 // append (k_append.cu)
@@ -105,7 +104,6 @@ struct AppendArgs {
   const bf16* v_t;
   int64_t stride_b;
   int batch, hn, W, max_open, ring_cap, Umax;
-  const int* step;      // device step counter of this layer (t, 1-based, already advanced)
   const uint8_t* flag;  // [batch]
   InstState* inst;
   bf16* ring;           // layer base [batch*hn][2][ring_cap][D]
@@ -159,6 +157,17 @@ struct AttnArgs {
   AppendArgs app;
 };
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+
+// one decode step of one retrieval layer in ONE clustered launch (k_layer.cu): trigger (R1),
+// distributed score + select (R2/R3, greedy), gather, append, attention. r.q_own = q_all.
+struct LayerArgs {
+  RetrieveArgs r;
+  AttnArgs at;  // fused = 1, at.app = the append arguments
+  int layer;    // (LKV_PROF builds: timestamp rows of this layer)
+};
+constexpr int PROF_SLOTS = 16;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
+constexpr int LAYER_UNITS_MAX = 8 * 2048;  // units per instance the single launch keeps on chip (else global scratch)
+cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st);
 
 // k-means / prompt (k_kmeans.cu)
 struct KmArgs {
@@ -252,6 +261,17 @@ __device__ __forceinline__ void pdl_wait_trigger() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef LKV_PDL_EARLY_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+// ---- optional phase timestamps (-DLKV_PROF builds only): thread 0 writes %globaltimer into slot
+__device__ __forceinline__ void prof_stamp(unsigned long long* p, int slot) {
+#ifdef LKV_PROF
+  if (p && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p[slot] = g;
+  }
 #endif
 }
 

@@ -32,7 +32,9 @@ def small_cfg(**kw):
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
                 check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False):
-    """Drive GPU and oracle through `steps` decode steps; assert parity at every step."""
+    """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
+    fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
+    "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
     lkv = _lkv()
     hn = cfg.num_kv_heads - kv_head_begin if kv_head_count is None else kv_head_count
     h0 = kv_head_begin
@@ -67,11 +69,15 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
             qo = qa[:, h0 * g:(h0 + hn) * g]
             kt = inp.k[t, l][:, h0:h0 + hn]
             vt = inp.v[t, l][:, h0:h0 + hn]
-            ctx.should_retrieve(l, qa, flag_d, r_d)
-            ctx.retrieve(l, qo)
-            if fused:
+            if fused == "layer":
+                ctx.decode_layer(l, qa, kt.contiguous(), vt.contiguous(), out, out32, flag_d, r_d)
+            elif fused:
+                ctx.should_retrieve(l, qa, flag_d, r_d)
+                ctx.retrieve(l, qo)
                 ctx.append_attn(l, kt.contiguous(), vt.contiguous(), qo, out, out32)
             else:
+                ctx.should_retrieve(l, qa, flag_d, r_d)
+                ctx.retrieve(l, qo)
                 ctx.append_output(l, kt.contiguous(), vt.contiguous())
                 ctx.sparse_attn(l, qo, out, out32)
             f_o, r_o = ep.should_retrieve(l, np32(qa))
@@ -128,7 +134,8 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
 
 
 # ------------------------------------------------------------------ episodes
-@pytest.mark.parametrize("seed,fused", [(0, False), (1, False), (2, False), (0, True), (1, True)])
+@pytest.mark.parametrize("seed,fused", [(0, False), (1, False), (2, False), (0, True), (1, True), (0, "layer"),
+                                        (1, "layer"), (2, "layer")])
 def test_episode_oracle_clustering_small(seed, fused):
     cfg = small_cfg()
     inp = make_inputs(cfg, cfg.decode_steps, seed)
@@ -142,7 +149,8 @@ def test_episode_c1_shape():
     for hq in (1, 4):
         cfg = C1.replace(num_q_heads=hq)
         inp = make_inputs(cfg, cfg.decode_steps, 0)
-        run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=(hq == 4))
+        for fused in (hq == 4, "layer"):
+            run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused)
 
 
 def test_episode_last_retrieval_and_shared_modes():
@@ -150,19 +158,25 @@ def test_episode_last_retrieval_and_shared_modes():
     inp = make_inputs(cfg, 30, 3)
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), trigger_ref=LAST_RETRIEVAL)
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), boundary_mode=SHARED)
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), trigger_ref=LAST_RETRIEVAL,
+                fused="layer")
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), boundary_mode=SHARED,
+                fused="layer")
 
 
 def test_episode_degenerate_tau_budget_force_seal():
     cfg = small_cfg(decode_steps=30, tau=1.01, budget_tokens=0)   # retrieve every step, empty budget
     inp = make_inputs(cfg, 30, 4)
-    _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
-    assert st["units_selected"] == 0
+    for fused in (False, "layer"):
+        _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)
+        assert st["units_selected"] == 0
     cfg = small_cfg(decode_steps=30, tau=-1.0)                      # only t == 1
     _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]))
     assert st["retrievals"] == cfg.batch * 2
     cfg = small_cfg(decode_steps=30, tau=-1.0, window_tokens=6)     # force-seal at max_open=3
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3)
     run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3, fused=True)
+    run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), max_open=3, fused="layer")
 
 
 def test_superset_budget_equals_full_attention():
@@ -241,13 +255,29 @@ def test_duplicate_centroids_ties_to_lower_id():
     a[0, 0, 2 * half:] = k - 1
     inp.K[0] = K2
     run_episode(cfg, inp, 6, lambda l, Kn_: a)
+    run_episode(cfg, inp, 6, lambda l, Kn_: a, fused="layer")
+
+
+@pytest.mark.parametrize("prompt_len", [12000 + 16, 16600 + 16])
+def test_decode_layer_many_units(prompt_len):
+    """Single-size units (c=1): ~12K units keep 6 units per thread per rank in shared memory; ~16.6K
+    units exceed the on-chip capacity (16384) and run the global-scratch variant of the select."""
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=8, batch=1, num_kv_heads=1, num_q_heads=4,
+                    prompt_len=prompt_len, avg_cluster_size=1, budget_tokens=300, tau=0.95)
+    inp = make_inputs(cfg, 8, 10)
+    N = prompt_len - cfg.sink_tokens
+    a = np.arange(N, dtype=np.int32)[None, None, :]
+    for fused in (False, "layer"):
+        _, n_flags, st = run_episode(cfg, inp, 8, lambda l, Kn: a, fused=fused, compare_ws=(fused == "layer"))
+        assert st["units_scored"] >= N and n_flags >= 2
 
 
 def test_zero_query_and_prompt_shorter_than_sinks():
     cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=6, batch=1, prompt_len=12, sink_tokens=16)
     inp = make_inputs(cfg, 6, 8)
     inp.q[2] = 0  # zero query: cosine 0 (S:36)
-    run_episode(cfg, inp, 6, lambda l, Kn: np.zeros((1, 2, 0), np.int32))
+    for fused in (False, "layer"):
+        run_episode(cfg, inp, 6, lambda l, Kn: np.zeros((1, 2, 0), np.int32), fused=fused)
 
 
 def test_head_shard_equals_full_run():
@@ -256,7 +286,9 @@ def test_head_shard_equals_full_run():
     inp = make_inputs(cfg, 16, 9)
     # the shard's clustering is the corresponding slice of the full clustering
     full_assign = {l: planted_assign(cfg, inp.labels[l]) for l in range(cfg.num_layers)}
-    run_episode(cfg, inp, 16, lambda l, Kn: full_assign[l][:, 1:2], kv_head_begin=1, kv_head_count=1)
+    for fused in (False, "layer"):
+        run_episode(cfg, inp, 16, lambda l, Kn: full_assign[l][:, 1:2], kv_head_begin=1, kv_head_count=1,
+                    fused=fused)
 
 
 # ------------------------------------------------------------------ k-means (GPU clustering)
@@ -331,15 +363,17 @@ def test_kmeans_tiny_tail_and_repair():
 
 
 # ------------------------------------------------------------------ full sizes (bench launch config)
+@pytest.mark.timeout(1200)
 def test_c2_layer_full_size_sampled():
     """One C2 retrieval layer + one full-cache layer at full size (32K prompt, 8 KV heads, g=4)
     in the bench's launch configuration; clustering = planted labels (an oracle k-means at this
     size is out of reach); 24 decode steps compared every step on every head."""
     cfg = C2.replace(num_layers=2, full_cache_layers=(0,), decode_steps=24)
     inp = make_inputs(cfg, 24, 0)
-    worst, n_flags, st = run_episode(cfg, inp, 24, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
-                                     compare_ws=False, fused=True)
-    assert n_flags >= 3
+    for fused in (True, "layer"):
+        worst, n_flags, st = run_episode(cfg, inp, 24, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
+                                         compare_ws=False, fused=fused)
+        assert n_flags >= 3
 
 
 def test_c2_kmeans_full_size_properties():
