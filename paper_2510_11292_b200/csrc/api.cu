@@ -153,6 +153,8 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   a.rows = c->d_rows;
   a.jobs = c->d_jobs + (size_t)layer * c->inst_per_layer;
   a.stats = c->d_stats;
+  r3_coefs(a.r3c);
+  a.inv_sqrt_d = (float)(1.0 / std::sqrt((double)D));
   return a;
 }
 

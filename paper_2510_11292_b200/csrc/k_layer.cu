@@ -100,7 +100,7 @@ __device__ __forceinline__ int lk_select(const RetrieveArgs& a, const AppendArgs
   __shared__ int s_need, s_all, s_off, s_total;
   __shared__ int s_warp[LK_W + 1];
 
-  if (tid == 0) r3_coefs(s_coef);
+  if (tid < 7) s_coef[tid] = a.r3c[tid];
   for (int i = tid; i < (ES + 31) / 32; i += AT_THREADS) TK[i] = 0u;
   if (tid < G) x_z[tid] = 0ull;
 
@@ -111,7 +111,7 @@ __device__ __forceinline__ int lk_select(const RetrieveArgs& a, const AppendArgs
   for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
   for (int i = tid; i < cnt; i += AT_THREADS) {
     float l[G];
-    logits_row<G>(sq, reinterpret_cast<const uint4*>(centb + (int64_t)(lo + i) * D), l);
+    logits_row<G>(sq, reinterpret_cast<const uint4*>(centb + (int64_t)(lo + i) * D), a.inv_sqrt_d, l);
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       E[j * ES + i] = l[j];
@@ -383,6 +383,536 @@ __device__ __forceinline__ int lk_select(const RetrieveArgs& a, const AppendArgs
   return total;
 }
 
+// ---------------------------------------------------------------- replicated select (n <= LK_REP_N)
+// Every rank scores its 1/8 of the units, pushes its A bits to all ranks (DSMEM stores), and then
+// runs the whole greedy selection locally on the replicated keys: three cluster barriers in total
+// (max, normaliser, keys) and every rank knows the complete new layout.
+constexpr int LK_REP_N = 8192;    // units per instance
+constexpr int LK_REP_SEL = 1024;  // selected units (<= min(n, B))
+// shared-memory regions of the replicated select (bytes, by n): RA [0, 4n) | SZ [4n, 6n) | TK bits |
+// X (the rest of the idle attention staging area): own logits E, then the radix candidate lists,
+// then the tail candidates, then the selected-unit LIST
+__host__ __device__ constexpr int rep_off_tk(int n) { return (6 * n + 15) & ~15; }
+__host__ __device__ constexpr int rep_off_x(int n) { return (rep_off_tk(n) + ((n + 31) / 32) * 4 + 15) & ~15; }
+constexpr int REP_X_MIN = AT_STAGES * AT_STAGE_BYTES - rep_off_x(LK_REP_N);
+struct SelEnt {  // one selected unit, in id (= destination) order
+  int dst, sz, u, pad;
+  const uint8_t* kb;  // first K row (current working set, or the host pool span)
+  const uint8_t* vb;
+};
+static_assert(LK_REP_SEL * (int)sizeof(SelEnt) <= REP_X_MIN, "rep LIST smem");
+static_assert(8 * (LK_REP_N / AT_CL) * 4 <= REP_X_MIN, "rep E smem");
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ unsigned long long rep_key(const uint32_t* RA, int u) {
+  return ((unsigned long long)(~RA[u]) << 16) | (unsigned)u;
+}
+
+// Returns the row count of the new working set; *nsel = selected units (LIST entries); own_dst[i] =
+// destination row of own unit lo+i (-1: not selected) for the deferred sel/seloff update.
+template <int G>
+__device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li, const int rank, const int n,
+                                             const int ws_cur, const float (*sq)[D], uint8_t* dsm, int* nsel,
+                                             int* own_dst, unsigned long long* prof) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = (n + AT_CL - 1) / AT_CL;
+  const int lo = min(n, rank * m), hi = min(n, lo + m), cnt = hi - lo;
+  const int off_x = rep_off_x(n), x_bytes = AT_STAGES * AT_STAGE_BYTES - off_x;
+  uint32_t* RA = reinterpret_cast<uint32_t*>(dsm);             // [n] A bits (replicated)
+  uint16_t* SZ = reinterpret_cast<uint16_t*>(dsm + 4 * n);     // [n] sizes (each rank loads all)
+  uint32_t* TK = reinterpret_cast<uint32_t*>(dsm + rep_off_tk(n));  // [n/32] taken bits
+  float* E = reinterpret_cast<float*>(dsm + off_x);            // [G][m] own logits / exps
+  SelEnt* LIST = reinterpret_cast<SelEnt*>(dsm + off_x);       // (after E and the lists are dead)
+
+  __shared__ float s_coef[7];
+  __shared__ float x_max[AT_CL][G];               // pushed by every rank
+  __shared__ unsigned long long x_z[AT_CL][G];    // pushed by every rank
+  __shared__ unsigned long long s_zl[G];
+  __shared__ float s_red[LK_W][G];
+  __shared__ float s_M[G], s_Z[G];
+  __shared__ int s_hist[256];
+  __shared__ unsigned long long s_prefix, s_kt;
+  __shared__ unsigned long long s_kmin[LK_W];
+  __shared__ int s_need, s_all, s_total, s_nsel;
+  __shared__ int s_warp[LK_W + 1];
+
+  if (tid < 7) s_coef[tid] = a.r3c[tid];
+  if (tid < G) s_zl[tid] = 0ull;
+  for (int i = tid; i < (n + 31) / 32; i += AT_THREADS) TK[i] = 0u;
+  for (int i = tid; i < cnt; i += AT_THREADS) own_dst[i] = -1;
+  const int32_t* usize = a.usize + (int64_t)li * a.Umax;
+  // sizes: the first 8 x 256 loads stay in flight across the logits below
+  int szv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int u = i * AT_THREADS + tid;
+    szv[i] = u < n ? usize[u] : 0;
+  }
+  prof_stamp(prof, 20);
+
+  // ---- logits (R2) of the own units, cluster max per head
+  const bf16* centb = a.centb + (int64_t)li * a.Umax * D;
+  float mymax[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
+  for (int i = tid; i < cnt; i += AT_THREADS) {
+    float l[G];
+    logits_row<G>(sq, reinterpret_cast<const uint4*>(centb + (int64_t)(lo + i) * D), a.inv_sqrt_d, l);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      E[j * m + i] = l[j];
+      mymax[j] = fmaxf(mymax[j], l[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int u = i * AT_THREADS + tid;
+    if (u < n) SZ[u] = (uint16_t)clamp16(szv[i]);
+  }
+  for (int u = 8 * AT_THREADS + tid; u < n; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    float v = mymax[j];
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) s_red[warp][j] = v;
+  }
+  __syncthreads();
+  if (tid < G * AT_CL) {
+    const int j = tid % G, r = tid / G;
+    float v = -INFINITY;
+    for (int w = 0; w < LK_W; ++w) v = fmaxf(v, s_red[w][j]);
+    *cl.map_shared_rank(&x_max[rank][j], r) = v;
+  }
+  prof_stamp(prof, 6);
+  cl.sync();
+  if (tid < G) {
+    float v = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < AT_CL; ++r) v = fmaxf(v, x_max[r][tid]);
+    s_M[tid] = v;
+  }
+  __syncthreads();
+
+  // ---- exp (R3) + exact fixed-point normaliser (integer sums: order independent)
+  unsigned long long zl[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) zl[j] = 0ull;
+  for (int i = tid; i < cnt; i += AT_THREADS) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const float e = exp_r3(__fsub_rn(E[j * m + i], s_M[j]), s_coef);
+      E[j * m + i] = e;
+      zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    unsigned long long z = zl[j];
+    for (int o = 16; o; o >>= 1) z += shfl_xor_u64(z, o);
+    if (lane == 0 && z) atomicAdd(&s_zl[j], z);
+  }
+  __syncthreads();
+  if (tid < G * AT_CL) {
+    const int j = tid % G, r = tid / G;
+    *cl.map_shared_rank(&x_z[rank][j], r) = s_zl[j];
+  }
+  cl.sync();
+  if (tid < G) {
+    unsigned long long z = 0ull;
+#pragma unroll
+    for (int r = 0; r < AT_CL; ++r) z += x_z[r][tid];
+    s_Z[tid] = __fmul_rn(__ull2float_rn(z), __int_as_float((127 - 40) << 23));
+  }
+  __syncthreads();
+
+  // ---- A_u of the own units, pushed to every rank
+  for (int i = tid; i < cnt; i += AT_THREADS) {
+    float A = 0.0f;
+#pragma unroll
+    for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[j * m + i], s_Z[j]));
+    A = __fdiv_rn(A, (float)G);
+    const uint32_t bits = __float_as_uint(A);
+#pragma unroll
+    for (int r = 0; r < AT_CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+  }
+  if (tid == 0) {
+    s_prefix = 0ull;
+    s_need = a.budget;
+    s_all = 0;
+  }
+  cl.sync();
+  prof_stamp(prof, 13);
+
+  // ---- greedy skip-and-continue over all n keys, locally (exact):
+  // (a) first-skip pivot = the smallest key whose running size sum in key order exceeds B: a
+  //     size-weighted radix select over the key bits below the common prefix of all keys (8 bits
+  //     per pass), the candidate ids compacted to the chosen bucket after every pass;
+  // (b) every key below the pivot is taken; (c) after the pivot only units with size <= the
+  //     remaining budget can be taken (it never grows): they are compacted (key | size << 48) and
+  //     one warp walks them, one warp-wide min per take.
+  // candidate lists (key | size << 48) in region X: two of LCAP entries
+  unsigned long long* LB = reinterpret_cast<unsigned long long*>(dsm + off_x);
+  const int LCAP = x_bytes / 16;
+  constexpr unsigned long long M48 = 0xFFFFFFFFFFFFull;
+  constexpr int DIRECT = 512;  // candidates ranked directly (all pairs) instead of another pass
+  __shared__ int s_nc, s_tb;
+  __shared__ unsigned long long s_kmax[LK_W];
+  const int per = (n + AT_THREADS - 1) / AT_THREADS;
+  const int u0 = min(n, tid * per), u1 = min(n, u0 + per);
+  {
+    unsigned long long kmn = ~0ull, kmx = 0ull;
+    for (int u = u0; u < u1; ++u) {
+      const unsigned long long k = rep_key(RA, u);
+      kmn = k < kmn ? k : kmn;
+      kmx = k > kmx ? k : kmx;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long y = shfl_xor_u64(kmn, o), z = shfl_xor_u64(kmx, o);
+      kmn = y < kmn ? y : kmn;
+      kmx = z > kmx ? z : kmx;
+    }
+    if (lane == 0) {
+      s_kmin[warp] = kmn;
+      s_kmax[warp] = kmx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < LK_W; ++w) {
+        kmn = s_kmin[w] < kmn ? s_kmin[w] : kmn;
+        kmx = s_kmax[w] > kmx ? s_kmax[w] : kmx;
+      }
+      if (n == 0 || (n == 1 && SZ[0] <= s_need)) {
+        s_all = 1;
+        s_tb = -1;
+      } else if (n == 1) {
+        s_prefix = kmn;  // the single unit does not fit: it is the pivot
+        s_tb = -1;
+      } else {
+        const int tb = 63 - __clzll(kmn ^ kmx);
+        s_tb = tb;
+        s_prefix = kmn & ~((2ull << tb) - 1ull);  // common prefix of every key
+      }
+    }
+    __syncthreads();
+  }
+  int tb = s_tb, nc = 0, cb = -1;  // cb = -1: candidates = all keys matching the prefix above tb
+  bool first_pass = true;
+  while (tb >= 0) {
+    const int lo_bit = tb >= 7 ? tb - 7 : 0;
+    const unsigned wmask = (2u << (tb - lo_bit)) - 1u;
+    const unsigned long long himask = (~0ull << (tb + 1)) & M48, pre0 = s_prefix;
+    s_hist[tid] = 0;
+    __syncthreads();
+    if (cb < 0) {
+      for (int u = tid; u < n; u += AT_THREADS) {
+        const unsigned long long k = rep_key(RA, u);
+        if ((k & himask) == pre0) atomicAdd(&s_hist[(unsigned)(k >> lo_bit) & wmask], (int)SZ[u]);
+      }
+    } else {
+      const unsigned long long* L = LB + cb * LCAP;
+      for (int i = tid; i < nc; i += AT_THREADS) {
+        const unsigned long long e = L[i];
+        atomicAdd(&s_hist[(unsigned)((e & M48) >> lo_bit) & wmask], (int)(e >> 48));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int v[8], ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = s_hist[lane * 8 + i];
+        ls += v[i];
+      }
+      int incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - ls;
+      const int need = s_need;
+      const unsigned hit = __ballot_sync(0xffffffffu, incl > need);
+      if (lane == 0) s_nc = 0;
+      if (hit == 0u) {
+        if (lane == 0) s_all = 1;  // (only possible on the first pass) the whole set fits the budget
+      } else {
+        const int first = __ffs(hit) - 1;
+        if (lane == first) {
+          int cum = excl, bk = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (cum + v[i] > need) {
+              bk = i;
+              break;
+            }
+            cum += v[i];
+          }
+          s_need = need - cum;
+          s_prefix |= (unsigned long long)(lane * 8 + bk) << lo_bit;
+        }
+      }
+    }
+    __syncthreads();
+    if (first_pass) prof_stamp(prof, 16);
+    first_pass = false;
+    if (s_all || lo_bit == 0) break;
+    tb = lo_bit - 1;
+    // compact the chosen bucket's candidates (if they fit the list capacity)
+    const unsigned long long msk = (~0ull << lo_bit) & M48, pre = s_prefix;
+    const int dsti = cb < 0 ? 0 : cb ^ 1;
+    unsigned long long* dstl = LB + dsti * LCAP;
+    if (cb < 0) {
+      for (int u0c = warp * 32; u0c < n; u0c += AT_THREADS) {
+        const int u = u0c + lane;
+        unsigned long long k = 0;
+        bool keep = false;
+        if (u < n) {
+          k = rep_key(RA, u);
+          keep = (k & msk) == pre;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (keep && slot < LCAP) dstl[slot] = k | ((unsigned long long)SZ[u] << 48);
+      }
+    } else {
+      const unsigned long long* L = LB + cb * LCAP;
+      for (int i0 = warp * 32; i0 < nc; i0 += AT_THREADS) {
+        const int i = i0 + lane;
+        unsigned long long e = 0;
+        bool keep = false;
+        if (i < nc) {
+          e = L[i];
+          keep = (e & msk) == pre;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) dstl[base + __popc(bal & ((1u << lane) - 1u))] = e;
+      }
+    }
+    __syncthreads();
+    if (s_nc > LCAP) {
+      cb = -1;  // (too many to list: the next pass filters all keys by the prefix again)
+      continue;
+    }
+    cb = dsti;
+    nc = s_nc;
+    if (nc <= DIRECT) {
+      // direct finish: the pivot is the candidate whose running size sum (in key order) crosses need
+      const unsigned long long* L = LB + cb * LCAP;
+      const int need = s_need;
+      for (int ci = tid; ci < nc; ci += AT_THREADS) {
+        const unsigned long long e = L[ci], k = e & M48;
+        int below = 0;
+        for (int cj = 0; cj < nc; ++cj) {
+          const unsigned long long f = L[cj];
+          if ((f & M48) < k) below += (int)(f >> 48);
+        }
+        if (below <= need && below + (int)(e >> 48) > need) {
+          s_prefix = k;
+          s_need = need - below;
+        }
+      }
+      __syncthreads();
+      break;
+    }
+  }
+  prof_stamp(prof, 17);
+  const bool all = s_all != 0;
+  const unsigned long long pivot = all ? ~0ull : s_prefix;
+  const int rem1 = all ? 0 : s_need;
+  // (b) prefix run taken; (c) tail candidates compacted as key | size << 48
+  unsigned long long* T = LB;  // (the lists are dead)
+  const int T_CAP = x_bytes / 8;
+  __syncthreads();  // (the id lists in the same region are dead)
+  if (tid == 0) s_nc = 0;
+  __syncthreads();
+  for (int u = u0; u < u1; ++u) {
+    const unsigned long long k = rep_key(RA, u);
+    if (k < pivot) {
+      atomicOr(&TK[u >> 5], 1u << (u & 31));
+    } else if (rem1 > 0 && k > pivot && SZ[u] <= rem1) {
+      const int slot = atomicAdd(&s_nc, 1);
+      if (slot < T_CAP) T[slot] = k | ((unsigned long long)SZ[u] << 48);
+    }
+  }
+  prof_stamp(prof, 15);
+  __syncthreads();
+  if (rem1 > 0) {
+    const int nt = s_nc;
+    int rem = rem1;
+    unsigned long long last = pivot;
+    if (nt <= T_CAP) {
+      if (warp == 0) {  // one warp, no block barriers per take
+        while (rem > 0) {
+          unsigned long long best = ~0ull;
+#pragma unroll 4
+          for (int i = lane; i < nt; i += 32) {
+            const unsigned long long e = T[i];
+            const unsigned long long k = e & 0xFFFFFFFFFFFFull;
+            if (k > last && k < best && (int)(e >> 48) <= rem) best = k;
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const unsigned long long y = shfl_xor_u64(best, o);
+            best = y < best ? y : best;
+          }
+          if (best == ~0ull) break;
+          const int ut = (int)(best & 0xFFFFull);
+          rem -= SZ[ut];
+          last = best;
+          if (lane == 0) atomicOr(&TK[ut >> 5], 1u << (ut & 31));
+        }
+      }
+    } else {  // (many small units after the pivot) block-wide min per take over all keys
+      while (rem > 0) {
+        unsigned long long best = ~0ull;
+        for (int u = u0; u < u1; ++u) {
+          const unsigned long long k = rep_key(RA, u);
+          if (k > last && k < best && SZ[u] <= rem) best = k;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const unsigned long long y = shfl_xor_u64(best, o);
+          best = y < best ? y : best;
+        }
+        if (lane == 0) s_kmin[warp] = best;
+        __syncthreads();
+        if (tid == 0) {
+          unsigned long long v = ~0ull;
+          for (int w = 0; w < LK_W; ++w) v = s_kmin[w] < v ? s_kmin[w] : v;
+          s_kt = v;
+        }
+        __syncthreads();
+        const unsigned long long kt = s_kt;
+        if (kt == ~0ull) break;
+        const int ut = (int)(kt & 0xFFFFull);
+        rem -= SZ[ut];
+        last = kt;
+        if (tid == 0) atomicOr(&TK[ut >> 5], 1u << (ut & 31));
+      }
+    }
+  }
+  __syncthreads();
+  prof_stamp(prof, 18);
+  if (tid == 0 && prof) prof[21] = s_nc;  // (tail candidates)
+
+  // ---- layout (selected units in id order) and the selected-unit list with row sources; the old
+  // sel/seloff are only read here (their update is deferred past the cluster's last barrier)
+  int rows_l = 0, cnt_l = 0;
+  for (int u = u0; u < u1; ++u)
+    if (TK[u >> 5] >> (u & 31) & 1u) {
+      rows_l += SZ[u];
+      ++cnt_l;
+    }
+  int total, ns;
+  int dst = lk_scan(rows_l, s_warp, total);
+  int k = lk_scan(cnt_l, s_warp, ns);
+  prof_stamp(prof, 19);
+  const int64_t gi = a.inst_global_base + li;
+  const uint8_t* curK = reinterpret_cast<const uint8_t*>(a.ws + ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride);
+  const uint8_t* curV = curK + (int64_t)a.budget * ROW_BYTES;
+  const uint8_t* pool = a.pool + (int64_t)li * a.pool_inst_bytes;
+  const uint8_t* sel = a.sel + (int64_t)li * a.Umax;
+  const int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
+  const int64_t* uoff = a.uoff + (int64_t)li * a.Umax;
+  unsigned long long reused = 0, fetched = 0, hbytes = 0;
+  for (int u = u0; u < u1; ++u) {
+    if (!(TK[u >> 5] >> (u & 31) & 1u)) continue;
+    const int sz = SZ[u];
+    const uint8_t had = sel[u];  // (the three loads are independent: one round trip)
+    const int so = seloff[u];
+    const int64_t uo = uoff[u];
+    SelEnt e;
+    e.dst = dst;
+    e.sz = sz;
+    e.u = u;
+    e.pad = 0;
+    if (had) {
+      e.kb = curK + (int64_t)so * ROW_BYTES;
+      e.vb = curV + (int64_t)so * ROW_BYTES;
+      ++reused;
+    } else {
+      const uint8_t* base = pool + uo * POOL_ROW_BYTES;
+      e.kb = base;
+      e.vb = base + (int64_t)sz * ROW_BYTES;
+      ++fetched;
+      hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
+    }
+    LIST[k++] = e;
+    if (u >= lo && u < hi) own_dst[u - lo] = dst;
+    dst += sz;
+  }
+  if (rank == 0) {
+    for (int o = 16; o; o >>= 1) {
+      reused += __shfl_xor_sync(0xffffffffu, reused, o);
+      fetched += __shfl_xor_sync(0xffffffffu, fetched, o);
+      hbytes += __shfl_xor_sync(0xffffffffu, hbytes, o);
+    }
+    if (lane == 0 && (reused | fetched)) {
+      atomicAdd(&a.stats->units_reused, reused);
+      atomicAdd(&a.stats->units_fetched, fetched);
+      atomicAdd(&a.stats->bytes_h2d, hbytes);
+    }
+    if (tid == 0) {
+      atomicAdd(&a.stats->units_selected, (unsigned long long)ns);
+      atomicAdd(&a.stats->units_scored, (unsigned long long)n);
+      if (li % a.hn == 0) atomicAdd(&a.stats->retrievals, 1ull);
+    }
+  }
+  if (tid == 0) {
+    s_total = total;
+    s_nsel = ns;
+  }
+  __syncthreads();
+  *nsel = s_nsel;
+  return s_total;
+}
+
+// Gather rows [R0, R1) of the new working set (sources from the selected-unit list; 16 lanes x 16 B
+// per row, four rows in flight per half-warp): new units zero-copy from the pinned host pool, kept
+// units device-to-device.
+__device__ __forceinline__ void lk_gather_list(const SelEnt* LIST, const int nsel, const int R0, const int R1,
+                                               uint8_t* nxtK, uint8_t* nxtV) {
+  const int sub = threadIdx.x & 15, hw = threadIdx.x >> 4;
+  for (int base = R0 + hw; base < R1; base += 4 * AT_HW) {
+    uint4 kv[4], vv[4];
+    int rr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = base + i * AT_HW;
+      rr[i] = r;
+      if (r < R1) {
+        int lo = 0, hi = nsel - 1;  // last entry with dst <= r
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (LIST[mid].dst <= r) lo = mid;
+          else hi = mid - 1;
+        }
+        const int off = r - LIST[lo].dst;
+        kv[i] = reinterpret_cast<const uint4*>(LIST[lo].kb + (int64_t)off * ROW_BYTES)[sub];
+        vv[i] = reinterpret_cast<const uint4*>(LIST[lo].vb + (int64_t)off * ROW_BYTES)[sub];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (rr[i] < R1) {
+        reinterpret_cast<uint4*>(nxtK + (int64_t)rr[i] * ROW_BYTES)[sub] = kv[i];
+        reinterpret_cast<uint4*>(nxtV + (int64_t)rr[i] * ROW_BYTES)[sub] = vv[i];
+      }
+  }
+}
+
 #ifdef LKV_PROF
 __device__ unsigned long long g_lkv_prof[64][2048][PROF_SLOTS];
 #endif
@@ -403,44 +933,175 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) layer_kernel(Layer
   const int li = blockIdx.x / AT_CL, rank = blockIdx.x % AT_CL;
   const int b = li / a.hn, h = li % a.hn, tid = threadIdx.x;
   extern __shared__ __align__(128) uint8_t lk_smem[];
-  __shared__ int s_t, s_n, s_cur, s_flag;
-  __shared__ double s_r;
+  __shared__ __align__(16) InstState s_S;  // state before this step
+  __shared__ InstState s_post;             // after this step's store_cache (attention window only)
+  __shared__ int2 s_fifo[32];
   __shared__ double s_cos[64];
+  __shared__ double s_r;
+  __shared__ int s_flag;
   __shared__ float sq[G][D];
-  if (tid == 0) {
-    const InstState* S = a.inst + li;
-    s_t = S->step + 1;  // read before the first cluster barrier; rank 0 commits t in append_one
-    s_n = S->n_units;
-    s_cur = S->ws_cur;
+  constexpr int DS = D / AT_CL;  // output dims finalised by each rank
+  __shared__ float mg_acc[AT_CL][G][DS];
+  __shared__ float mg_ml[AT_CL][G][2];
+  __shared__ int s_own_dst[LK_REP_N / AT_CL];
+  InstState* S = a.inst + li;
+
+  // ---- 1. loads: the instance state and (Hq <= 32) the trigger operands: q_t and BOTH q_ref
+  // buffers, so no load waits for the step parity
+  if (tid < 4) reinterpret_cast<uint4*>(&s_S)[tid] = reinterpret_cast<const uint4*>(S)[tid];
+  const int l8 = tid & 7, hh = tid >> 3;
+  const bool fast_trig = !a.shared_copy && a.Hq <= AT_THREADS / 8;
+  const bool act = fast_trig && hh < a.Hq;
+  const uint4* qc4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b);
+  const uint4* qr4[2] = {reinterpret_cast<const uint4*>(a.qref + ((int64_t)0 * a.Bmax + b) * a.Hq * D),
+                         reinterpret_cast<const uint4*>(a.qref + ((int64_t)1 * a.Bmax + b) * a.Hq * D)};
+  uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0, r00 = c0, r01 = c0, r10 = c0, r11 = c0;
+  if (act) {
+    c0 = qc4[hh * 16 + l8];
+    c1 = qc4[hh * 16 + l8 + 8];
+    r00 = qr4[0][hh * 16 + l8];
+    r01 = qr4[0][hh * 16 + l8 + 8];
+    r10 = qr4[1][hh * 16 + l8];
+    r11 = qr4[1][hh * 16 + l8 + 8];
   }
   __syncthreads();
-  // every rank's read of the instance state happens-before rank 0's append commits it: split cluster
-  // barrier, arrived here and waited on after the trigger (the trigger hides its latency)
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   prof_stamp(prof, 2);
-  const int t = s_t, par = t & 1;
+  {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/8): centroid rows, sizes and
+     // the old selection / pool offsets. The trigger resolves in ~2 us; on an unflagged step the
+     // lines are simply not used (the step is latency-bound, HBM mostly idle).
+    const int nu = s_S.n_units, mu = (nu + AT_CL - 1) / AT_CL;
+    const int plo = min(nu, rank * mu), phi = min(nu, plo + mu);
+    const uint8_t* cb8 = reinterpret_cast<const uint8_t*>(a.centb + ((int64_t)li * a.Umax + plo) * D);
+    for (int i = tid; i < 2 * (phi - plo); i += AT_THREADS) prefetch_l2(cb8 + (int64_t)i * 128);
+    const int64_t ib = (int64_t)li * a.Umax;
+    const uint8_t* p_us = reinterpret_cast<const uint8_t*>(a.usize + ib + plo);
+    const uint8_t* p_so = reinterpret_cast<const uint8_t*>(a.seloff + ib + plo);
+    const uint8_t* p_uo = reinterpret_cast<const uint8_t*>(a.uoff + ib + plo);
+    const uint8_t* p_se = a.sel + ib + plo;
+    const int nl4 = ((phi - plo) * 4 + 127) / 128, nl8 = ((phi - plo) * 8 + 127) / 128, nl1 = (phi - plo + 127) / 128;
+    if (tid < nl4) {
+      prefetch_l2(p_us + tid * 128);
+      prefetch_l2(p_so + tid * 128);
+    }
+    if (tid < nl8) prefetch_l2(p_uo + tid * 128);
+    if (tid < nl1) prefetch_l2(p_se + tid * 128);
+  }
+  const int t = s_S.step + 1, par = t & 1;
+  const int cap = app.ring_cap;
+  if (tid >= 32 && tid < 64) {  // prefetch the sealed-segment FIFO head entries (evictions)
+    const int k = tid - 32;
+    if (k < s_S.fifo_count) s_fifo[k] = app.fifo[(int64_t)li * cap + (s_S.fifo_head + k) % cap];
+  }
+  // every rank's reads of the instance state happen-before the appending rank commits it: split
+  // cluster barrier, arrived here and waited on before the first later barrier
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+
+  // ---- 2. trigger r_t (recipe R1), identical on every rank: 8 lanes per head, lane l8 sums dims
+  // [8 l8, 8 l8 + 8) and [8 l8 + 64, 8 l8 + 72) sequentially, adds them (the tree's first level),
+  // then the xor tree 4, 2, 1
   const uint16_t* qc = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b;
   const uint16_t* qr_old = reinterpret_cast<const uint16_t*>(a.qref) + ((int64_t)(par ^ 1) * a.Bmax + b) * a.Hq * D;
-
-  // ---- 1. trigger (R1), identical on every rank
-  if (a.shared_copy) {
-    if (tid == 0) {
-      s_flag = a.flag_src[b];
-      s_r = a.r_src[b];
+  if (fast_trig) {
+    const uint4 ra0 = par ? r00 : r10, ra1 = par ? r01 : r11;  // q_ref buffer (t - 1) & 1
+    double dot[2], na[2], nb[2];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float fa[8], fc[8];
+      unpack8(half ? ra1 : ra0, fa);
+      unpack8(half ? c1 : c0, fc);
+      double d_ = 0.0, a_ = 0.0, b_ = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double x = (double)fa[e], y = (double)fc[e];
+        d_ = __dadd_rn(d_, __dmul_rn(x, y));
+        a_ = __dadd_rn(a_, __dmul_rn(x, x));
+        b_ = __dadd_rn(b_, __dmul_rn(y, y));
+      }
+      dot[half] = d_;
+      na[half] = a_;
+      nb[half] = b_;
     }
-  } else {
+    double dt = __dadd_rn(dot[0], dot[1]), an = __dadd_rn(na[0], na[1]), bn = __dadd_rn(nb[0], nb[1]);
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+      dt = __dadd_rn(dt, __shfl_xor_sync(0xffffffffu, dt, off));
+      an = __dadd_rn(an, __shfl_xor_sync(0xffffffffu, an, off));
+      bn = __dadd_rn(bn, __shfl_xor_sync(0xffffffffu, bn, off));
+    }
+    if (act && l8 == 0) {
+      double cs = 0.0;
+      if (an != 0.0 && bn != 0.0) {
+        cs = __ddiv_rn(dt, __dmul_rn(__dsqrt_rn(an), __dsqrt_rn(bn)));
+        cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
+      }
+      s_cos[hh] = cs;
+    }
+    // the owned KV head's g query rows (scoring operand) are already in registers
+    const int jq = hh - (a.h0 + h) * G;
+    if (act && jq >= 0 && jq < G) {
+      float f[8];
+      unpack8(c0, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sq[jq][8 * l8 + e] = f[e];
+      unpack8(c1, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sq[jq][64 + 8 * l8 + e] = f[e];
+    }
+  } else if (!a.shared_copy) {
     trigger_cosines<AT_THREADS>(qc, qr_old, a.Hq, s_cos);
-    __syncthreads();
-    if (tid == 0) {
-      const double rr = trigger_mean(s_cos, a.Hq);
-      s_r = rr;
-      s_flag = (t == 1) || (rr < a.tau);
-    }
   }
   __syncthreads();
-  const int flag = s_flag;
+  if (tid == 0) {
+    int flag;
+    if (a.shared_copy) {
+      flag = a.flag_src[b];
+      s_r = a.r_src[b];
+    } else {
+      const double rr = trigger_mean(s_cos, a.Hq);
+      s_r = rr;
+      flag = (t == 1) || (rr < a.tau);
+    }
+    s_flag = flag;
+    // post-store_cache window (the same seal / append / evict rules as append_one, state only)
+    InstState p = s_S;
+    const int dec = p.step;
+    int2 pushed = make_int2(0, 0);
+    int pushed_k = -1;
+    if ((flag && p.open_len > 0) || p.open_len >= app.max_open) {
+      pushed = make_int2(p.open_start, p.open_len);
+      pushed_k = p.fifo_count;
+      p.fifo_count++;
+      p.open_len = 0;
+    }
+    if (p.open_len == 0) p.open_start = dec;
+    if (p.buffered == 0) p.ring_head = dec;
+    p.open_len++;
+    p.buffered++;
+    int k = 0;
+    while (p.buffered > app.W && p.fifo_count > 0 && !p.error) {
+      const int2 seg = k == pushed_k ? pushed
+                       : k < 32     ? s_fifo[k]
+                                    : app.fifo[(int64_t)li * cap + (s_S.fifo_head + k) % cap];
+      if (p.n_units >= app.Umax || p.pool_rows + seg.y > app.pool_rows_cap) {
+        p.error = 1;
+        break;
+      }
+      p.n_units++;
+      p.pool_rows += seg.y;
+      p.buffered -= seg.y;
+      p.ring_head += seg.y;
+      p.fifo_head = (p.fifo_head + 1) % cap;
+      p.fifo_count--;
+      ++k;
+    }
+    s_post = p;
+  }
+  __syncthreads();
   prof_stamp(prof, 3);
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#ifdef LKV_PROF
+  if (prof && tid == 0) prof[22] = clock64();
+#endif
+  const int flag = s_flag;
   if (rank == 0 && h == 0) {
     if (tid == 0) {
       a.flag[b] = (uint8_t)flag;
@@ -455,37 +1116,146 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) layer_kernel(Layer
     }
   }
 
-  // ---- 2. retrieve: distributed score + select, then the gather spread over the ranks
+  // ---- 3. retrieve (flagged): select, then gather this rank's 1/8 of the new working set; the
+  // rank attends exactly the rows it gathered, so no barrier separates gather and attention
+  const int64_t gi = a.inst_global_base + li;
+  const int n = s_S.n_units, ws_cur = s_S.ws_cur;
+  const bf16* ws_k;  // this rank's working-set rows
+  int ws_n;
+  bool rep = false;
+  int total = 0;
   if (flag) {
-    const uint16_t* qb = qc + (int64_t)(a.h0 + h) * G * D;
-    for (int i = tid; i < G * D; i += AT_THREADS) sq[i / D][i % D] = bf2f(qb[i]);
-    __syncthreads();
-    const int total = s_n <= AT_CL * LK_MCAP ? lk_select<G, true>(a, app, li, rank, s_n, s_cur, sq, lk_smem)
-                                             : lk_select<G, false>(a, app, li, rank, s_n, s_cur, sq, lk_smem);
-    prof_stamp(prof, 4);
-    cg::this_cluster().sync();  // row table complete (cluster-scope release/acquire)
-    if (total > 0) {
-      const int64_t gi = a.inst_global_base + li;
-      bf16* nxtK = a.ws + (s_cur ^ 1) * a.ws_buf_stride + gi * a.ws_inst_stride;
-      const GatherJob J{total, 0, nxtK, nxtK + (int64_t)a.budget * D};
-      const int per = (total + AT_CL - 1) / AT_CL;
-      const int r0 = rank * per, r1 = min(total, r0 + per);
-      if (r0 < r1) gather_rows(app, li, J, r0, r1);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (!fast_trig) {
+      const uint16_t* qb = qc + (int64_t)(a.h0 + h) * G * D;
+      for (int i = tid; i < G * D; i += AT_THREADS) sq[i / D][i % D] = bf2f(qb[i]);
+      __syncthreads();
+    }
+    bf16* nxtK = a.ws + (ws_cur ^ 1) * a.ws_buf_stride + gi * a.ws_inst_stride;
+    rep = n <= LK_REP_N && min(n, a.budget) <= LK_REP_SEL;
+    if (rep) {
+      int nsel;
+      total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, s_own_dst, prof);
+      prof_stamp(prof, 4);
+#ifdef LKV_PROF
+      if (prof && tid == 0) prof[23] = clock64();
+#endif
+      const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
+      lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_off_x(n)), nsel, R0, R1,
+                     reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
+      ws_k = nxtK + (int64_t)R0 * D;
+      ws_n = R1 - R0;
+    } else {
+      total = n <= AT_CL * LK_MCAP ? lk_select<G, true>(a, app, li, rank, n, ws_cur, sq, lk_smem)
+                                   : lk_select<G, false>(a, app, li, rank, n, ws_cur, sq, lk_smem);
+      prof_stamp(prof, 4);
+      cg::this_cluster().sync();  // row table complete (cluster-scope release/acquire)
+      const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
+      if (R0 < R1) gather_rows(app, li, GatherJob{total, 0, nxtK, nxtK + (int64_t)a.budget * D}, R0, R1);
+      ws_k = nxtK + (int64_t)R0 * D;
+      ws_n = R1 - R0;
+    }
+  } else {
+    const int wr = s_S.ws_rows;
+    const int R0 = wr * rank / AT_CL, R1 = wr * (rank + 1) / AT_CL;
+    ws_k = a.ws + ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride + (int64_t)R0 * D;
+    ws_n = R1 - R0;
+  }
+  prof_stamp(prof, 5);
+
+  // ---- 4. attention over this rank's 1/8 of sinks, working set and post-append local window; the
+  // last rank owns the window's tail, i.e. the new token, and writes its row itself first
+  const AttnArgs& at = A.at;
+  bf16* ringK = app.ring + (int64_t)li * 2 * cap * D;
+  bf16* ringV = ringK + (int64_t)cap * D;
+  if (rank == AT_CL - 1 && tid < 32) {
+    const int slot = s_S.step % cap;
+    const uint4* src = reinterpret_cast<const uint4*>((tid < 16 ? app.k_t : app.v_t) + (int64_t)b * app.stride_b +
+                                                      (int64_t)h * D);
+    reinterpret_cast<uint4*>((tid < 16 ? ringK : ringV) + (int64_t)slot * D)[tid & 15] = src[tid & 15];
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes (gather, token) -> TMA reads
+  Pieces P;
+  P.np = 0;
+  {
+    const int se = s_S.s_eff;
+    const int s0 = se * rank / AT_CL, s1 = se * (rank + 1) / AT_CL;
+    const bf16* sk = at.sinks + (int64_t)li * 2 * at.S * D;
+    P.add(s1 - s0, sk + (int64_t)s0 * D, sk + (int64_t)at.S * D + (int64_t)s0 * D);
+    P.add(ws_n, ws_k, ws_k + (int64_t)a.budget * D);
+    const int nb = s_post.buffered;
+    const int w0 = nb * rank / AT_CL, w1 = nb * (rank + 1) / AT_CL;
+    const int hs = (s_post.ring_head + w0) % cap;
+    const int first = min(w1 - w0, cap - hs);
+    P.add(first, ringK + (int64_t)hs * D, ringV + (int64_t)hs * D);
+    P.add(w1 - w0 - first, ringK, ringV);
+  }
+  int rows = 0;
+  for (int p = 0; p < P.np; ++p) rows += P.n[p];
+  prof_stamp(prof, 7);
+  const uint16_t* qown = qc + (int64_t)(a.h0 + h) * G * D;
+  const float* part = attn_partial<G>(qown, at.scale_log2, P, 0, rows, prof);
+
+  // ---- 5. merge: every rank pushes its partial's dims [16 r, 16 r + 16) to rank r and its (max, sum)
+  // to all ranks (DSMEM stores), one cluster barrier, each rank finalises 16 dims of every head
+  cg::cluster_group cl = cg::this_cluster();
+  // (unflagged: complete the entry barrier first — it also guarantees every rank has started, so
+  // its shared memory may be written)
+  if (!flag) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  for (int idx = tid; idx < G * D; idx += AT_THREADS) {
+    const int j = idx / D, e = idx % D;
+    *cl.map_shared_rank(&mg_acc[rank][j][e % DS], e / DS) = part[j * (D + 2) + e];
+  }
+  if (tid < G * AT_CL) {
+    const int j = tid % G, r = tid / G;
+    float* dm = cl.map_shared_rank(&mg_ml[rank][j][0], r);
+    dm[0] = part[j * (D + 2) + D];
+    dm[1] = part[j * (D + 2) + D + 1];
+  }
+  prof_stamp(prof, 10);
+  cl.sync();
+  prof_stamp(prof, 11);
+  if (tid < G * DS) {
+    const int j = tid / DS, e = tid % DS;
+    float M = -INFINITY;
+#pragma unroll
+    for (int y = 0; y < AT_CL; ++y) M = fmaxf(M, mg_ml[y][j][0]);
+    float Lsum = 0.f, Acc = 0.f;
+#pragma unroll
+    for (int y = 0; y < AT_CL; ++y) {
+      const float w = mg_ml[y][j][0] == -INFINITY ? 0.f : exp2f(mg_ml[y][j][0] - M);
+      Lsum = fmaf(w, mg_ml[y][j][1], Lsum);
+      Acc = fmaf(w, mg_acc[y][j][e], Acc);
+    }
+    const float o = Acc / Lsum;
+    const int64_t oi = ((int64_t)(b * a.hn + h) * G + j) * D + rank * DS + e;
+    at.out[oi] = __float2bfloat16_rn(o);
+    if (at.out_f32) at.out_f32[oi] = o;
+  }
+  prof_stamp(prof, 12);
+
+  // ---- 6. deferred state updates (every rank has read the old selection by now)
+  if (flag && rep) {
+    const int m = (n + AT_CL - 1) / AT_CL;
+    const int lo = min(n, rank * m), hi = min(n, lo + m);
+    uint8_t* sel = a.sel + (int64_t)li * a.Umax;
+    int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
+    for (int u = lo + tid; u < hi; u += AT_THREADS) {
+      const int d = s_own_dst[u - lo];
+      if (d >= 0) {
+        sel[u] = 1;
+        seloff[u] = d;
+      } else if (sel[u]) {
+        sel[u] = 0;
+      }
+    }
+    if (rank == 0 && tid == 0) {
+      S->ws_cur = ws_cur ^ 1;
+      S->ws_rows = total;
     }
   }
-
-  // ---- 3. store_cache (rank 0), publish to the cluster (generic writes -> TMA reads: proxy fences)
-  prof_stamp(prof, 5);
-  if (rank == 0) append_one(app, li, flag);
-  prof_stamp(prof, 6);
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  cg::this_cluster().sync();
-  prof_stamp(prof, 7);
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // select used the staging smem
-
-  // ---- 4. attention, one split per rank
-  attn_body<G, true>(A.at, li, rank, AT_CL, prof);
+  // store_cache side effects (seal / append / evict) by the last rank; commits the step
+  if (rank == AT_CL - 1) append_one(app, li, flag, &s_S);
   prof_stamp(prof, 14);
 }
 

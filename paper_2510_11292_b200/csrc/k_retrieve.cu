@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a)
   const int u = blockIdx.x * TL_THREADS + tid;
   if (u >= n) return;
   float l[G];
-  logits_row<G>(sq, reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D), l);
+  logits_row<G>(sq, reinterpret_cast<const uint4*>(a.centb + ((int64_t)li * a.Umax + u) * D), a.inv_sqrt_d, l);
   float* E = a.scratch_e + (int64_t)li * G * a.Umax;
 #pragma unroll
   for (int j = 0; j < G; ++j) E[(int64_t)j * a.Umax + u] = l[j];
@@ -147,7 +147,7 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
     s_sz = reinterpret_cast<uint16_t*>(KEYS + 3 * a.Umax);
   }
 
-  if (tid == 0) r3_coefs(s_coef);
+  if (tid < 7) s_coef[tid] = a.r3c[tid];
   for (int i = tid; i < (a.Umax + 31) / 32; i += SS_THREADS) s_taken[i] = 0u;
   if (tid < G) s_z[tid] = 0ull;
   float* E = a.scratch_e + (int64_t)li * G * a.Umax;

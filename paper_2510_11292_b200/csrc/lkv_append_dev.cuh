@@ -36,7 +36,10 @@ __device__ __forceinline__ void gather_rows(const AppendArgs& a, int li, const G
 // Called by every thread of one CTA (blockDim >= 128: thread e < 128 owns dimension e of the
 // centroid); `flag` = this step's trigger decision. The token's decode index is the instance's
 // completed-step count, which this call commits (+1); leaves the post-append state in global memory.
-__device__ __forceinline__ void append_one(const AppendArgs& a, const int li, const int flag) {
+// pre: optional copy of the instance state already in shared memory (else loaded from global).
+// The working-set fields (ws_cur, ws_rows) belong to the retrieval and are not written here.
+__device__ __forceinline__ void append_one(const AppendArgs& a, const int li, const int flag,
+                                           const InstState* pre = nullptr) {
   const int b = li / a.hn;
   const int tid = threadIdx.x;
   InstState* S = a.inst + li;
@@ -48,7 +51,7 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, co
   __shared__ InstState s;  // (function-scope shared: one instance per CTA)
   __shared__ int s_dec;
   if (tid == 0) {
-    s = *S;
+    s = pre ? *pre : *S;
     const int dec = s.step;  // decode index (0-based) of this token
     s_dec = dec;
     s.step = dec + 1;
@@ -128,7 +131,18 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, co
     __syncthreads();
   }
   __syncthreads();
-  if (tid == 0) *S = s;
+  if (tid == 0) {
+    S->n_units = s.n_units;
+    S->pool_rows = s.pool_rows;
+    S->open_len = s.open_len;
+    S->open_start = s.open_start;
+    S->buffered = s.buffered;
+    S->ring_head = s.ring_head;
+    S->fifo_head = s.fifo_head;
+    S->fifo_count = s.fifo_count;
+    S->error = s.error;
+    S->step = s.step;
+  }
 }
 
 

@@ -16,7 +16,7 @@ constexpr int AT_SMEM = AT_STAGES * AT_STAGE_BYTES + 64;
 constexpr int AT_CL = 8;  // cluster size of the fused append+attention launch (one cluster per instance)
 
 struct RowSpan {
-  const bf16* k0;  // sinks
+  const bf16* k0;  // sinks (or the full cache)
   const bf16* v0;
   int n0;
   const bf16* k1;  // working set
@@ -27,72 +27,42 @@ struct RowSpan {
   int head, cap;
 };
 
-__device__ __forceinline__ void row_ptrs(const RowSpan& sp, int r, const uint4*& kp, const uint4*& vp) {
-  if (r < sp.n0) {
-    kp = reinterpret_cast<const uint4*>(sp.k0 + (int64_t)r * D);
-    vp = reinterpret_cast<const uint4*>(sp.v0 + (int64_t)r * D);
-    return;
+// Rows of an attention set as up to AT_PMAX contiguous pieces in virtual-row order.
+constexpr int AT_PMAX = 4;
+struct Pieces {
+  int np;
+  int v0[AT_PMAX], n[AT_PMAX];
+  const bf16* k[AT_PMAX];
+  const bf16* v[AT_PMAX];
+  __device__ __forceinline__ void add(int cnt, const bf16* kb, const bf16* vb) {
+    if (cnt > 0) {
+      const int base = np ? v0[np - 1] + n[np - 1] : 0;
+      v0[np] = base;
+      n[np] = cnt;
+      k[np] = kb;
+      v[np] = vb;
+      ++np;
+    }
   }
-  r -= sp.n0;
-  if (r < sp.n1) {
-    kp = reinterpret_cast<const uint4*>(sp.k1 + (int64_t)r * D);
-    vp = reinterpret_cast<const uint4*>(sp.v1 + (int64_t)r * D);
-    return;
-  }
-  r -= sp.n1;
-  const int slot = (sp.head + r) % sp.cap;
-  kp = reinterpret_cast<const uint4*>(sp.k2 + (int64_t)slot * D);
-  vp = reinterpret_cast<const uint4*>(sp.v2 + (int64_t)slot * D);
-}
+};
 
-// Attention of instance li, split `split` of `nsplit` (FUSED: nsplit = AT_CL ranks of one cluster,
-// merged through DSMEM; else global partials merged by the last CTA). Every thread of the CTA calls.
-template <int G, bool FUSED>
-__device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const int split, const int nsplit,
-                                          unsigned long long* prof = nullptr) {
-  namespace cg = cooperative_groups;
-  const int b = li / a.hn, h = li % a.hn;
+// CTA-level flash-decode partial over virtual rows [r_begin, r_end) of the pieces, for the G query
+// heads at qb (bf16 [G][D]). Returns the merged partial in shared memory, [G][D+2] floats:
+// unnormalised accumulator (log2-domain max subtracted), then (max, sum). Every thread calls;
+// the caller's subsequent reads of the result are ordered by the internal barriers.
+template <int G>
+__device__ __forceinline__ float* attn_partial(const uint16_t* qb, const float scale_log2, const Pieces& P,
+                                               const int r_begin, const int r_end, unsigned long long* prof) {
   const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
-
-  RowSpan sp;
-  int n_rows;
-  if (a.inst) {
-    const InstState& S = a.inst[li];
-    const int64_t gi = a.inst_global_base + li;
-    sp.k0 = a.sinks + (int64_t)li * 2 * a.S * D;
-    sp.v0 = sp.k0 + (int64_t)a.S * D;
-    sp.n0 = S.s_eff;
-    sp.k1 = a.ws + S.ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride;
-    sp.v1 = sp.k1 + (int64_t)a.B * D;
-    sp.n1 = S.ws_rows;
-    sp.k2 = a.ring + (int64_t)li * 2 * a.ring_cap * D;
-    sp.v2 = sp.k2 + (int64_t)a.ring_cap * D;
-    sp.head = S.ring_head;
-    sp.cap = a.ring_cap;
-    n_rows = sp.n0 + sp.n1 + S.buffered;
-  } else {
-    sp.k0 = a.full + (int64_t)li * 2 * a.full_cap * D;
-    sp.v0 = sp.k0 + a.full_cap * D;
-    const int64_t rows = a.full_P + *a.step;
-    n_rows = (int)(rows < a.full_cap ? rows : a.full_cap);
-    sp.n0 = n_rows;
-    sp.n1 = 0;
-    sp.k1 = sp.v1 = sp.k2 = sp.v2 = nullptr;
-    sp.head = 0;
-    sp.cap = 1;
-  }
-  const int r_begin = (int)((int64_t)n_rows * split / nsplit);
-  const int r_end = (int)((int64_t)n_rows * (split + 1) / nsplit);
-
+  const int np = P.np;
   // query fragment: this lane's 8 dims for each of the G heads, pre-scaled into log2 domain
   float q[G][8];
-  const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)h * G * D;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     uint4 u = reinterpret_cast<const uint4*>(qb + j * D)[sub];
     unpack8(u, q[j]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) q[j][k] *= a.scale_log2;
+    for (int k = 0; k < 8; ++k) q[j][k] *= scale_log2;
   }
   float m[G], l[G], acc[G][8];
 #pragma unroll
@@ -103,41 +73,9 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const
     for (int k = 0; k < 8; ++k) acc[j][k] = 0.f;
   }
 
-  // ---- rows stream through shared memory: 64-row chunks, AT_STAGES-deep ring, filled by TMA
-  // bulk copies (each piece of the attention set is contiguous: sinks, working set, ring (with
-  // one wrap), or the full cache); thread 0 is the producer, all warps consume every chunk.
   extern __shared__ __align__(128) uint8_t at_smem[];
   uint8_t* sKV = at_smem;  // [AT_STAGES][K 64x256 B | V 64x256 B]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(at_smem + AT_STAGES * AT_STAGE_BYTES);
-  // pieces in virtual-row order: (first virtual row, count, K base, V base)
-  int p_v0[4], p_n[4];
-  const bf16* p_k[4];
-  const bf16* p_vv[4];
-  int np = 0;
-  {
-    int v = 0;
-    auto add = [&](int cnt, const bf16* kb, const bf16* vb) {
-      if (cnt > 0) {
-        p_v0[np] = v;
-        p_n[np] = cnt;
-        p_k[np] = kb;
-        p_vv[np] = vb;
-        ++np;
-        v += cnt;
-      }
-    };
-    if (a.inst) {
-      add(sp.n0, sp.k0, sp.v0);
-      add(sp.n1, sp.k1, sp.v1);
-      const int nb = n_rows - sp.n0 - sp.n1;
-      const int h0 = sp.head % sp.cap;
-      const int first = nb < sp.cap - h0 ? nb : sp.cap - h0;
-      add(first, sp.k2 + (int64_t)h0 * D, sp.v2 + (int64_t)h0 * D);
-      add(nb - first, sp.k2, sp.v2);
-    } else {
-      add(sp.n0, sp.k0, sp.v0);
-    }
-  }
   const int n_chunks = (r_end - r_begin + AT_CHUNK - 1) / AT_CHUNK;
   auto issue = [&](int c) {
     const int st = c % AT_STAGES;
@@ -146,11 +84,11 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const
     uint8_t* dV = dK + AT_CHUNK * ROW_BYTES;
     ptx_mbar_expect_tx(&full_bar[st], (uint32_t)(c1 - c0) * 2 * ROW_BYTES);
     for (int p = 0; p < np; ++p) {
-      const int lo = max(c0, p_v0[p]), hi = min(c1, p_v0[p] + p_n[p]);
+      const int lo = max(c0, P.v0[p]), hi = min(c1, P.v0[p] + P.n[p]);
       if (lo >= hi) continue;
       const uint32_t bytes = (uint32_t)(hi - lo) * ROW_BYTES;
-      ptx_bulk_g2s(dK + (lo - c0) * ROW_BYTES, p_k[p] + (int64_t)(lo - p_v0[p]) * D, bytes, &full_bar[st]);
-      ptx_bulk_g2s(dV + (lo - c0) * ROW_BYTES, p_vv[p] + (int64_t)(lo - p_v0[p]) * D, bytes, &full_bar[st]);
+      ptx_bulk_g2s(dK + (lo - c0) * ROW_BYTES, P.k[p] + (int64_t)(lo - P.v0[p]) * D, bytes, &full_bar[st]);
+      ptx_bulk_g2s(dV + (lo - c0) * ROW_BYTES, P.v[p] + (int64_t)(lo - P.v0[p]) * D, bytes, &full_bar[st]);
     }
   };
   if (tid == 0) {
@@ -270,9 +208,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const
   }
   __syncthreads();
 
-  // per-CTA partial: global scratch (split merge by the last CTA) or own smem (cluster merge)
-  float* part = FUSED ? reinterpret_cast<float*>(at_smem + AT_W * G * D * sizeof(float))
-                      : a.part + ((int64_t)li * nsplit + split) * G * (D + 2);
+  float* part = reinterpret_cast<float*>(at_smem + AT_W * G * D * sizeof(float));
   for (int idx = tid; idx < G * D; idx += AT_THREADS) {
     const int j = idx / D, e = idx % D;
     float M = -INFINITY;
@@ -290,6 +226,69 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const
       part[j * (D + 2) + D] = M;
       part[j * (D + 2) + D + 1] = Lsum;
     }
+  }
+  __syncthreads();
+  return part;
+}
+
+// Attention of instance li, split `split` of `nsplit` (FUSED: nsplit = AT_CL ranks of one cluster,
+// merged through DSMEM; else global partials merged by the last CTA). Every thread of the CTA calls.
+template <int G, bool FUSED>
+__device__ __forceinline__ void attn_body(const AttnArgs& a, const int li, const int split, const int nsplit,
+                                          unsigned long long* prof = nullptr) {
+  namespace cg = cooperative_groups;
+  const int b = li / a.hn, h = li % a.hn;
+  const int tid = threadIdx.x;
+  RowSpan sp;
+  int n_rows;
+  if (a.inst) {
+    const InstState& S = a.inst[li];
+    const int64_t gi = a.inst_global_base + li;
+    sp.k0 = a.sinks + (int64_t)li * 2 * a.S * D;
+    sp.v0 = sp.k0 + (int64_t)a.S * D;
+    sp.n0 = S.s_eff;
+    sp.k1 = a.ws + S.ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride;
+    sp.v1 = sp.k1 + (int64_t)a.B * D;
+    sp.n1 = S.ws_rows;
+    sp.k2 = a.ring + (int64_t)li * 2 * a.ring_cap * D;
+    sp.v2 = sp.k2 + (int64_t)a.ring_cap * D;
+    sp.head = S.ring_head;
+    sp.cap = a.ring_cap;
+    n_rows = sp.n0 + sp.n1 + S.buffered;
+  } else {
+    sp.k0 = a.full + (int64_t)li * 2 * a.full_cap * D;
+    sp.v0 = sp.k0 + a.full_cap * D;
+    const int64_t rows = a.full_P + *a.step;
+    n_rows = (int)(rows < a.full_cap ? rows : a.full_cap);
+    sp.n0 = n_rows;
+    sp.n1 = 0;
+    sp.k1 = sp.v1 = sp.k2 = sp.v2 = nullptr;
+    sp.head = 0;
+    sp.cap = 1;
+  }
+  const int r_begin = (int)((int64_t)n_rows * split / nsplit);
+  const int r_end = (int)((int64_t)n_rows * (split + 1) / nsplit);
+
+  Pieces P;
+  P.np = 0;
+  if (a.inst) {
+    P.add(sp.n0, sp.k0, sp.v0);
+    P.add(sp.n1, sp.k1, sp.v1);
+    const int nb = n_rows - sp.n0 - sp.n1;
+    const int h0 = sp.head % sp.cap;
+    const int first = nb < sp.cap - h0 ? nb : sp.cap - h0;
+    P.add(first, sp.k2 + (int64_t)h0 * D, sp.v2 + (int64_t)h0 * D);
+    P.add(nb - first, sp.k2, sp.v2);
+  } else {
+    P.add(sp.n0, sp.k0, sp.v0);
+  }
+  const uint16_t* qb = reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)h * G * D;
+  float* part_s = attn_partial<G>(qb, a.scale_log2, P, r_begin, r_end, prof);
+  // per-CTA partial: own smem (cluster merge) or global scratch (split merge by the last CTA)
+  float* part = part_s;
+  if constexpr (!FUSED) {
+    part = a.part + ((int64_t)li * nsplit + split) * G * (D + 2);
+    for (int i = tid; i < G * (D + 2); i += AT_THREADS) part[i] = part_s[i];
   }
 
   if constexpr (FUSED) {

@@ -89,6 +89,8 @@ struct RetrieveArgs {
   uint8_t* scratch_sort;     // [batch*hn][Umax * 14] sort buffers when n exceeds the smem capacity
   RowSrc* rows;              // [batch*hn][B]
   StatsDev* stats;
+  float r3c[7];              // recipe R3 Taylor coefficients fl32(ln2^i / i!) (r3_coefs)
+  float inv_sqrt_d;          // recipe R2 scale fl32(1 / fl64(sqrt(d)))
 };
 // should_retrieve on a retrieval layer: r_t / flag (recipe R1) + logits of flagged instances
 cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st);
@@ -165,7 +167,7 @@ struct LayerArgs {
   AttnArgs at;  // fused = 1, at.app = the append arguments
   int layer;    // (LKV_PROF builds: timestamp rows of this layer)
 };
-constexpr int PROF_SLOTS = 16;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
+constexpr int PROF_SLOTS = 24;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
 constexpr int LAYER_UNITS_MAX = 8 * 2048;  // units per instance the single launch keeps on chip (else global scratch)
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st);
 
@@ -219,6 +221,20 @@ cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t
 cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st);
 
 bool kmeans_tc_available();
+
+// Recipe R3's 7 Taylor coefficients fl32(ln2^i / i!): IEEE double products and quotient (round to
+// nearest), then one rounding to float; computed on the host once per call.
+inline void r3_coefs(float* c) {
+  double p = 1.0, fact = 1.0;
+  const double ln2 = 0.6931471805599453094;
+  for (int i = 0; i <= 6; ++i) {
+    if (i > 0) {
+      p = p * ln2;
+      fact = fact * (double)i;
+    }
+    c[i] = (float)(p / fact);
+  }
+}
 
 // Launch with the programmatic-stream-serialization attribute (PDL); captured into CUDA graphs as
 // programmatic edges.

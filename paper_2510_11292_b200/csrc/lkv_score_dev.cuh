@@ -23,18 +23,6 @@ __device__ __forceinline__ float exp_r3(float x, const float* c) {
   return __fmul_rn(p, scale);
 }
 
-// the 7 Taylor coefficients fl32(ln2^i / i!) of recipe R3 (one thread)
-__device__ __forceinline__ void r3_coefs(float* c) {
-  double p = 1.0, fact = 1.0;
-  const double ln2 = 0.6931471805599453094;
-  for (int i = 0; i <= 6; ++i) {
-    if (i > 0) {
-      p = __dmul_rn(p, ln2);
-      fact = __dmul_rn(fact, (double)i);
-    }
-    c[i] = __double2float_rn(__ddiv_rn(p, fact));
-  }
-}
 
 __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
   unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
@@ -92,8 +80,10 @@ __device__ __forceinline__ double trigger_mean(const double* s_cos, int Hq) {
 }
 
 // R2 logits of one unit row (bf16 centroid, 256 B) against the G query heads in sq (fp32)
+// (inv_sqrt_d = fl32(1 / fl64(sqrt(d))), computed on the host: RetrieveArgs::inv_sqrt_d)
 template <int G>
-__device__ __forceinline__ void logits_row(const float (*sq)[D], const uint4* row, float* out) {
+__device__ __forceinline__ void logits_row(const float (*sq)[D], const uint4* row, const float inv_sqrt_d,
+                                           float* out) {
   uint4 cr[D / 8];
 #pragma unroll
   for (int c8 = 0; c8 < D / 8; ++c8) cr[c8] = __ldg(row + c8);
@@ -109,7 +99,6 @@ __device__ __forceinline__ void logits_row(const float (*sq)[D], const uint4* ro
 #pragma unroll
       for (int j = 0; j < G; ++j) acc[j] = __fmaf_rn(sq[j][c8 * 8 + k], cf[k], acc[j]);
   }
-  const float inv_sqrt_d = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn((double)D)));
 #pragma unroll
   for (int j = 0; j < G; ++j) out[j] = __fmul_rn(acc[j], inv_sqrt_d);
 }

@@ -1,0 +1,86 @@
+"""Probe: per-phase timeline of the retrieval-layer kernel inside the graph-replayed C2 step.
+
+Needs the profiling build (python paper_2510_11292_b200/build.py --prof); loads it through
+LOUISKV_LIB. Slots (globaltimer ns, thread 0 of every CTA): 0 entry, 1 after griddepcontrol.wait,
+2 state read, 3 trigger done, 4 select done (flagged), 5 gather done, 6 append done (rank 0),
+7 after publish barrier, 8 first attention chunk landed, 9 main loop done, 10/11 merge barrier,
+12/13 final barrier, 14 exit. Reports medians relative to the launch's earliest entry.
+"""
+import ctypes, json, os, sys
+import numpy as np
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+os.environ["LOUISKV_LIB"] = os.path.join(ROOT, "paper_2510_11292_b200", "liblouiskv_prof.so")
+sys.path.insert(0, ROOT)
+import torch
+import paper_2510_11292_b200 as lkv
+import synth
+from synth.configs import CONFIGS
+
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
+tau = float(sys.argv[2]) if len(sys.argv) > 2 else None
+if tau is not None:
+    cfg = cfg.replace(tau=tau)
+dev = torch.device("cuda", 0)
+L, full, b, Hkv = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch, cfg.num_kv_heads
+STEPS = 24
+ctx = lkv.Context(lkv.make_config(cfg, max_output_len=STEPS + 4))
+plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
+for l in range(L):
+    K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
+    ctx.cluster_prompt(l, K, V)
+    del K, V
+q, kk, vv, _ = synth.decode_stream(cfg, STEPS + 2, 0, dev, plants)
+q_in, k_in, v_in = q[0].clone(), kk[0].clone(), vv[0].clone()
+out = torch.empty_like(q_in)
+flags = torch.zeros((L, b), dtype=torch.uint8, device=dev)
+
+
+def issue():
+    for l in range(L):
+        ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], flag_out=flags[l])
+
+
+issue()
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.graph(g, stream=s):
+    issue()
+rd = lkv.lib().louiskv_prof_read
+rd.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+buf = np.zeros((64, 2048, 24), np.uint64)
+n_cta = b * Hkv * 8
+rows = {"unflagged": [], "flagged": []}
+gaps = []
+for i in range(1, STEPS + 1):
+    q_in.copy_(q[i]); k_in.copy_(kk[i]); v_in.copy_(vv[i])
+    g.replay()
+    torch.cuda.synchronize()
+    if i < 4:
+        continue
+    assert rd(buf.ctypes.data, buf.nbytes) == 0
+    fl = flags.cpu().numpy()
+    prev_end = None
+    for l in range(L):
+        if l in full:
+            prev_end = None
+            continue
+        t = buf[l, :n_cta].astype(np.int64)
+        t0 = t[:, 0].min()
+        rel = (t - t0).astype(np.float64)
+        rel[t == 0] = np.nan
+        rel[:, 21] = t[:, 21]  # a count, not a time
+        ok = (t[:, 23] > t[:, 22]) & (t[:, 4] > t[:, 3])
+        rel[:, 22] = np.where(ok, (t[:, 23] - t[:, 22]) / np.maximum(t[:, 4] - t[:, 3], 1), np.nan)  # SM GHz
+        rel[:, 23] = np.nan
+        key = "flagged" if fl[l].any() else "unflagged"
+        rows[key].append(np.nanmedian(rel, axis=0).tolist() + [np.nanmax(rel[:, 14])])
+        buf[l] = 0
+        if prev_end is not None:
+            gaps.append(t0 - prev_end)
+        prev_end = t[:, 14].max()
+res = {k: (np.median(np.array(v), axis=0).round(0).tolist() if v else None) for k, v in rows.items()}
+res["n"] = {k: len(v) for k, v in rows.items()}
+res["gap_prev_exit_to_entry_ns_median"] = float(np.median(gaps)) if gaps else None
+print(json.dumps(res))
