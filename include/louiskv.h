@@ -54,6 +54,7 @@ enum { LOUISKV_TRIG_PREV_STEP = 0, LOUISKV_TRIG_LAST_RETRIEVAL = 1 };
 enum { LOUISKV_BOUNDARY_PER_LAYER = 0, LOUISKV_BOUNDARY_SHARED = 1 };
 enum { LOUISKV_FETCH_ZERO_COPY = 0 };
 enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
+enum { LOUISKV_ATTN_TC = 0, LOUISKV_ATTN_SIMT = 1 };
 
 typedef struct {
   int32_t num_layers, num_q_heads, num_kv_heads, head_dim; /* head_dim must be 128 */
@@ -74,6 +75,8 @@ typedef struct {
   int32_t max_open_segment;  /* force-seal bound on the open segment (0 -> window_tokens) */
   int32_t fetch_mode;        /* LOUISKV_FETCH_ZERO_COPY */
   int32_t device;            /* CUDA device ordinal */
+  int32_t attn_impl;         /* full-cache attention: LOUISKV_ATTN_TC (mma.sync + TMA tensor maps,
+                                default) | LOUISKV_ATTN_SIMT (CUDA cores) */
 } louiskv_config;
 
 typedef struct {

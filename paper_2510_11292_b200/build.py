@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
          "-Xptxas", "-v", "-cudart", "static"]
-SOURCES = ["api.cu", "k_retrieve.cu", "k_append.cu", "k_attn.cu", "k_layer.cu", "k_kmeans.cu", "k_kmeans_tc.cu"]
+SOURCES = ["api.cu", "k_retrieve.cu", "k_append.cu", "k_attn.cu", "k_attn_tc.cu", "k_layer.cu", "k_kmeans.cu", "k_kmeans_tc.cu"]
 
 
 def _stale(target, deps):

@@ -575,6 +575,11 @@ louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_
   if (c->stage[layer] != 3) return fail(c, LOUISKV_ERR_STATE, "sparse_attn must follow append_output");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   AttnArgs a = attn_args(c, layer, q_own, stride_b, out, out_f32);
+  if (is_full(c, layer) && c->cfg.attn_impl != LOUISKV_ATTN_SIMT) {
+    const cudaError_t e = launch_attn_full_tc(a, c->inst_per_layer, st);
+    if (e == cudaSuccess) return LOUISKV_OK;
+    if (e != cudaErrorNotSupported) return cuda_fail(c, e, "attn (tensor cores)");
+  }
   LKV_LAUNCH(c, launch_attn(a, st), "attn");
   return LOUISKV_OK;
 }
@@ -608,7 +613,8 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
   if (layer < 0 || layer >= c->L || !q_all || !k_t || !v_t || !out)
     return fail(c, LOUISKV_ERR_INVALID_ARG, "decode_layer: bad args");
   const void* q_own = reinterpret_cast<const bf16*>(q_all) + (int64_t)c->h0 * c->g * D;
-  if (is_full(c, layer)) {  // full-cache layer: the step kernel + the attention
+  if (is_full(c, layer) || c->Umax > LAYER_REP_UNITS || std::min(c->Umax, c->Bud) > LAYER_REP_SEL) {
+    // full-cache layer (step kernel + attention), or an instance too large for the single launch
     louiskv_status s = louiskv_should_retrieve(c, layer, q_all, stride_q, d_flag_out, d_r_out, stream);
     if (s == LOUISKV_OK) s = louiskv_retrieve(c, layer, q_own, stride_q, stream);
     if (s == LOUISKV_OK) s = louiskv_append_attn(c, layer, k_t, v_t, stride_kv, q_own, stride_q, out, out_f32, stream);

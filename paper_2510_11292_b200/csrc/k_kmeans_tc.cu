@@ -374,6 +374,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return get_encode(); }
+
 bool kmeans_tc_available() {
   static int avail = -1;
   if (avail < 0) {

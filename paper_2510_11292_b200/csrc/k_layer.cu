@@ -21,7 +21,6 @@
 
 namespace lkv {
 
-constexpr int LK_MCAP = LAYER_UNITS_MAX / AT_CL;  // units per rank held in shared memory
 constexpr int LK_W = AT_THREADS / 32;
 
 // block-wide exclusive scan (AT_THREADS threads)
@@ -55,340 +54,12 @@ __device__ __forceinline__ int lk_scan(int v, int* s_warp, int& total) {
 
 __device__ __forceinline__ int clamp16(int sz) { return sz > 0xFFFF ? 0xFFFF : sz; }
 
-// Distributed group-consistent scoring + budgeted greedy + working-set layout of instance li.
-// Returns the row count of the new working set (identical on every rank); the row table of the
-// gather is complete in global memory after the caller's next cluster barrier.
-// SMB: this rank's logits / keys / sizes / taken bits live in the (idle) attention staging smem;
-// else (more than LK_MCAP units per rank) in the instance's global scratch.
-template <int G, bool SMB>
-__device__ __forceinline__ int lk_select(const RetrieveArgs& a, const AppendArgs& app, const int li, const int rank,
-                                         const int n, const int ws_cur, const float (*sq)[D], uint8_t* dsm) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = (n + AT_CL - 1) / AT_CL;
-  const int lo = min(n, rank * m), hi = min(n, lo + m), cnt = hi - lo;
-  const int ES = SMB ? LK_MCAP : m;  // row stride of E
-  float* E;                           // [G][ES]
-  unsigned long long* KEYS;           // [ES]
-  uint16_t* SZ;                       // [ES]
-  uint32_t* TK;                       // [ceil(ES/32)]
-  if constexpr (SMB) {
-    E = reinterpret_cast<float*>(dsm);
-    KEYS = reinterpret_cast<unsigned long long*>(E + G * LK_MCAP);
-    SZ = reinterpret_cast<uint16_t*>(KEYS + LK_MCAP);
-    TK = reinterpret_cast<uint32_t*>(SZ + LK_MCAP);
-  } else {  // 8 ranks x m <= Umax + 7 rounded: within [G][Umax] floats and Umax * 26 bytes per instance
-    E = a.scratch_e + (int64_t)li * G * a.Umax + (int64_t)rank * G * m;
-    uint8_t* base = a.scratch_sort + (int64_t)li * a.Umax * 26;
-    KEYS = reinterpret_cast<unsigned long long*>(base) + (int64_t)rank * m;
-    SZ = reinterpret_cast<uint16_t*>(base + (int64_t)a.Umax * 8) + (int64_t)rank * m;
-    TK = reinterpret_cast<uint32_t*>(base + (int64_t)a.Umax * 12) + (int64_t)rank * ((m + 31) / 32);
-  }
-
-  __shared__ float s_coef[7];
-  __shared__ float x_max[G];               // exchanged through DSMEM
-  __shared__ unsigned long long x_z[G];    // exchanged
-  __shared__ int x_hist[2][256];           // exchanged (double-buffered by pass parity)
-  __shared__ unsigned long long x_min[2];  // exchanged (double-buffered by take parity)
-  __shared__ int x_tot;                    // exchanged
-  __shared__ float s_red[LK_W][G];
-  __shared__ unsigned long long s_kmin[LK_W];
-  __shared__ float s_M[G], s_Z[G];
-  __shared__ int s_gh[256];
-  __shared__ unsigned long long s_prefix, s_kt;
-  __shared__ int s_need, s_all, s_off, s_total;
-  __shared__ int s_warp[LK_W + 1];
-
-  if (tid < 7) s_coef[tid] = a.r3c[tid];
-  for (int i = tid; i < (ES + 31) / 32; i += AT_THREADS) TK[i] = 0u;
-  if (tid < G) x_z[tid] = 0ull;
-
-  // ---- logits (R2) of this rank's units, local max per head
-  const bf16* centb = a.centb + (int64_t)li * a.Umax * D;
-  float mymax[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
-  for (int i = tid; i < cnt; i += AT_THREADS) {
-    float l[G];
-    logits_row<G>(sq, reinterpret_cast<const uint4*>(centb + (int64_t)(lo + i) * D), a.inv_sqrt_d, l);
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      E[j * ES + i] = l[j];
-      mymax[j] = fmaxf(mymax[j], l[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    float v = mymax[j];
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) s_red[warp][j] = v;
-  }
-  __syncthreads();
-  if (tid < G) {
-    float v = -INFINITY;
-    for (int w = 0; w < LK_W; ++w) v = fmaxf(v, s_red[w][tid]);
-    x_max[tid] = v;
-  }
-  cl.sync();
-  if (tid < G) {
-    float v = -INFINITY;
-    for (int r = 0; r < AT_CL; ++r) v = fmaxf(v, *cl.map_shared_rank(&x_max[tid], r));
-    s_M[tid] = v;
-  }
-  __syncthreads();
-
-  // ---- exp (R3) + exact fixed-point normaliser, summed over the cluster
-  unsigned long long zl[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) zl[j] = 0ull;
-  for (int i = tid; i < cnt; i += AT_THREADS) {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float e = exp_r3(__fsub_rn(E[j * ES + i], s_M[j]), s_coef);
-      E[j * ES + i] = e;
-      zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    unsigned long long z = zl[j];
-    for (int o = 16; o; o >>= 1) z += shfl_xor_u64(z, o);
-    if (lane == 0 && z) atomicAdd(&x_z[j], z);
-  }
-  cl.sync();
-  if (tid < G) {
-    unsigned long long z = 0ull;
-    for (int r = 0; r < AT_CL; ++r) z += *cl.map_shared_rank(&x_z[tid], r);
-    s_Z[tid] = __fmul_rn(__ull2float_rn(z), __int_as_float((127 - 40) << 23));
-  }
-  __syncthreads();
-
-  // ---- A_u and keys (A desc, id asc); sizes clamped to 16 bits (B <= 65534: a clamped unit never fits)
-  const int32_t* usize = a.usize + (int64_t)li * a.Umax;
-  for (int i = tid; i < cnt; i += AT_THREADS) {
-    float A = 0.0f;
-#pragma unroll
-    for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[j * ES + i], s_Z[j]));
-    A = __fdiv_rn(A, (float)G);
-    KEYS[i] = ((unsigned long long)(~__float_as_uint(A)) << 16) | (unsigned)(lo + i);
-    SZ[i] = (uint16_t)clamp16(usize[lo + i]);
-  }
-  if (tid == 0) {
-    s_prefix = 0ull;
-    s_need = a.budget;
-    s_all = 0;
-  }
-
-  // ---- first-skip pivot: size-weighted radix select over the cluster (6 passes of 8-bit digits)
-  for (int pass = 0; pass < 6; ++pass) {
-    const int shift = 40 - 8 * pass;
-    const unsigned long long hi_mask = (pass == 0) ? 0ull : (~0ull << (shift + 8)) & 0xFFFFFFFFFFFFull;
-    int* H = x_hist[pass & 1];
-    H[tid] = 0;  // AT_THREADS == 256 bins
-    __syncthreads();
-    const unsigned long long prefix = s_prefix;
-    for (int i0 = warp * 32; i0 < cnt; i0 += AT_THREADS) {
-      const int i = i0 + lane;
-      int bk = -1, sz = 0;
-      if (i < cnt) {
-        const unsigned long long k = KEYS[i];
-        if ((k & hi_mask) == prefix) {
-          bk = (int)((k >> shift) & 255);
-          sz = SZ[i];
-        }
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, bk);
-      const unsigned sum = __reduce_add_sync(peers, (unsigned)sz);
-      if (bk >= 0 && lane == __ffs(peers) - 1) atomicAdd(&H[bk], (int)sum);
-    }
-    cl.sync();
-    {
-      int gsum = 0;
-#pragma unroll
-      for (int r = 0; r < AT_CL; ++r) gsum += *cl.map_shared_rank(&H[tid], r);
-      s_gh[tid] = gsum;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      int v[8], ls = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = s_gh[lane * 8 + i];
-        ls += v[i];
-      }
-      int incl = ls;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - ls;
-      const int need = s_need;
-      const unsigned hit = __ballot_sync(0xffffffffu, incl > need);
-      if (hit == 0u) {
-        if (lane == 0) s_all = 1;  // (pass 0 sees everything) the whole set fits the budget
-      } else {
-        const int first = __ffs(hit) - 1;
-        if (lane == first) {
-          int cum = excl, bk = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (cum + v[i] > need) {
-              bk = i;
-              break;
-            }
-            cum += v[i];
-          }
-          s_need = need - cum;
-          s_prefix = prefix | ((unsigned long long)(lane * 8 + bk) << shift);
-        }
-      }
-    }
-    __syncthreads();
-    if (s_all) break;
-  }
-  const bool all = s_all != 0;
-  const unsigned long long pivot = all ? ~0ull : s_prefix;
-  const int per = (cnt + AT_THREADS - 1) / AT_THREADS;
-  const int u0 = tid * per, u1 = min(cnt, u0 + per);
-  for (int i = u0; i < u1; ++i)
-    if (KEYS[i] < pivot) atomicOr(&TK[i >> 5], 1u << (i & 31));
-  // ---- tail: the greedy's next take = the smallest key after the last take among units that still
-  // fit; one cluster-wide min per take
-  {
-    int rem = all ? 0 : s_need;
-    unsigned long long last = pivot;
-    int it = 0;
-    while (rem > 0) {
-      unsigned long long best = ~0ull;
-      for (int i = u0; i < u1; ++i) {
-        const unsigned long long k = KEYS[i];
-        if (k > last && k < best && SZ[i] <= rem) best = k;
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const unsigned long long y = shfl_xor_u64(best, o);
-        best = y < best ? y : best;
-      }
-      if (lane == 0) s_kmin[warp] = best;
-      __syncthreads();
-      if (tid == 0) {
-        unsigned long long v = ~0ull;
-        for (int w = 0; w < LK_W; ++w) v = s_kmin[w] < v ? s_kmin[w] : v;
-        x_min[it & 1] = v;
-      }
-      cl.sync();
-      if (tid == 0) {
-        unsigned long long v = ~0ull;
-        for (int r = 0; r < AT_CL; ++r) {
-          const unsigned long long y = *cl.map_shared_rank(&x_min[it & 1], r);
-          v = y < v ? y : v;
-        }
-        s_kt = v;
-      }
-      __syncthreads();
-      const unsigned long long kt = s_kt;
-      if (kt == ~0ull) break;  // nothing else fits
-      const int ut = (int)(kt & 0xFFFFull);
-      rem -= clamp16(usize[ut]);
-      last = kt;
-      if (tid == 0 && ut >= lo && ut < hi) atomicOr(&TK[(ut - lo) >> 5], 1u << ((ut - lo) & 31));
-      ++it;
-    }
-  }
-  __syncthreads();
-
-  // ---- layout (selected units in id order): rank offset = rows of the lower ranks
-  int local = 0, local_cnt = 0;
-  for (int i = u0; i < u1; ++i)
-    if (TK[i >> 5] >> (i & 31) & 1u) {
-      local += SZ[i];
-      ++local_cnt;
-    }
-  int rank_total;
-  int dst = lk_scan(local, s_warp, rank_total);
-  if (tid == 0) x_tot = rank_total;
-  cl.sync();
-  if (tid == 0) {
-    int off = 0, tot = 0;
-    for (int r = 0; r < AT_CL; ++r) {
-      const int v = *cl.map_shared_rank(&x_tot, r);
-      if (r < rank) off += v;
-      tot += v;
-    }
-    s_off = off;
-    s_total = tot;
-  }
-  __syncthreads();
-  dst += s_off;
-  const int total = s_total;
-
-  const int nxt = ws_cur ^ 1;
-  const int64_t gi = a.inst_global_base + li;
-  const bf16* curK = a.ws + ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride;
-  const bf16* curV = curK + (int64_t)a.budget * D;
-  const uint8_t* pool = a.pool + (int64_t)li * a.pool_inst_bytes;
-  uint8_t* sel = a.sel + (int64_t)li * a.Umax;
-  int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
-  const int64_t* uoff = a.uoff + (int64_t)li * a.Umax;
-  RowSrc* rows = a.rows + (int64_t)li * app.budget;
-  unsigned long long reused = 0, fetched = 0, hbytes = 0;
-  for (int i = u0; i < u1; ++i) {
-    const int u = lo + i;
-    const bool take = TK[i >> 5] >> (i & 31) & 1u;
-    const bool had = sel[u] != 0;
-    if (take) {
-      const int sz = SZ[i];
-      if (had) {
-        const int so = seloff[u];
-        for (int k = 0; k < sz; ++k)
-          rows[dst + k] = RowSrc{reinterpret_cast<const uint4*>(curK + (int64_t)(so + k) * D),
-                                 reinterpret_cast<const uint4*>(curV + (int64_t)(so + k) * D)};
-        ++reused;
-      } else {
-        const uint8_t* base = pool + uoff[u] * POOL_ROW_BYTES;
-        for (int k = 0; k < sz; ++k)
-          rows[dst + k] = RowSrc{reinterpret_cast<const uint4*>(base + (int64_t)k * ROW_BYTES),
-                                 reinterpret_cast<const uint4*>(base + (int64_t)(sz + k) * ROW_BYTES)};
-        ++fetched;
-        hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
-      }
-      sel[u] = 1;
-      seloff[u] = dst;
-      dst += sz;
-    } else if (had) {
-      sel[u] = 0;
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    reused += __shfl_xor_sync(0xffffffffu, reused, o);
-    fetched += __shfl_xor_sync(0xffffffffu, fetched, o);
-    hbytes += __shfl_xor_sync(0xffffffffu, hbytes, o);
-    local_cnt += __shfl_xor_sync(0xffffffffu, local_cnt, o);
-  }
-  if (lane == 0 && (reused | fetched)) {
-    atomicAdd(&a.stats->units_reused, reused);
-    atomicAdd(&a.stats->units_fetched, fetched);
-    atomicAdd(&a.stats->bytes_h2d, hbytes);
-    atomicAdd(&a.stats->units_selected, (unsigned long long)local_cnt);
-  }
-  if (rank == 0 && tid == 0) {
-    atomicAdd(&a.stats->units_scored, (unsigned long long)n);
-    if (li % a.hn == 0) atomicAdd(&a.stats->retrievals, 1ull);
-    InstState* S = a.inst + li;
-    S->ws_cur = nxt;
-    S->ws_rows = total;
-  }
-  return total;
-}
-
 // ---------------------------------------------------------------- replicated select (n <= LK_REP_N)
 // Every rank scores its 1/8 of the units, pushes its A bits to all ranks (DSMEM stores), and then
 // runs the whole greedy selection locally on the replicated keys: three cluster barriers in total
 // (max, normaliser, keys) and every rank knows the complete new layout.
-constexpr int LK_REP_N = 8192;    // units per instance
-constexpr int LK_REP_SEL = 1024;  // selected units (<= min(n, B))
+constexpr int LK_REP_N = LAYER_REP_UNITS;  // units per instance
+constexpr int LK_REP_SEL = LAYER_REP_SEL;  // selected units (<= min(n, B))
 // shared-memory regions of the replicated select (bytes, by n): RA [0, 4n) | SZ [4n, 6n) | TK bits |
 // X (the rest of the idle attention staging area): own logits E, then the radix candidate lists,
 // then the tail candidates, then the selected-unit LIST
@@ -1132,29 +803,20 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) layer_kernel(Layer
       __syncthreads();
     }
     bf16* nxtK = a.ws + (ws_cur ^ 1) * a.ws_buf_stride + gi * a.ws_inst_stride;
-    rep = n <= LK_REP_N && min(n, a.budget) <= LK_REP_SEL;
-    if (rep) {
-      int nsel;
-      total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, s_own_dst, prof);
-      prof_stamp(prof, 4);
+    // (the host launches this kernel only when every instance fits the replicated select:
+    // Umax <= LK_REP_N and min(Umax, B) <= LK_REP_SEL; else the multi-kernel sequence)
+    rep = true;
+    int nsel;
+    total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, s_own_dst, prof);
+    prof_stamp(prof, 4);
 #ifdef LKV_PROF
-      if (prof && tid == 0) prof[23] = clock64();
+    if (prof && tid == 0) prof[23] = clock64();
 #endif
-      const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
-      lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_off_x(n)), nsel, R0, R1,
-                     reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
-      ws_k = nxtK + (int64_t)R0 * D;
-      ws_n = R1 - R0;
-    } else {
-      total = n <= AT_CL * LK_MCAP ? lk_select<G, true>(a, app, li, rank, n, ws_cur, sq, lk_smem)
-                                   : lk_select<G, false>(a, app, li, rank, n, ws_cur, sq, lk_smem);
-      prof_stamp(prof, 4);
-      cg::this_cluster().sync();  // row table complete (cluster-scope release/acquire)
-      const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
-      if (R0 < R1) gather_rows(app, li, GatherJob{total, 0, nxtK, nxtK + (int64_t)a.budget * D}, R0, R1);
-      ws_k = nxtK + (int64_t)R0 * D;
-      ws_n = R1 - R0;
-    }
+    const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
+    lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_off_x(n)), nsel, R0, R1,
+                   reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
+    ws_k = nxtK + (int64_t)R0 * D;
+    ws_n = R1 - R0;
   } else {
     const int wr = s_S.ws_rows;
     const int R0 = wr * rank / AT_CL, R1 = wr * (rank + 1) / AT_CL;
@@ -1266,7 +928,6 @@ static cudaError_t launch_layer_g(const LayerArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(layer_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
     attr = true;
   }
-  static_assert(G * LK_MCAP * 4 + LK_MCAP * 10 + LK_MCAP / 8 <= AT_STAGES * AT_STAGE_BYTES, "select smem");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.r.batch * a.r.hn * AT_CL);
   cfg.blockDim = dim3(AT_THREADS);
@@ -1285,7 +946,7 @@ static cudaError_t launch_layer_g(const LayerArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st) {
-  if (a.r.Hq > 64) return cudaErrorInvalidValue;
+  if (a.r.Hq > 64 || a.r.Umax > LK_REP_N || min(a.r.Umax, a.r.budget) > LK_REP_SEL) return cudaErrorInvalidValue;
   switch (a.r.g) {
     case 1: return launch_layer_g<1>(a, st);
     case 2: return launch_layer_g<2>(a, st);

@@ -159,6 +159,8 @@ struct AttnArgs {
   AppendArgs app;
 };
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
+// full-cache layers on tensor cores (k_attn_tc.cu); cudaErrorNotSupported -> use launch_attn
+cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_t st);
 
 // one decode step of one retrieval layer in ONE clustered launch (k_layer.cu): trigger (R1),
 // distributed score + select (R2/R3, greedy), gather, append, attention. r.q_own = q_all.
@@ -168,7 +170,10 @@ struct LayerArgs {
   int layer;    // (LKV_PROF builds: timestamp rows of this layer)
 };
 constexpr int PROF_SLOTS = 24;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
-constexpr int LAYER_UNITS_MAX = 8 * 2048;  // units per instance the single launch keeps on chip (else global scratch)
+// the single launch handles instances with at most LAYER_REP_UNITS units and at most LAYER_REP_SEL
+// selectable units (min(Umax, B)); larger contexts run the multi-kernel sequence
+constexpr int LAYER_REP_UNITS = 8192;
+constexpr int LAYER_REP_SEL = 1024;
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st);
 
 // k-means / prompt (k_kmeans.cu)

@@ -31,7 +31,8 @@ def small_cfg(**kw):
 
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
-                check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False):
+                check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False,
+                attn_impl=0):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
     fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
     "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
@@ -40,7 +41,8 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     h0 = kv_head_begin
     g = cfg.group
     ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
-                                      boundary_mode=boundary_mode, max_open_segment=max_open or 0))
+                                      boundary_mode=boundary_mode, max_open_segment=max_open or 0,
+                                      attn_impl=attn_impl))
     ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
                        kv_head_begin=h0, kv_head_count=hn)
     L, b = cfg.num_layers, cfg.batch
@@ -141,6 +143,14 @@ def test_episode_oracle_clustering_small(seed, fused):
     inp = make_inputs(cfg, cfg.decode_steps, seed)
     worst, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused)
     assert n_flags > 5 and st["segments_evicted"] > 0 and st["units_reused"] > 0
+
+
+def test_episode_simt_full_cache_attention():
+    """The CUDA-core full-cache attention (attn_impl=SIMT) stays parity-green next to the default
+    tensor-core kernel (full-cache layer 0 of the small config, prompt + 40 decode rows)."""
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, 11)
+    run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: planted_assign(cfg, inp.labels[l]), attn_impl=1)
 
 
 def test_episode_c1_shape():

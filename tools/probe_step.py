@@ -17,6 +17,7 @@ ap.add_argument("--steps", type=int, default=64)
 ap.add_argument("--taus", default="-2,2,default")
 ap.add_argument("--unfused", action="store_true")
 ap.add_argument("--layer", action="store_true", help="louiskv_decode_layer per layer")
+ap.add_argument("--attn-impl", type=int, default=0, help="full-cache attention: 0 tensor cores, 1 SIMT")
 args = ap.parse_args()
 base = CONFIGS[args.config]
 dev = torch.device("cuda", 0)
@@ -25,7 +26,7 @@ for tau_s in args.taus.split(","):
     cfg = base if tau_s == "default" else base.replace(tau=float(tau_s))
     L, full = cfg.num_layers, set(cfg.full_cache_layers)
     T = 2 + 8 + 2 * args.steps
-    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=T + 1))
+    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=T + 1, attn_impl=args.attn_impl))
     plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
     for l in range(L):
         K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])

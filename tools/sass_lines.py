@@ -33,6 +33,8 @@ stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issu
 why = collections.defaultdict(collections.Counter)
 tot = 0
 for r in rows[2:]:
+    if len(r) <= si or not r[ai].startswith("0x"):
+        break  # (next kernel's block)
     off = int(r[ai], 16) - base
     s = int(r[si] or 0)
     tot += s
