@@ -24,12 +24,14 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, prof: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, prof: bool = False, variant: str = "", defines=()) -> str:
     """prof=True: a separate liblouiskv_prof.so with per-phase %globaltimer stamps (-DLKV_PROF) for
-    tools/probe_phases.py; never loaded by the tests or the bench."""
-    objdir = os.path.join(HERE, "build_prof" if prof else "build")
-    lib = LIB.replace(".so", "_prof.so") if prof else LIB
-    flags = FLAGS + (["-DLKV_PROF"] if prof else [])
+    tools/probe_phases.py; variant/defines: an experimental liblouiskv_<variant>.so. Neither is ever
+    loaded by the tests or the bench."""
+    tag = "prof" if prof else variant
+    objdir = os.path.join(HERE, "build_" + tag if tag else "build")
+    lib = LIB.replace(".so", "_" + tag + ".so") if tag else LIB
+    flags = FLAGS + (["-DLKV_PROF"] if prof else []) + ["-D" + d for d in defines]
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
     headers.append(os.path.join(INCLUDE, "louiskv.h"))
@@ -54,4 +56,7 @@ def build(verbose: bool = False, force: bool = False, prof: bool = False) -> str
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, prof="--prof" in sys.argv))
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, prof="--prof" in sys.argv,
+                variant=var[0] if var else "", defines=defs))

@@ -588,8 +588,11 @@ __device__ __forceinline__ void lk_gather_list(const SelEnt* LIST, const int nse
 __device__ unsigned long long g_lkv_prof[64][2048][PROF_SLOTS];
 #endif
 
+#ifndef LKV_LAYER_MINB
+#define LKV_LAYER_MINB 1
+#endif
 template <int G>
-__global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) layer_kernel(LayerArgs A) {
+__global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer_kernel(LayerArgs A) {
   namespace cg = cooperative_groups;
 #ifdef LKV_PROF
   unsigned long long* prof = (A.layer < 64 && blockIdx.x < 2048) ? g_lkv_prof[A.layer][blockIdx.x] : nullptr;
