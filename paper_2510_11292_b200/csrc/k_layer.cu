@@ -17,6 +17,7 @@
 // same sequence of cluster barriers (all branches depend only on cluster-uniform values).
 #include "lkv_append_dev.cuh"
 #include "lkv_attn_dev.cuh"
+#include "lkv_attn_mma_dev.cuh"
 #include "lkv_score_dev.cuh"
 
 namespace lkv {
@@ -629,6 +630,9 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   const uint4* qc4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b);
   const uint4* qr4[2] = {reinterpret_cast<const uint4*>(a.qref + ((int64_t)0 * a.Bmax + b) * a.Hq * D),
                          reinterpret_cast<const uint4*>(a.qref + ((int64_t)1 * a.Bmax + b) * a.Hq * D)};
+  // the owned heads' q as the attention MMA's A fragments (used at the end; loaded now)
+  uint32_t qa[8][2];
+  mma_q_frags<G>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)(a.h0 + h) * G * D, qa);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0, r00 = c0, r01 = c0, r10 = c0, r11 = c0;
   if (act) {
     c0 = qc4[hh * 16 + l8];
@@ -839,7 +843,6 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
                                                       (int64_t)h * D);
     reinterpret_cast<uint4*>((tid < 16 ? ringK : ringV) + (int64_t)slot * D)[tid & 15] = src[tid & 15];
   }
-  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes (gather, token) -> TMA reads
   Pieces P;
   P.np = 0;
   {
@@ -858,8 +861,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   int rows = 0;
   for (int p = 0; p < P.np; ++p) rows += P.n[p];
   prof_stamp(prof, 7);
-  const uint16_t* qown = qc + (int64_t)(a.h0 + h) * G * D;
-  const float* part = attn_partial<G>(qown, at.scale_log2, P, 0, rows, prof);
+  const float* part = attn_partial_mma<G>(qa, at.scale_log2, P, rows, prof);
 
   // ---- 5. merge: every rank pushes its partial's dims [16 r, 16 r + 16) to rank r and its (max, sum)
   // to all ranks (DSMEM stores), one cluster barrier, each rank finalises 16 dims of every head

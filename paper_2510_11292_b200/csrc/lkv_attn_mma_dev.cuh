@@ -1,0 +1,207 @@
+// Tensor-core (mma.sync m16n8k16 bf16 -> fp32) CTA-level flash-decode partial over an attention set
+// given as row pieces — the attention step of the single-launch layer kernel (k_layer.cu).
+// o = softmax(q K_I^T / sqrt(d)) V_I (P:63-65 [§3.1]) for the g query heads of one KV head.
+//
+// 8 warps, 64-row chunks: warp w owns rows [8w, 8w+8) of every chunk. S^T = Q K^T with the g heads
+// as the MMA's M rows (padded to 16) and the warp's 8 rows as N, 8 k-steps over d = 128; scale into
+// the log2 domain in fp32, online softmax per head; P (bf16, rows 8-15 of the k extent zero) is the
+// A operand of O += P V over 16 n-tiles of 8 dims. The 3-stage smem ring (K | V, each two 64-dim
+// 128-B-swizzled halves, so ldmatrix is bank-conflict free) is filled by cp.async 16-B copies, which
+// gather the pieces (sinks, working set, local window) in any alignment.
+#pragma once
+#include "lkv_attn_dev.cuh"
+
+namespace lkv {
+namespace am {
+
+constexpr int WARPS = AT_THREADS / 32;  // 8
+constexpr int CHUNK = 64;
+constexpr int STAGES = AT_STAGES;        // 3
+constexpr int HALF = CHUNK * 128;        // one 64-dim half of K (or V) of a chunk: 8 KB
+constexpr int STAGE = 4 * HALF;          // 32 KB == AT_STAGE_BYTES
+static_assert(STAGE == AT_STAGE_BYTES, "stage size");
+
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (uint32_t)((c >> 3) * HALF + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D += A (16x16: regs {a_lo, 0, a_hi, 0} - rows 8-15 zero) * B (16x8: regs {b_lo, b_hi})
+__device__ __forceinline__ void mma16816(float* d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a_lo), "r"(0u), "r"(a_hi), "r"(0u), "r"(b_lo), "r"(b_hi));
+}
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+
+}  // namespace am
+
+// q of the G heads (bf16 [G][D] at qb) as the A fragments of the S^T MMA: row = head lane/4 (< G),
+// k = dims; rows 8-15 are the zero padding (not stored)
+template <int G>
+__device__ __forceinline__ void mma_q_frags(const uint16_t* qb, uint32_t (&qa)[8][2]) {
+  const int lane = threadIdx.x & 31, hq = lane >> 2;
+  const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qb);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int d0 = kk * 16 + (lane & 3) * 2;
+    qa[kk][0] = hq < G ? q32[(hq * D + d0) >> 1] : 0u;
+    qa[kk][1] = hq < G ? q32[(hq * D + d0 + 8) >> 1] : 0u;
+  }
+}
+
+// Returns the CTA partial in shared memory, [G][D+2] floats (unnormalised accumulator, then the
+// log2-domain max and the sum), exactly as attn_partial. Rows [0, rows) of the pieces; qa from
+// mma_q_frags. All threads.
+template <int G>
+__device__ __forceinline__ float* attn_partial_mma(const uint32_t (&qa)[8][2], const float scale_log2, const Pieces& P,
+                                                   const int rows, unsigned long long* prof) {
+  using namespace am;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(128) uint8_t at_smem[];  // (128-B aligned: the software swizzle is row-relative)
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(at_smem);
+  const int n_chunks = (rows + CHUNK - 1) / CHUNK;
+
+  auto load = [&](int c) {  // 2048 16-B pieces per chunk, 8 per thread; rows past the end zero-filled
+    const uint32_t dst = sbase + (c % STAGES) * STAGE;
+#pragma unroll 1
+    for (int k = 0; k < (2 * CHUNK * 16) / AT_THREADS; ++k) {
+      const int i = tid + k * AT_THREADS;
+      const int kv = i >> 10, r = (i >> 4) & (CHUNK - 1), j = i & 15;
+      const int vr = c * CHUNK + r;
+      const bf16* src = P.k[0];
+      int bytes = 0;
+      if (vr < rows) {
+        int p = 0;
+        while (p + 1 < P.np && vr >= P.v0[p + 1]) ++p;
+        src = (kv ? P.v[p] : P.k[p]) + (int64_t)(vr - P.v0[p]) * D + j * 8;
+        bytes = 16;
+      }
+      cp16(dst + kv * 2 * HALF + swz(r, j), src, bytes);
+    }
+  };
+  __syncthreads();  // rows this CTA just wrote (gather, new token) are read back by other threads
+#pragma unroll 1
+  for (int c = 0; c < STAGES - 1; ++c) {
+    if (c < n_chunks) load(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float m_run = -INFINITY, l_run = 0.f;
+  float acc[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  const int row8 = warp * 8;
+#pragma unroll 1
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + STAGES - 1 < n_chunks) load(c + STAGES - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+    __syncthreads();
+    if (c == 0) prof_stamp(prof, 8);
+    const uint32_t kb = sbase + (c % STAGES) * STAGE, vb = kb + 2 * HALF;
+    // ---- S^T (heads x the warp's 8 rows)
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(kb + swz(row8 + (lane & 7), 4 * k2 + (lane >> 3)), b0, b1, b2, b3);
+      mma16816(s, qa[2 * k2][0], qa[2 * k2][1], b0, b1);
+      mma16816(s, qa[2 * k2 + 1][0], qa[2 * k2 + 1][1], b2, b3);
+    }
+    // ---- online softmax of head lane/4 over rows 2(lane%4), +1
+    const int vr = c * CHUNK + row8 + (lane & 3) * 2;
+    float p0 = vr < rows ? s[0] * scale_log2 : -INFINITY;
+    float p1 = vr + 1 < rows ? s[1] * scale_log2 : -INFINITY;
+    float mx = fmaxf(p0, p1);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);
+    float corr = 1.f;
+    if (m_new == -INFINITY) {
+      p0 = p1 = 0.f;
+    } else {
+      corr = exp2f(m_run - m_new);
+      p0 = exp2f(p0 - m_new);
+      p1 = exp2f(p1 - m_new);
+      m_run = m_new;
+    }
+    l_run = l_run * corr + p0 + p1;
+    const uint32_t pa = (uint32_t)f2bf_rne(p0) | ((uint32_t)f2bf_rne(p1) << 16);
+    // ---- O += P V (k extent: the warp's 8 rows; the other 8 are zero)
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(vb + swz(row8 + (lane & 7), 4 * q4 + (lane >> 3)), b0, b1, b2, b3);
+      const uint32_t bb[4] = {b0, b1, b2, b3};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float* d = acc[4 * q4 + t];
+        d[0] *= corr;
+        d[1] *= corr;
+        mma16816(d, pa, 0u, bb[t], 0u);
+      }
+    }
+    __syncthreads();  // stage c % STAGES fully consumed before it is refilled
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  prof_stamp(prof, 9);
+
+  // ---- merge the 8 warps through shared memory (the ring is idle now)
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+  __syncthreads();
+  float* s_acc = reinterpret_cast<float*>(at_smem);  // [WARPS][G][D]
+  float* s_ml = s_acc + WARPS * G * D;                // [WARPS][G][2]
+  float* part = s_ml + WARPS * G * 2;                 // [G][D+2]
+  const int hq = lane >> 2;
+  if (hq < G) {
+#pragma unroll
+    for (int dt = 0; dt < 16; ++dt) {
+      const int d0 = dt * 8 + (lane & 3) * 2;
+      s_acc[(warp * G + hq) * D + d0] = acc[dt][0];
+      s_acc[(warp * G + hq) * D + d0 + 1] = acc[dt][1];
+    }
+    if ((lane & 3) == 0) {
+      s_ml[(warp * G + hq) * 2] = m_run;
+      s_ml[(warp * G + hq) * 2 + 1] = l_run;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < G * D; idx += AT_THREADS) {
+    const int j = idx / D, e = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, s_ml[(w * G + j) * 2]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        const float mw = s_ml[(w * G + j) * 2];
+        const float sc = mw == -INFINITY ? 0.f : exp2f(mw - M);
+        Lsum += s_ml[(w * G + j) * 2 + 1] * sc;
+        A += s_acc[(w * G + j) * D + e] * sc;
+      }
+    }
+    part[j * (D + 2) + e] = A;
+    if (e == 0) {
+      part[j * (D + 2) + D] = M;
+      part[j * (D + 2) + D + 1] = Lsum;
+    }
+  }
+  __syncthreads();
+  return part;
+}
+
+}  // namespace lkv
