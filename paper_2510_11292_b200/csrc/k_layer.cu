@@ -634,6 +634,10 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   uint32_t qa[8][2];
   mma_q_frags<G>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)(a.h0 + h) * G * D, qa);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0, r00 = c0, r01 = c0, r10 = c0, r11 = c0;
+  uint4 nv = c0;  // (last rank, threads < 32) the new token's K / V row pieces, for the attention
+  if (rank == AT_CL - 1 && tid < 32)
+    nv = reinterpret_cast<const uint4*>((tid < 16 ? A.at.app.k_t : A.at.app.v_t) + (int64_t)b * A.at.app.stride_b +
+                                        (int64_t)h * D)[tid & 15];
   if (act) {
     c0 = qc4[hh * 16 + l8];
     c1 = qc4[hh * 16 + l8 + 8];
@@ -666,6 +670,42 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   }
   const int t = s_S.step + 1, par = t & 1;
   const int cap = app.ring_cap;
+  const AttnArgs& at = A.at;
+  bf16* ringK = app.ring + (int64_t)li * 2 * cap * D;
+  bf16* ringV = ringK + (int64_t)cap * D;
+  const int64_t gi = a.inst_global_base + li;
+  // this rank's attention plan: 1/8 of sinks, working set and local window (the new token, the
+  // window's last row, taken from the input by the last rank)
+  auto make_plan = [&](AttnPlan& pl, const bf16* wsk, int ws_rows_r, int win_head, int win_n) {
+    pl.P.np = 0;
+    const int se = s_S.s_eff;
+    const int s0 = se * rank / AT_CL, s1 = se * (rank + 1) / AT_CL;
+    const bf16* sk = at.sinks + (int64_t)li * 2 * at.S * D;
+    pl.P.add(s1 - s0, sk + (int64_t)s0 * D, sk + (int64_t)at.S * D + (int64_t)s0 * D);
+    pl.P.add(ws_rows_r, wsk, wsk + (int64_t)a.budget * D);
+    const int w0 = win_n * rank / AT_CL, w1 = win_n * (rank + 1) / AT_CL;
+    const int hs = (win_head + w0) % cap;
+    const int first = min(w1 - w0, cap - hs);
+    pl.P.add(first, ringK + (int64_t)hs * D, ringV + (int64_t)hs * D);
+    pl.P.add(w1 - w0 - first, ringK, ringV);
+    pl.rows = (s1 - s0) + ws_rows_r + (w1 - w0);
+    pl.mask_lo = pl.mask_hi = 0;
+    pl.new_vr = (rank == AT_CL - 1 && w1 > w0) ? pl.rows - 1 : -1;
+    return w0;
+  };
+  // speculative (no retrieval) plan, issued now so the loads overlap the trigger: current working
+  // set, and the window before this step's evictions (a superset; evicted rows are masked later)
+  AttnPlan pl;
+  const int dec0 = s_S.step;
+  const int sup_head = s_S.buffered > 0 ? s_S.ring_head : dec0, sup_n = dec0 - sup_head + 1;
+  int ws_r0 = s_S.ws_rows * rank / AT_CL, ws_r1 = s_S.ws_rows * (rank + 1) / AT_CL;
+  const int sup_w0 = make_plan(pl, a.ws + s_S.ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride + (int64_t)ws_r0 * D,
+                               ws_r1 - ws_r0, sup_head, sup_n);
+  int npre = min((pl.rows + am::CHUNK - 1) / am::CHUNK, am::STAGES - 1);
+  for (int c = 0; c < npre; ++c) {
+    attn_load_chunk(pl, c, nv);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (tid >= 32 && tid < 64) {  // prefetch the sealed-segment FIFO head entries (evictions)
     const int k = tid - 32;
     if (k < s_S.fifo_count) s_fifo[k] = app.fifo[(int64_t)li * cap + (s_S.fifo_head + k) % cap];
@@ -794,21 +834,20 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     }
   }
 
-  // ---- 3. retrieve (flagged): select, then gather this rank's 1/8 of the new working set; the
-  // rank attends exactly the rows it gathered, so no barrier separates gather and attention
-  const int64_t gi = a.inst_global_base + li;
+  // ---- 3. retrieve (flagged): drain the speculative loads (the select uses the staging memory),
+  // select, gather this rank's 1/8 of the new working set — the rows it then attends itself, so no
+  // barrier separates gather and attention — and plan again
   const int n = s_S.n_units, ws_cur = s_S.ws_cur;
-  const bf16* ws_k;  // this rank's working-set rows
-  int ws_n;
   bool rep = false;
   int total = 0;
   if (flag) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (!fast_trig) {
       const uint16_t* qb = qc + (int64_t)(a.h0 + h) * G * D;
       for (int i = tid; i < G * D; i += AT_THREADS) sq[i / D][i % D] = bf2f(qb[i]);
-      __syncthreads();
     }
+    __syncthreads();
     bf16* nxtK = a.ws + (ws_cur ^ 1) * a.ws_buf_stride + gi * a.ws_inst_stride;
     // (the host launches this kernel only when every instance fits the replicated select:
     // Umax <= LK_REP_N and min(Umax, B) <= LK_REP_SEL; else the multi-kernel sequence)
@@ -822,46 +861,21 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
     lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_off_x(n)), nsel, R0, R1,
                    reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
-    ws_k = nxtK + (int64_t)R0 * D;
-    ws_n = R1 - R0;
+    make_plan(pl, nxtK + (int64_t)R0 * D, R1 - R0, s_post.ring_head, s_post.buffered);
+    npre = 0;
   } else {
-    const int wr = s_S.ws_rows;
-    const int R0 = wr * rank / AT_CL, R1 = wr * (rank + 1) / AT_CL;
-    ws_k = a.ws + ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride + (int64_t)R0 * D;
-    ws_n = R1 - R0;
+    // the post-store_cache window is a suffix of the speculative one: mask the evicted front rows
+    const int ex = s_post.ring_head - sup_head;  // rows evicted from the front of the superset
+    const int w1 = sup_n * (rank + 1) / AT_CL;
+    const int v_ring = pl.rows - (w1 - sup_w0);  // (the window rows come last in the plan)
+    pl.mask_lo = v_ring;
+    pl.mask_hi = v_ring + max(0, min(ex, w1) - sup_w0);
   }
   prof_stamp(prof, 5);
 
-  // ---- 4. attention over this rank's 1/8 of sinks, working set and post-append local window; the
-  // last rank owns the window's tail, i.e. the new token, and writes its row itself first
-  const AttnArgs& at = A.at;
-  bf16* ringK = app.ring + (int64_t)li * 2 * cap * D;
-  bf16* ringV = ringK + (int64_t)cap * D;
-  if (rank == AT_CL - 1 && tid < 32) {
-    const int slot = s_S.step % cap;
-    const uint4* src = reinterpret_cast<const uint4*>((tid < 16 ? app.k_t : app.v_t) + (int64_t)b * app.stride_b +
-                                                      (int64_t)h * D);
-    reinterpret_cast<uint4*>((tid < 16 ? ringK : ringV) + (int64_t)slot * D)[tid & 15] = src[tid & 15];
-  }
-  Pieces P;
-  P.np = 0;
-  {
-    const int se = s_S.s_eff;
-    const int s0 = se * rank / AT_CL, s1 = se * (rank + 1) / AT_CL;
-    const bf16* sk = at.sinks + (int64_t)li * 2 * at.S * D;
-    P.add(s1 - s0, sk + (int64_t)s0 * D, sk + (int64_t)at.S * D + (int64_t)s0 * D);
-    P.add(ws_n, ws_k, ws_k + (int64_t)a.budget * D);
-    const int nb = s_post.buffered;
-    const int w0 = nb * rank / AT_CL, w1 = nb * (rank + 1) / AT_CL;
-    const int hs = (s_post.ring_head + w0) % cap;
-    const int first = min(w1 - w0, cap - hs);
-    P.add(first, ringK + (int64_t)hs * D, ringV + (int64_t)hs * D);
-    P.add(w1 - w0 - first, ringK, ringV);
-  }
-  int rows = 0;
-  for (int p = 0; p < P.np; ++p) rows += P.n[p];
+  // ---- 4. attention (tensor cores) over this rank's plan
   prof_stamp(prof, 7);
-  const float* part = attn_partial_mma<G>(qa, at.scale_log2, P, rows, prof);
+  const float* part = attn_run_mma<G>(qa, at.scale_log2, pl, npre, nv, prof);
 
   // ---- 5. merge: every rank pushes its partial's dims [16 r, 16 r + 16) to rank r and its (max, sum)
   // to all ranks (DSMEM stores), one cluster barrier, each rank finalises 16 dims of every head

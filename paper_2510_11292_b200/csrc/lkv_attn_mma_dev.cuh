@@ -62,40 +62,75 @@ __device__ __forceinline__ void mma_q_frags(const uint16_t* qb, uint32_t (&qa)[8
   }
 }
 
+// An attention set as row pieces plus: an excluded virtual-row range [mask_lo, mask_hi) (rows loaded
+// speculatively but not in the set) and one row (`new_vr`, -1: none) supplied from registers instead
+// of memory — the current token, before its ring slot is written.
+struct AttnPlan {
+  Pieces P;
+  int rows;
+  int mask_lo, mask_hi;
+  int new_vr;
+};
+
+// Issue chunk c of the plan into stage c % STAGES as cp.async 16-B copies: thread t copies 16-B piece
+// t % 16 of rows t/16 + 16m (m < 4), K and V (rows past the end zero-filled). The new-token row is
+// not copied: threads t < 32 of the owning CTA store `nv` (K piece t for t < 16, V piece t - 16) —
+// the row held in registers since entry. Every thread calls; the caller commits the group.
+__device__ __forceinline__ void attn_load_chunk(const AttnPlan& pl, const int c, const uint4 nv) {
+  using namespace am;
+  extern __shared__ __align__(128) uint8_t at_smem[];
+  const int tid = threadIdx.x, j = tid & 15;
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(at_smem) + (c % STAGES) * STAGE;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int r = (tid >> 4) + 16 * m;
+    const int vr = c * CHUNK + r;
+    if (vr == pl.new_vr) continue;
+    const bf16* ks = pl.P.k[0];
+    const bf16* vs = pl.P.k[0];
+    int bytes = 0;
+    if (vr < pl.rows) {
+      // piece lookup with the (at most 4) pieces kept in registers
+      int off = vr;
+      ks = pl.P.k[0];
+      vs = pl.P.v[0];
+#pragma unroll
+      for (int p = 1; p < AT_PMAX; ++p)
+        if (p < pl.P.np && vr >= pl.P.v0[p]) {
+          off = vr - pl.P.v0[p];
+          ks = pl.P.k[p];
+          vs = pl.P.v[p];
+        }
+      ks += (int64_t)off * D + j * 8;
+      vs += (int64_t)off * D + j * 8;
+      bytes = 16;
+    }
+    cp16(dst + swz(r, j), ks, bytes);
+    cp16(dst + 2 * HALF + swz(r, j), vs, bytes);
+  }
+  if (pl.new_vr >= c * CHUNK && pl.new_vr < (c + 1) * CHUNK && tid < 32) {
+    const uint32_t sdst = dst + (tid >> 4) * 2 * HALF + swz(pl.new_vr - c * CHUNK, j);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sdst), "r"(nv.x), "r"(nv.y), "r"(nv.z), "r"(nv.w)
+                 : "memory");
+  }
+}
+
 // Returns the CTA partial in shared memory, [G][D+2] floats (unnormalised accumulator, then the
-// log2-domain max and the sum), exactly as attn_partial. Rows [0, rows) of the pieces; qa from
-// mma_q_frags. All threads.
+// log2-domain max and the sum), exactly as attn_partial. The first `npre` chunks (< STAGES) were
+// issued and committed (one group each) by the caller. qa from mma_q_frags. All threads.
 template <int G>
-__device__ __forceinline__ float* attn_partial_mma(const uint32_t (&qa)[8][2], const float scale_log2, const Pieces& P,
-                                                   const int rows, unsigned long long* prof) {
+__device__ __forceinline__ float* attn_run_mma(const uint32_t (&qa)[8][2], const float scale_log2, const AttnPlan& pl,
+                                               const int npre, const uint4 nv, unsigned long long* prof) {
   using namespace am;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ __align__(128) uint8_t at_smem[];  // (128-B aligned: the software swizzle is row-relative)
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(at_smem);
+  const int rows = pl.rows;
   const int n_chunks = (rows + CHUNK - 1) / CHUNK;
-
-  auto load = [&](int c) {  // 2048 16-B pieces per chunk, 8 per thread; rows past the end zero-filled
-    const uint32_t dst = sbase + (c % STAGES) * STAGE;
+  __syncthreads();  // rows this CTA just wrote (gather) are read back by other threads
 #pragma unroll 1
-    for (int k = 0; k < (2 * CHUNK * 16) / AT_THREADS; ++k) {
-      const int i = tid + k * AT_THREADS;
-      const int kv = i >> 10, r = (i >> 4) & (CHUNK - 1), j = i & 15;
-      const int vr = c * CHUNK + r;
-      const bf16* src = P.k[0];
-      int bytes = 0;
-      if (vr < rows) {
-        int p = 0;
-        while (p + 1 < P.np && vr >= P.v0[p + 1]) ++p;
-        src = (kv ? P.v[p] : P.k[p]) + (int64_t)(vr - P.v0[p]) * D + j * 8;
-        bytes = 16;
-      }
-      cp16(dst + kv * 2 * HALF + swz(r, j), src, bytes);
-    }
-  };
-  __syncthreads();  // rows this CTA just wrote (gather, new token) are read back by other threads
-#pragma unroll 1
-  for (int c = 0; c < STAGES - 1; ++c) {
-    if (c < n_chunks) load(c);
+  for (int c = npre; c < STAGES - 1; ++c) {
+    if (c < n_chunks) attn_load_chunk(pl, c, nv);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   float m_run = -INFINITY, l_run = 0.f;
@@ -105,7 +140,7 @@ __device__ __forceinline__ float* attn_partial_mma(const uint32_t (&qa)[8][2], c
   const int row8 = warp * 8;
 #pragma unroll 1
   for (int c = 0; c < n_chunks; ++c) {
-    if (c + STAGES - 1 < n_chunks) load(c + STAGES - 1);
+    if (c + STAGES - 1 < n_chunks) attn_load_chunk(pl, c + STAGES - 1, nv);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
     __syncthreads();
@@ -122,8 +157,10 @@ __device__ __forceinline__ float* attn_partial_mma(const uint32_t (&qa)[8][2], c
     }
     // ---- online softmax of head lane/4 over rows 2(lane%4), +1
     const int vr = c * CHUNK + row8 + (lane & 3) * 2;
-    float p0 = vr < rows ? s[0] * scale_log2 : -INFINITY;
-    float p1 = vr + 1 < rows ? s[1] * scale_log2 : -INFINITY;
+    const bool ok0 = vr < rows && (vr < pl.mask_lo || vr >= pl.mask_hi);
+    const bool ok1 = vr + 1 < rows && (vr + 1 < pl.mask_lo || vr + 1 >= pl.mask_hi);
+    float p0 = ok0 ? s[0] * scale_log2 : -INFINITY;
+    float p1 = ok1 ? s[1] * scale_log2 : -INFINITY;
     float mx = fmaxf(p0, p1);
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
