@@ -107,11 +107,19 @@ void louiskv_destroy(louiskv_ctx* ctx);
  *   the device (fp32 + bf16), KV rows offloaded cluster-major to the host pool, sinks kept.
  * Full-cache layer: K, V copied to the device cache.
  * Must be called once per layer before the first decode step; resets that layer's decode
- * state. Errors: INVALID_ARG (layer, batch > max_batch, prompt_len > max_prompt_len,
- * batch differing from an earlier call), STATE. */
+ * state. Asynchronous: the KV offload runs on a library-owned copy stream (device staging ->
+ * pinned pool), overlapping later calls; every decode-path call on this layer makes its stream
+ * wait for it (inside a graph capture as an external event-wait node), and the introspection
+ * calls synchronise it. Errors: INVALID_ARG (layer, batch > max_batch,
+ * prompt_len > max_prompt_len, batch differing from an earlier call), STATE. */
 louiskv_status louiskv_cluster_prompt(louiskv_ctx* ctx, int32_t layer, const void* k, const void* v,
                                       int64_t stride_b, int64_t stride_t, int64_t stride_h,
                                       int32_t batch, int64_t prompt_len, void* stream);
+
+/* Makes `stream` wait for every prompt offload still in flight ("offload (K, V) to CPU
+ * memory pool asynchronously"): after it, the whole prefill of every layer is complete in
+ * stream order. Enqueues event waits only. Errors: INVALID_ARG, CUDA. */
+louiskv_status louiskv_prompt_fence(louiskv_ctx* ctx, void* stream);
 
 /* Same as cluster_prompt but with the clustering supplied by the caller (external or
  * reference clustering): h_assign host int32 [batch][kv_head_count][P-S] cluster ids in

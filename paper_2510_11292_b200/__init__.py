@@ -27,7 +27,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE"
            7: "NOT_IMPLEMENTED"}
 
 # ABI symbols declared in include/louiskv.h (checked by tests/test_abi.py)
-SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louiskv_set_prompt_units",
+SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louiskv_prompt_fence", "louiskv_set_prompt_units",
            "louiskv_should_retrieve", "louiskv_retrieve", "louiskv_append_output", "louiskv_sparse_attn",
            "louiskv_append_attn", "louiskv_decode_layer",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
@@ -77,6 +77,7 @@ def lib():
         L.louiskv_destroy.argtypes = [vp]
         L.louiskv_destroy.restype = None
         L.louiskv_cluster_prompt.argtypes = [vp, i32, vp, vp, i64, i64, i64, i32, i64, vp]
+        L.louiskv_prompt_fence.argtypes = [vp, vp]
         L.louiskv_set_prompt_units.argtypes = [vp, i32, vp, vp, i64, i64, i64, i32, i64, i32, vp, vp, vp]
         L.louiskv_should_retrieve.argtypes = [vp, i32, vp, i64, u8p, vp, vp]
         L.louiskv_retrieve.argtypes = [vp, i32, vp, i64, vp]
@@ -171,6 +172,10 @@ class Context:
         b, P = k.shape[0], k.shape[1]
         self._chk(self._L.louiskv_cluster_prompt(self.h, layer, _ptr(k), _ptr(v), k.stride(0), k.stride(1),
                                                  k.stride(2), b, P, _stream(stream)))
+
+    def prompt_fence(self, stream=None):
+        """Make `stream` wait for every pending prompt offload (copy-engine D2H into the pool)."""
+        self._chk(self._L.louiskv_prompt_fence(self.h, _stream(stream)))
 
     def set_prompt_units(self, layer, k, v, assign: np.ndarray, centroids: np.ndarray, stream=None):
         b, P = k.shape[0], k.shape[1]

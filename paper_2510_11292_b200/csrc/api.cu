@@ -70,6 +70,16 @@ struct louiskv_ctx {
   int* d_step = nullptr;   // [L] device decode-step counters (graph-replay safe)
   int* d_error = nullptr;  // device capacity-overflow flag
   uint64_t km_tc_iters = 0, km_simt_iters = 0;
+  // prompt offload: cluster-major rows are staged on the device (double buffer) and moved into the
+  // pinned pool by the copy engine on off_stream, overlapping the next layer's clustering
+  uint8_t* d_stage[2] = {nullptr, nullptr};
+  int64_t stage_bytes = 0;
+  int stage_next = 0;
+  bool stage_used[2] = {false, false};
+  cudaStream_t off_stream = nullptr;
+  cudaEvent_t ev_free[2] = {nullptr, nullptr}, ev_staged = nullptr;
+  std::vector<cudaEvent_t> ev_done;  // [L] offload of layer l complete
+  std::vector<char> off_pending;     // [L] a decode-path stream has not yet waited on ev_done[l]
   std::vector<void*> allocs;
   std::string err;
   bool sticky = false;
@@ -247,6 +257,11 @@ void louiskv_destroy(louiskv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
+  for (cudaEvent_t e : ctx->ev_done)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {ctx->ev_free[0], ctx->ev_free[1], ctx->ev_staged})
+    if (e) cudaEventDestroy(e);
+  if (ctx->off_stream) cudaStreamDestroy(ctx->off_stream);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->h_pool) cudaFreeHost(ctx->h_pool);
   delete ctx;
@@ -354,6 +369,23 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_stats, 1);
   ok = ok && dalloc(c, &c->d_step, (size_t)c->L);
   ok = ok && dalloc(c, &c->d_error, 1);
+  {
+    // staging for the prompt offload: whole layers up to 256 MiB per buffer, else instance chunks
+    const int64_t inst_b = std::max<int64_t>(c->Nmax, 1) * POOL_ROW_BYTES;
+    c->stage_bytes = std::max<int64_t>(inst_b, std::min<int64_t>(inst_b * nl, 256ll << 20));
+    if (c->n_r > 0 && c->Nmax > 0) {
+      ok = ok && dalloc(c, &c->d_stage[0], (size_t)c->stage_bytes);
+      ok = ok && dalloc(c, &c->d_stage[1], (size_t)c->stage_bytes);
+    }
+    ok = ok && cudaStreamCreateWithFlags(&c->off_stream, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_free[0], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming) == cudaSuccess;
+    c->ev_done.assign(c->L, nullptr);
+    c->off_pending.assign(c->L, 0);
+    for (int l = 0; l < c->L && ok; ++l)
+      ok = cudaEventCreateWithFlags(&c->ev_done[l], cudaEventDisableTiming) == cudaSuccess;
+  }
   if (!ok) {
     louiskv_destroy(c);
     return LOUISKV_ERR_OOM_DEVICE;
@@ -381,6 +413,52 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   }
   *out = c;
   return LOUISKV_OK;
+}
+
+// Prompt offload: stage the cluster-major K/V rows of a chunk of instances on the
+// device, then one strided copy-engine transfer into the pinned pool on off_stream. Two staging
+// buffers alternate, so the D2H of layer l overlaps the clustering of layer l+1; the decode-path
+// calls of layer l wait on ev_done[l] (offload_wait).
+static cudaError_t offload_prompt(louiskv_ctx* c, int layer, const KmArgs& a, cudaStream_t st) {
+  cudaError_t e;
+  const int ni = a.batch * a.hn;
+  if (a.N > 0 && a.kc > 0) {
+    const int64_t inst_b = (int64_t)a.N * POOL_ROW_BYTES;
+    const int per = (int)std::max<int64_t>(1, std::min<int64_t>(ni, c->stage_bytes / inst_b));
+    const int64_t ib = inst_base(c, layer);
+    for (int li0 = 0; li0 < ni; li0 += per) {
+      const int nli = std::min(per, ni - li0);
+      const int buf = c->stage_next;
+      c->stage_next ^= 1;
+      if (c->stage_used[buf] && (e = cudaStreamWaitEvent(st, c->ev_free[buf], 0)) != cudaSuccess) return e;
+      if ((e = launch_km_offload(a, li0, nli, c->d_stage[buf], inst_b, st)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(c->ev_staged, st)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(c->off_stream, c->ev_staged, 0)) != cudaSuccess) return e;
+      if ((e = cudaMemcpy2DAsync(c->h_pool + (ib + li0) * c->pool_inst_bytes, (size_t)c->pool_inst_bytes,
+                                 c->d_stage[buf], (size_t)inst_b, (size_t)inst_b, (size_t)nli,
+                                 cudaMemcpyDeviceToHost, c->off_stream)) != cudaSuccess)
+        return e;
+      if ((e = cudaEventRecord(c->ev_free[buf], c->off_stream)) != cudaSuccess) return e;
+      c->stage_used[buf] = true;
+    }
+    if ((e = launch_km_units(a, st)) != cudaSuccess) return e;
+  }
+  if ((e = cudaEventRecord(c->ev_done[layer], c->off_stream)) != cudaSuccess) return e;
+  c->off_pending[layer] = 1;
+  return cudaSuccess;
+}
+
+// Make `st` wait for the prompt offload of `layer` (once; inside a graph capture the wait becomes an
+// external event-wait node, which is free once the offload has completed).
+static cudaError_t offload_wait(louiskv_ctx* c, int layer, cudaStream_t st) {
+  if (!c->off_pending[layer]) return cudaSuccess;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs == cudaStreamCaptureStatusActive) return cudaStreamWaitEvent(st, c->ev_done[layer], cudaEventWaitExternal);
+  e = cudaStreamWaitEvent(st, c->ev_done[layer], 0);
+  if (e == cudaSuccess) c->off_pending[layer] = 0;
+  return e;
 }
 
 static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k, const void* v, int64_t sb,
@@ -476,6 +554,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
     a.ext_cent = d_ec;
   }
   cudaError_t e = run_kmeans_prompt(a, st, &c->km_tc_iters, &c->km_simt_iters);
+  if (e == cudaSuccess) e = offload_prompt(c, layer, a, st);
   if (h_assign) {
     cudaStreamSynchronize(st);
     cudaFree(d_ea);
@@ -509,6 +588,7 @@ louiskv_status louiskv_should_retrieve(louiskv_ctx* c, int32_t layer, const void
     return fail(c, LOUISKV_ERR_STATE, "should_retrieve: previous step incomplete");
   if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "should_retrieve: max_output_len reached");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   const int t = c->t[layer] + 1;
   if (is_full(c, layer)) {
     // full-cache layers never retrieve; the step counter advances in append_output
@@ -539,6 +619,7 @@ louiskv_status louiskv_retrieve(louiskv_ctx* c, int32_t layer, const void* q_own
   c->stage[layer] = 2;
   if (is_full(c, layer)) return LOUISKV_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   RetrieveArgs a = retrieve_args(c, layer, q_own, stride_b);
   a.budget = std::max(c->Bud, 0);
   LKV_LAUNCH(c, launch_select_gather(a, st), "select+gather");
@@ -552,6 +633,7 @@ louiskv_status louiskv_append_output(louiskv_ctx* c, int32_t layer, const void* 
   if (c->stage[layer] != 1 && c->stage[layer] != 2)
     return fail(c, LOUISKV_ERR_STATE, "append_output must follow should_retrieve/retrieve");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
 
   if (is_full(c, layer)) {
     LKV_LAUNCH(c,
@@ -574,6 +656,7 @@ louiskv_status louiskv_sparse_attn(louiskv_ctx* c, int32_t layer, const void* q_
   if (layer < 0 || layer >= c->L || !q_own || !out) return fail(c, LOUISKV_ERR_INVALID_ARG, "sparse_attn: bad args");
   if (c->stage[layer] != 3) return fail(c, LOUISKV_ERR_STATE, "sparse_attn must follow append_output");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   AttnArgs a = attn_args(c, layer, q_own, stride_b, out, out_f32);
   if (is_full(c, layer) && c->cfg.attn_impl != LOUISKV_ATTN_SIMT) {
     const cudaError_t e = launch_attn_full_tc(a, c->inst_per_layer, st);
@@ -598,6 +681,7 @@ louiskv_status louiskv_append_attn(louiskv_ctx* c, int32_t layer, const void* k_
   if (c->stage[layer] != 1 && c->stage[layer] != 2)
     return fail(c, LOUISKV_ERR_STATE, "append_attn must follow should_retrieve/retrieve");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   AttnArgs a = attn_args(c, layer, q_own, stride_q, out, out_f32);
   a.fused = 1;
   a.app = append_args(c, layer, k_t, v_t, stride_kv);
@@ -626,6 +710,7 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
   if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "decode_layer: max_output_len reached");
   const int t = c->t[layer] + 1;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   LayerArgs la{};
   la.r = retrieve_args(c, layer, q_all, stride_q);
   la.r.budget = std::max(c->Bud, 0);
@@ -649,7 +734,16 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
 }
 
 // ---------------------------------------------------------------- introspection
+louiskv_status louiskv_prompt_fence(louiskv_ctx* c, void* stream) {
+  LKV_CHECK_CTX(c);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int l = 0; l < c->L; ++l) LKV_LAUNCH(c, offload_wait(c, l, st), "prompt fence");
+  return LOUISKV_OK;
+}
+
 static louiskv_status inst_lookup(louiskv_ctx* c, int layer, int b, int h, int64_t* gi) {
+  if (c->off_stream && cudaStreamSynchronize(c->off_stream) != cudaSuccess)
+    return fail(c, LOUISKV_ERR_CUDA, "prompt offload failed");
   if (layer < 0 || layer >= c->L || b < 0 || b >= c->Bmax || h < 0 || h >= c->hn)
     return fail(c, LOUISKV_ERR_INVALID_ARG, "bad (layer, b, h)");
   if (is_full(c, layer)) return fail(c, LOUISKV_ERR_INVALID_ARG, "full-cache layer has no units");

@@ -613,9 +613,13 @@ __global__ void km_ext_kernel(KmArgs a) {
 }
 
 // offload: pool row r (cluster-major order) <- key perm[r]; unit-major spans [K rows | V rows]
-__global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a) {
+// Cluster-major permutation of instances [li0, li0 + gridDim.y) into dst (instance stride dst_stride
+// bytes): a device staging buffer whose rows the copy engine then moves into the pinned host pool
+// ("offload (K, V) to CPU memory pool asynchronously"), so the host-link transfer overlaps the
+// next layer's clustering instead of holding SMs.
+__global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a, int li0, uint8_t* dst_base, int64_t dst_stride) {
   pdl_wait_trigger();
-  const int li = blockIdx.y;
+  const int li = li0 + blockIdx.y;
   const int r = blockIdx.x * 8 + (threadIdx.x >> 4), sub = threadIdx.x & 15;
   if (r >= a.N) return;
   const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
@@ -623,10 +627,16 @@ __global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a) {
   const int i = perm[r];
   const int j = a.assign[(int64_t)li * a.Nmax + i];
   const int o = off[j], n = off[j + 1] - o;
-  uint4* dst = reinterpret_cast<uint4*>(a.pool + (int64_t)li * a.pool_inst_bytes + (int64_t)o * POOL_ROW_BYTES);
+  uint4* dst = reinterpret_cast<uint4*>(dst_base + (int64_t)blockIdx.y * dst_stride + (int64_t)o * POOL_ROW_BYTES);
   dst[(int64_t)(r - o) * 16 + sub] = reinterpret_cast<const uint4*>(xrow(a, li, i))[sub];
   dst[(int64_t)(n + r - o) * 16 + sub] = reinterpret_cast<const uint4*>(vrow(a, li, i))[sub];
   if (sub == 0) a.pool_pos[(int64_t)li * a.pool_rows_cap + r] = a.S + i;
+}
+
+cudaError_t launch_km_offload(const KmArgs& a, int li0, int nli, uint8_t* dst, int64_t dst_stride, cudaStream_t st) {
+  if (a.N <= 0 || a.kc <= 0 || nli <= 0) return cudaSuccess;
+  launch_k(km_offload_kernel, dim3(dim3((a.N + 7) / 8, nli)), dim3(128), 0, st, a, li0, dst, dst_stride);
+  return cudaGetLastError();
 }
 
 // unit table + instance reset after clustering
@@ -676,6 +686,12 @@ __global__ void reset_insts_kernel(InstState* inst, int n, int P, int s_eff) {
   s.prompt_len = P;
   s.s_eff = s_eff;
   inst[i] = s;
+}
+
+cudaError_t launch_km_units(const KmArgs& a, cudaStream_t st) {
+  if (a.N <= 0 || a.kc <= 0) return cudaSuccess;
+  launch_k(km_units_kernel, dim3(dim3((a.kc + 255) / 256, a.batch * a.hn)), dim3(256), 0, st, a, a.S + a.N);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st);  // k_kmeans_tc.cu
@@ -734,8 +750,8 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
       launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
     }
   }
-  launch_k(km_offload_kernel, dim3(dim3((a.N + 7) / 8, ni)), dim3(128), 0, st, a);
-  launch_k(km_units_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, P);
+  // the caller stages the cluster-major rows (launch_km_offload), copies them to the host pool and
+  // then writes the unit table (launch_km_units)
   return cudaGetLastError();
 }
 

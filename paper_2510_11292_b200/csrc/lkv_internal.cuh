@@ -221,6 +221,9 @@ struct KmArgs {
 };
 // tc_iters / simt_iters: host counters of which assignment kernel ran
 cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_iters, uint64_t* simt_iters);
+// cluster-major rows of instances [li0, li0+nli) -> dst (+ pool positions); then the unit table
+cudaError_t launch_km_offload(const KmArgs& a, int li0, int nli, uint8_t* dst, int64_t dst_stride, cudaStream_t st);
+cudaError_t launch_km_units(const KmArgs& a, cudaStream_t st);
 cudaError_t launch_full_prompt(const bf16* k, const bf16* v, int64_t sb, int64_t st_, int64_t sh, int batch, int hn,
                                int64_t P, bf16* full, int64_t full_cap, cudaStream_t st);
 cudaError_t launch_reset_insts(InstState* inst, int n, int P, int s_eff, cudaStream_t st);
