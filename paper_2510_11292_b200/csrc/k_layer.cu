@@ -79,6 +79,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// L2 prefetch of [p, p + bytes) widened to 16-B granules (the buffers are 256-B aligned allocations)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, int64_t bytes) {
+  const uint64_t a0 = reinterpret_cast<uint64_t>(p) & ~15ull;
+  const uint64_t a1 = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
+  if (a1 > a0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long rep_key(const uint32_t* RA, int u) {
   return ((unsigned long long)(~RA[u]) << 16) | (unsigned)u;
 }
@@ -127,18 +135,40 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   }
   prof_stamp(prof, 20);
 
-  // ---- logits (R2) of the own units, cluster max per head
+  // ---- logits (R2) of the own units, cluster max per head. The rank's centroid rows are staged in
+  // shared memory by coalesced cp.async (16 lanes per 256-B row; row pitch 272 B so that the
+  // one-row-per-thread reads below are bank-conflict free), RB rows per round.
   const bf16* centb = a.centb + (int64_t)li * a.Umax * D;
   float mymax[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
-  for (int i = tid; i < cnt; i += AT_THREADS) {
-    float l[G];
-    logits_row<G>(sq, reinterpret_cast<const uint4*>(centb + (int64_t)(lo + i) * D), a.inv_sqrt_d, l);
+  {
+    constexpr int PITCH = ROW_BYTES + 16;
+    const int e_bytes = (G * m * 4 + 127) & ~127;
+    uint8_t* CS = dsm + off_x + e_bytes;
+    const int RB = min(cnt, max(32, ((x_bytes - e_bytes) / PITCH) & ~31));
+    const uint32_t cs_s = (uint32_t)__cvta_generic_to_shared(CS);
+#pragma unroll 1
+    for (int b0 = 0; b0 < cnt; b0 += RB) {
+      const int nb = min(RB, cnt - b0);
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(centb + (int64_t)(lo + b0) * D);
+      for (int i = tid; i < nb * 16; i += AT_THREADS)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cs_s + (i >> 4) * PITCH + (i & 15) * 16),
+                     "l"(src + (int64_t)i * 16)
+                     : "memory");
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+      __syncthreads();
+#pragma unroll 1
+      for (int i = tid; i < nb; i += AT_THREADS) {
+        float l[G];
+        logits_row_smem<G>(sq, reinterpret_cast<const uint4*>(CS + i * PITCH), a.inv_sqrt_d, l);
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      E[j * m + i] = l[j];
-      mymax[j] = fmaxf(mymax[j], l[j]);
+        for (int j = 0; j < G; ++j) {
+          E[j * m + b0 + i] = l[j];
+          mymax[j] = fmaxf(mymax[j], l[j]);
+        }
+      }
+      __syncthreads();
     }
   }
 #pragma unroll
@@ -238,7 +268,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   const int u0 = min(n, tid * per), u1 = min(n, u0 + per);
   {
     unsigned long long kmn = ~0ull, kmx = 0ull;
-    for (int u = u0; u < u1; ++u) {
+    for (int u = tid; u < n; u += AT_THREADS) {
       const unsigned long long k = rep_key(RA, u);
       kmn = k < kmn ? k : kmn;
       kmx = k > kmx ? k : kmx;
@@ -282,9 +312,25 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     s_hist[tid] = 0;
     __syncthreads();
     if (cb < 0) {
-      for (int u = tid; u < n; u += AT_THREADS) {
+      // most keys share a few buckets (the bulk of A has one exponent): each thread sums its
+      // contiguous units per run of equal buckets, and a warp whose lanes all hold the same bucket
+      // adds once — no same-address atomic storms
+      int mb = -1, macc = 0;
+      for (int u = u0; u < u1; ++u) {
         const unsigned long long k = rep_key(RA, u);
-        if ((k & himask) == pre0) atomicAdd(&s_hist[(unsigned)(k >> lo_bit) & wmask], (int)SZ[u]);
+        if ((k & himask) != pre0) continue;
+        const int bk = (int)((unsigned)(k >> lo_bit) & wmask);
+        if (mb < 0) mb = bk;
+        if (bk == mb) macc += (int)SZ[u];
+        else atomicAdd(&s_hist[bk], (int)SZ[u]);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, mb);
+      if (peers == 0xffffffffu) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) macc += __shfl_xor_sync(0xffffffffu, macc, o);
+        if (lane == 0 && mb >= 0 && macc) atomicAdd(&s_hist[mb], macc);
+      } else if (mb >= 0 && macc) {
+        atomicAdd(&s_hist[mb], macc);
       }
     } else {
       const unsigned long long* L = LB + cb * LCAP;
@@ -409,12 +455,25 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   __syncthreads();  // (the id lists in the same region are dead)
   if (tid == 0) s_nc = 0;
   __syncthreads();
-  for (int u = u0; u < u1; ++u) {
-    const unsigned long long k = rep_key(RA, u);
-    if (k < pivot) {
-      atomicOr(&TK[u >> 5], 1u << (u & 31));
-    } else if (rem1 > 0 && k > pivot && SZ[u] <= rem1) {
-      const int slot = atomicAdd(&s_nc, 1);
+  // one warp per 32 consecutive units: the taken bits are one TK word (exclusive owner, plain
+  // store), the tail candidates are compacted with one shared atomic per warp
+  for (int base = warp * 32; base < n; base += AT_THREADS) {
+    const int u = base + lane;
+    bool take = false, cand = false;
+    unsigned long long k = 0;
+    if (u < n) {
+      k = rep_key(RA, u);
+      take = k < pivot;
+      cand = rem1 > 0 && k > pivot && SZ[u] <= rem1;
+    }
+    const unsigned tbits = __ballot_sync(0xffffffffu, take);
+    const unsigned cbits = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) TK[base >> 5] = tbits;
+    int b0 = 0;
+    if (lane == 0 && cbits) b0 = atomicAdd(&s_nc, __popc(cbits));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (cand) {
+      const int slot = b0 + __popc(cbits & ((1u << lane) - 1u));
       if (slot < T_CAP) T[slot] = k | ((unsigned long long)SZ[u] << 48);
     }
   }
@@ -487,9 +546,11 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
       rows_l += SZ[u];
       ++cnt_l;
     }
-  int total, ns;
-  int dst = lk_scan(rows_l, s_warp, total);
-  int k = lk_scan(cnt_l, s_warp, ns);
+  // one scan of (rows | count << 16): rows <= B <= 65534, count <= LK_REP_N
+  int tot_p;
+  const int ex_p = lk_scan(rows_l | (cnt_l << 16), s_warp, tot_p);
+  const int total = tot_p & 0xFFFF, ns = tot_p >> 16;
+  int dst = ex_p & 0xFFFF, k = ex_p >> 16;
   prof_stamp(prof, 19);
   const int64_t gi = a.inst_global_base + li;
   const uint8_t* curK = reinterpret_cast<const uint8_t*>(a.ws + ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride);
@@ -499,12 +560,31 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   const int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
   const int64_t* uoff = a.uoff + (int64_t)li * a.Umax;
   unsigned long long reused = 0, fetched = 0, hbytes = 0;
-  for (int u = u0; u < u1; ++u) {
-    if (!(TK[u >> 5] >> (u & 31) & 1u)) continue;
+  constexpr int LB_N = 8;  // the selection-state loads of 8 units are issued together (one round trip)
+  for (int ub = u0; ub < u1; ub += LB_N) {
+    uint8_t hadv[LB_N];
+    int sov[LB_N];
+    int64_t uov[LB_N];
+#pragma unroll
+    for (int i = 0; i < LB_N; ++i) {
+      const int u = ub + i;
+      hadv[i] = 0;
+      sov[i] = 0;
+      uov[i] = 0;
+      if (u < u1 && (TK[u >> 5] >> (u & 31) & 1u)) {
+        hadv[i] = sel[u];
+        sov[i] = seloff[u];
+        uov[i] = uoff[u];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < LB_N; ++i) {
+    const int u = ub + i;
+    if (u >= u1 || !(TK[u >> 5] >> (u & 31) & 1u)) continue;
     const int sz = SZ[u];
-    const uint8_t had = sel[u];  // (the three loads are independent: one round trip)
-    const int so = seloff[u];
-    const int64_t uo = uoff[u];
+    const uint8_t had = hadv[i];
+    const int so = sov[i];
+    const int64_t uo = uov[i];
     SelEnt e;
     e.dst = dst;
     e.sz = sz;
@@ -524,6 +604,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     LIST[k++] = e;
     if (u >= lo && u < hi) own_dst[u - lo] = dst;
     dst += sz;
+    }
   }
   if (rank == 0) {
     for (int o = 16; o; o >>= 1) {
@@ -614,7 +695,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   __shared__ double s_cos[64];
   __shared__ double s_r;
   __shared__ int s_flag;
-  __shared__ float sq[G][D];
+  __shared__ __align__(16) float sq[G][D];
   constexpr int DS = D / AT_CL;  // output dims finalised by each rank
   __shared__ float mg_acc[AT_CL][G][DS];
   __shared__ float mg_ml[AT_CL][G][2];
@@ -648,26 +729,21 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   }
   __syncthreads();
   prof_stamp(prof, 2);
-  {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/8): centroid rows, sizes and
-     // the old selection / pool offsets. The trigger resolves in ~2 us; on an unflagged step the
-     // lines are simply not used (the step is latency-bound, HBM mostly idle).
+  if (tid == 0) {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/8): centroid
+     // rows, sizes and the old selection / pool offsets — five bulk prefetches (TMA unit, no LSU
+     // traffic). The trigger resolves in ~2 us; on an unflagged step the lines are simply not used.
     const int nu = s_S.n_units, mu = (nu + AT_CL - 1) / AT_CL;
     const int plo = min(nu, rank * mu), phi = min(nu, plo + mu);
-    const uint8_t* cb8 = reinterpret_cast<const uint8_t*>(a.centb + ((int64_t)li * a.Umax + plo) * D);
-    for (int i = tid; i < 2 * (phi - plo); i += AT_THREADS) prefetch_l2(cb8 + (int64_t)i * 128);
     const int64_t ib = (int64_t)li * a.Umax;
-    const uint8_t* p_us = reinterpret_cast<const uint8_t*>(a.usize + ib + plo);
-    const uint8_t* p_so = reinterpret_cast<const uint8_t*>(a.seloff + ib + plo);
-    const uint8_t* p_uo = reinterpret_cast<const uint8_t*>(a.uoff + ib + plo);
-    const uint8_t* p_se = a.sel + ib + plo;
-    const int nl4 = ((phi - plo) * 4 + 127) / 128, nl8 = ((phi - plo) * 8 + 127) / 128, nl1 = (phi - plo + 127) / 128;
-    if (tid < nl4) {
-      prefetch_l2(p_us + tid * 128);
-      prefetch_l2(p_so + tid * 128);
+    if (phi > plo) {
+      bulk_prefetch_l2(a.centb + (ib + plo) * D, (phi - plo) * ROW_BYTES);
+      bulk_prefetch_l2(a.usize + ib + plo, (phi - plo) * 4);
+      bulk_prefetch_l2(a.seloff + ib + plo, (phi - plo) * 4);
+      bulk_prefetch_l2(a.uoff + ib + plo, (phi - plo) * 8);
+      bulk_prefetch_l2(a.sel + ib + plo, phi - plo);
     }
-    if (tid < nl8) prefetch_l2(p_uo + tid * 128);
-    if (tid < nl1) prefetch_l2(p_se + tid * 128);
   }
+  prof_stamp(prof, 24);
   const int t = s_S.step + 1, par = t & 1;
   const int cap = app.ring_cap;
   const AttnArgs& at = A.at;
@@ -677,17 +753,31 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   // this rank's attention plan: 1/8 of sinks, working set and local window (the new token, the
   // window's last row, taken from the input by the last rank)
   auto make_plan = [&](AttnPlan& pl, const bf16* wsk, int ws_rows_r, int win_head, int win_n) {
-    pl.P.np = 0;
+    // always the same four pieces at fixed indices (possibly empty: the piece lookup takes the
+    // last piece starting at or before a row), so the plan stays in registers
     const int se = s_S.s_eff;
     const int s0 = se * rank / AT_CL, s1 = se * (rank + 1) / AT_CL;
     const bf16* sk = at.sinks + (int64_t)li * 2 * at.S * D;
-    pl.P.add(s1 - s0, sk + (int64_t)s0 * D, sk + (int64_t)at.S * D + (int64_t)s0 * D);
-    pl.P.add(ws_rows_r, wsk, wsk + (int64_t)a.budget * D);
     const int w0 = win_n * rank / AT_CL, w1 = win_n * (rank + 1) / AT_CL;
     const int hs = (win_head + w0) % cap;
     const int first = min(w1 - w0, cap - hs);
-    pl.P.add(first, ringK + (int64_t)hs * D, ringV + (int64_t)hs * D);
-    pl.P.add(w1 - w0 - first, ringK, ringV);
+    pl.P.np = 4;
+    pl.P.v0[0] = 0;
+    pl.P.n[0] = s1 - s0;
+    pl.P.k[0] = sk + (int64_t)s0 * D;
+    pl.P.v[0] = sk + (int64_t)at.S * D + (int64_t)s0 * D;
+    pl.P.v0[1] = s1 - s0;
+    pl.P.n[1] = ws_rows_r;
+    pl.P.k[1] = wsk;
+    pl.P.v[1] = wsk + (int64_t)a.budget * D;
+    pl.P.v0[2] = s1 - s0 + ws_rows_r;
+    pl.P.n[2] = first;
+    pl.P.k[2] = ringK + (int64_t)hs * D;
+    pl.P.v[2] = ringV + (int64_t)hs * D;
+    pl.P.v0[3] = s1 - s0 + ws_rows_r + first;
+    pl.P.n[3] = w1 - w0 - first;
+    pl.P.k[3] = ringK;
+    pl.P.v[3] = ringV;
     pl.rows = (s1 - s0) + ws_rows_r + (w1 - w0);
     pl.mask_lo = pl.mask_hi = 0;
     pl.new_vr = (rank == AT_CL - 1 && w1 > w0) ? pl.rows - 1 : -1;
@@ -706,13 +796,16 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     attn_load_chunk(pl, c, nv);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  prof_stamp(prof, 25);
   if (tid >= 32 && tid < 64) {  // prefetch the sealed-segment FIFO head entries (evictions)
     const int k = tid - 32;
     if (k < s_S.fifo_count) s_fifo[k] = app.fifo[(int64_t)li * cap + (s_S.fifo_head + k) % cap];
   }
-  // every rank's reads of the instance state happen-before the appending rank commits it: split
-  // cluster barrier, arrived here and waited on before the first later barrier
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  // split cluster barrier (arrived here, waited on before the first DSMEM store): every rank has
+  // started before any rank writes its shared memory. Relaxed: a release would stall until the
+  // speculative attention loads above have landed. (Every rank's reads of the instance state are
+  // ordered before the appending rank's commit by the merge barrier, which every rank passes first.)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   // ---- 2. trigger r_t (recipe R1), identical on every rank: 8 lanes per head, lane l8 sums dims
   // [8 l8, 8 l8 + 8) and [8 l8 + 64, 8 l8 + 72) sequentially, adds them (the tree's first level),
@@ -768,6 +861,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   } else if (!a.shared_copy) {
     trigger_cosines<AT_THREADS>(qc, qr_old, a.Hq, s_cos);
   }
+  prof_stamp(prof, 26);
   __syncthreads();
   if (tid == 0) {
     int flag;
@@ -814,6 +908,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     }
     s_post = p;
   }
+  prof_stamp(prof, 27);
   __syncthreads();
   prof_stamp(prof, 3);
 #ifdef LKV_PROF
@@ -980,5 +1075,10 @@ cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st) {
 #ifdef LKV_PROF
 extern "C" int louiskv_prof_read(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, lkv::g_lkv_prof, bytes);
+}
+extern "C" int louiskv_prof_clear(void) {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, lkv::g_lkv_prof);
+  return (int)cudaMemset(p, 0, sizeof(lkv::g_lkv_prof));
 }
 #endif

@@ -169,7 +169,7 @@ struct LayerArgs {
   AttnArgs at;  // fused = 1, at.app = the append arguments
   int layer;    // (LKV_PROF builds: timestamp rows of this layer)
 };
-constexpr int PROF_SLOTS = 24;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
+constexpr int PROF_SLOTS = 32;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
 // the single launch handles instances with at most LAYER_REP_UNITS units and at most LAYER_REP_SEL
 // selectable units (min(Umax, B)); larger contexts run the multi-kernel sequence
 constexpr int LAYER_REP_UNITS = 8192;

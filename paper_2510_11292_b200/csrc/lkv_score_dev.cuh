@@ -103,4 +103,34 @@ __device__ __forceinline__ void logits_row(const float (*sq)[D], const uint4* ro
   for (int j = 0; j < G; ++j) out[j] = __fmul_rn(acc[j], inv_sqrt_d);
 }
 
+// logits_row with the centroid row in shared memory (same arithmetic, same order); the query
+// values are read as broadcast float4s (one shared-memory wavefront per 4 FMAs per head)
+template <int G>
+__device__ __forceinline__ void logits_row_smem(const float (*sq)[D], const uint4* row, const float inv_sqrt_d,
+                                                float* out) {
+  float acc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) acc[j] = 0.0f;
+#pragma unroll 2
+  for (int c8 = 0; c8 < D / 8; ++c8) {
+    float cf[8];
+    unpack8(row[c8], cf);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const float4 qa = reinterpret_cast<const float4*>(&sq[j][c8 * 8])[0];
+      const float4 qb = reinterpret_cast<const float4*>(&sq[j][c8 * 8])[1];
+      acc[j] = __fmaf_rn(qa.x, cf[0], acc[j]);
+      acc[j] = __fmaf_rn(qa.y, cf[1], acc[j]);
+      acc[j] = __fmaf_rn(qa.z, cf[2], acc[j]);
+      acc[j] = __fmaf_rn(qa.w, cf[3], acc[j]);
+      acc[j] = __fmaf_rn(qb.x, cf[4], acc[j]);
+      acc[j] = __fmaf_rn(qb.y, cf[5], acc[j]);
+      acc[j] = __fmaf_rn(qb.z, cf[6], acc[j]);
+      acc[j] = __fmaf_rn(qb.w, cf[7], acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) out[j] = __fmul_rn(acc[j], inv_sqrt_d);
+}
+
 }  // namespace lkv

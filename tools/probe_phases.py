@@ -4,7 +4,8 @@ Needs the profiling build (python paper_2510_11292_b200/build.py --prof); loads 
 LOUISKV_LIB. Slots (globaltimer ns, thread 0 of every CTA): 0 entry, 1 after griddepcontrol.wait,
 2 state read, 3 trigger done, 4 select done (flagged), 5 gather done, 6 append done (rank 0),
 7 after publish barrier, 8 first attention chunk landed, 9 main loop done, 10/11 merge barrier,
-12/13 final barrier, 14 exit. Reports medians relative to the launch's earliest entry.
+12/13 final barrier, 14 exit; 24 after the L2 prefetch, 25 speculative attention loads issued,
+26 trigger math done (before the block barrier), 27 tid 0 flag + window done. Reports medians relative to the launch's earliest entry.
 """
 import ctypes, json, os, sys
 import numpy as np
@@ -49,12 +50,17 @@ with torch.cuda.graph(g, stream=s):
     issue()
 rd = lkv.lib().louiskv_prof_read
 rd.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-buf = np.zeros((64, 2048, 24), np.uint64)
+clr = lkv.lib().louiskv_prof_clear
+ORDER = [0, 1, 2, 24, 25, 26, 27, 3, 20, 6, 13, 16, 17, 15, 18, 19, 4, 5, 7, 8, 9, 10, 11, 12, 14]
+deltas = {"unflagged": [], "flagged": []}
+buf = np.zeros((64, 2048, 32), np.uint64)
 n_cta = b * Hkv * 8
 rows = {"unflagged": [], "flagged": []}
 gaps = []
 for i in range(1, STEPS + 1):
     q_in.copy_(q[i]); k_in.copy_(kk[i]); v_in.copy_(vv[i])
+    torch.cuda.synchronize()
+    clr()
     g.replay()
     torch.cuda.synchronize()
     if i < 4:
@@ -75,6 +81,17 @@ for i in range(1, STEPS + 1):
         rel[:, 22] = np.where(ok, (t[:, 23] - t[:, 22]) / np.maximum(t[:, 4] - t[:, 3], 1), np.nan)  # SM GHz
         rel[:, 23] = np.nan
         key = "flagged" if fl[l].any() else "unflagged"
+        # per CTA: time from the previous present stamp (program order), median over CTAs
+        dl = {}
+        for c in range(n_cta):
+            prev = None
+            for sl in ORDER:
+                if t[c, sl] == 0:
+                    continue
+                if prev is not None:
+                    dl.setdefault(f"{prev}->{sl}", []).append(int(t[c, sl] - t[c, prev]))
+                prev = sl
+        deltas[key].append({k_: float(np.median(v_)) for k_, v_ in dl.items()})
         rows[key].append(np.nanmedian(rel, axis=0).tolist() + [np.nanmax(rel[:, 14])])
         buf[l] = 0
         if prev_end is not None:
@@ -83,4 +100,8 @@ for i in range(1, STEPS + 1):
 res = {k: (np.median(np.array(v), axis=0).round(0).tolist() if v else None) for k, v in rows.items()}
 res["n"] = {k: len(v) for k, v in rows.items()}
 res["gap_prev_exit_to_entry_ns_median"] = float(np.median(gaps)) if gaps else None
+for k_, lst in deltas.items():
+    if lst:
+        keys = sorted({x for d_ in lst for x in d_}, key=lambda z: ORDER.index(int(z.split("->")[1])))
+        res["delta_" + k_] = {x: float(np.median([d_[x] for d_ in lst if x in d_])) for x in keys}
 print(json.dumps(res))

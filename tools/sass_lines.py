@@ -7,21 +7,21 @@ full = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True
 sec = re.search(r"\.section\s+\.text\." + re.escape(func) + r".*?(?=\n\s*\.section|\Z)", full, re.S)
 dis = sec.group(0) if sec else ""
 line_of = {}
-inner = outer = None
+inner = outer = "?"
+new_group = True
 for ln in dis.splitlines():
     m = re.search(r'//## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', ln)
     if m:
-        f, l = m.group(1).split("/")[-1], int(m.group(2))
-        if m.group(3) is None:
-            outer = f"{f}:{l}"
-            inner = inner if inner else outer
-        else:
-            inner = f"{f}:{l}"
+        loc = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
+        if new_group:  # the first marker of a group is the innermost location, the last the kernel's
+            inner = loc
+            new_group = False
+        outer = loc
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
     if m:
-        line_of[int(m.group(1), 16)] = (inner or "?", outer or "?", m.group(2).strip())
-        inner = None
+        line_of[int(m.group(1), 16)] = (inner, outer, m.group(2).strip())
+        new_group = True
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
