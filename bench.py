@@ -45,6 +45,10 @@ def parse():
     p.add_argument("--cpu-steps", type=int, default=48, help="oracle decode steps for cpu_baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--kmeans-impl", type=int, default=0)
+    p.add_argument("--shard", default="batch", choices=["batch", "heads"],
+                   help="multi-GPU partitioning: 'batch' = every rank its own sequences (weak scaling, no "
+                        "collective); 'heads' = ranks own contiguous KV-head ranges of the same sequences and "
+                        "all-gather the per-head attention outputs over NCCL after every layer (strong scaling)")
     return p.parse_args()
 
 
@@ -121,6 +125,31 @@ def dist_setup():
 def rank_seed(seed: int, rank: int) -> int:
     """Weak scaling: every rank draws its own independent sequences."""
     return seed + 1000 * rank
+
+
+def head_range(rank: int, world: int, num_kv_heads: int):
+    """KV-head shard of `rank`: contiguous ranges, num_kv_heads / world heads each."""
+    if num_kv_heads % world:
+        raise ValueError(f"--shard heads needs num_kv_heads ({num_kv_heads}) divisible by the world size ({world})")
+    hc = num_kv_heads // world
+    return rank * hc, hc
+
+
+def gather_heads(out_own, gathered, world: int):
+    """All-gather of one layer's per-head attention outputs (north_star: NCCL over NVLink, only for the
+    outputs). out_own [b, g*hc, d] -> gathered [world, b, g*hc, d] (rank-major: rank r holds query heads
+    [r*g*hc, (r+1)*g*hc)). Stream-ordered, so it is captured into the step's CUDA graph."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(gathered.view((-1,) + tuple(out_own.shape[1:])), out_own)
+    else:
+        gathered[0].copy_(out_own)
+
+
+def assemble_heads(gathered):
+    """[world, b, g*hc, d] -> [b, Hq, d] in model head order (what the O-projection consumes)."""
+    w, b, gh, d = gathered.shape
+    return gathered.permute(1, 0, 2, 3).reshape(b, w * gh, d)
 
 
 def max_over_ranks(x: float, world: int) -> float:
@@ -228,15 +257,21 @@ def main():
     K, W = args.steps, args.warmup
     A = args.attr_steps
     T = 1 + W + K + K + A + 2  # direct step + warmup + timed + e2e + attribution (+slack)
-    seed = rank_seed(args.seed, rank)
-    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=max(cfg.max_output_len, T + 1), device=local,
+    heads = args.shard == "heads"
+    # batch sharding: every rank its own sequences; head sharding: the same sequences, own KV heads
+    seed = args.seed if heads else rank_seed(args.seed, rank)
+    hb, hc = head_range(rank, world, Hkv) if heads else (0, Hkv)
+    gq = g * hc  # query heads owned by this rank
+    jobs = 1 if heads else world  # independent sequence batches processed by the whole job
+    ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=hb, kv_head_count=hc,
+                                      max_output_len=max(cfg.max_output_len, T + 1), device=local,
                                       kmeans_impl=args.kmeans_impl))
 
     # ---------------- prefill: cluster_prompt for every layer, timed as one region ending at the
     # prompt fence (k-means keys/s; the copy-engine offload of layer l overlaps layer l+1's k-means)
     plants = [synth.planted(cfg, l, seed, dev) for l in range(L)]
-    prompts = [synth.prompt_kv(cfg, l, seed, dev, plants[l]) for l in range(L)]
-    km_keys = sum(b * Hkv * (cfg.prompt_len - cfg.sink_tokens) for l in range(L) if l not in full)
+    prompts = [tuple(t[:, :, hb:hb + hc] for t in synth.prompt_kv(cfg, l, seed, dev, plants[l])) for l in range(L)]
+    km_keys = sum(b * hc * (cfg.prompt_len - cfg.sink_tokens) for l in range(L) if l not in full)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -245,7 +280,8 @@ def main():
     ctx.prompt_fence()
     e1.record()
     torch.cuda.synchronize()
-    km_ms = e0.elapsed_time(e1)
+    km_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    km_keys *= world  # keys clustered by the whole job (every rank: its own heads or sequences)
     del prompts
     st0 = ctx.stats()
 
@@ -255,7 +291,11 @@ def main():
     q_in = torch.empty((L, b, Hq, d), dtype=torch.bfloat16, device=dev)
     k_in = torch.empty((L, b, Hkv, d), dtype=torch.bfloat16, device=dev)
     v_in = torch.empty((L, b, Hkv, d), dtype=torch.bfloat16, device=dev)
-    out = torch.empty((L, b, Hq, d), dtype=torch.bfloat16, device=dev)
+    out = torch.empty((L, b, gq, d), dtype=torch.bfloat16, device=dev)
+    # head sharding: per-layer all-gather of the owned heads' outputs -> [L, world, b, gq, d]
+    gathered = torch.empty((L, world, b, gq, d), dtype=torch.bfloat16, device=dev) if heads else None
+    k_own = k_in[:, :, hb:hb + hc]
+    v_own = v_in[:, :, hb:hb + hc]
 
     flags = torch.zeros((L, b), dtype=torch.uint8, device=dev)
 
@@ -265,7 +305,9 @@ def main():
         for l in range(L):
             if events is not None:
                 events[l].record()
-            ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], flag_out=flags[l])
+            ctx.decode_layer(l, q_in[l], k_own[l], v_own[l], out[l], flag_out=flags[l])
+            if heads:
+                gather_heads(out[l], gathered[l], world)
         if events is not None:
             events[L].record()
 
@@ -294,43 +336,69 @@ def main():
         graph.replay()
         step_idx += 1
     # ---------------- timed region (device-resident inputs)
+    P_, nr_ = cfg.prompt_len, L - len(full)
+    kv_step_bytes = (len(full) * b * hc * (P_ + T) + nr_ * b * hc * (cfg.sink_tokens + cfg.budget_tokens
+                                                                      + cfg.window_tokens)) * 512
+    L2_BYTES = 126 * 2 ** 20
+    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if kv_step_bytes < 2 * L2_BYTES else None
     clocks = ClockSampler(local)
     barrier(world)
     clocks.start()
     st_a = ctx.stats()
     barrier(world)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for i in range(K):
+    def dev_timed(body):
+        """Device time of K calls of body(i). When the rank's per-step KV bytes fit in L2 (head sharding
+        over many GPUs), L2 is flushed between steps, outside the timed spans (per-step event pairs)."""
+        if flush_buf is None:
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for i in range(K):
+                body(i)
+            t1.record()
+            torch.cuda.synchronize()
+            return t0.elapsed_time(t1)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for i in range(K):
+            flush_buf.add_(1)
+            evs[i][0].record()
+            body(i)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(z) for a, z in evs)
+
+    def timed_body(i):
+        nonlocal step_idx
         load(step_idx)
         graph.replay()
         step_idx += 1
-    ev1.record()
+
+    ms = dev_timed(timed_body)
     barrier(world)
     clk = clocks.stop()
-    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    ms = max_over_ranks(ms, world)
     st_b = ctx.stats()
-    value = world * b * K / (ms / 1e3)
+    value = jobs * b * K / (ms / 1e3)
 
     # ---------------- e2e: host inputs -> device, graph, outputs -> host, every step
     qh = q[step_idx:step_idx + K].cpu().pin_memory()
     kh = kk[step_idx:step_idx + K].cpu().pin_memory()
     vh = vv[step_idx:step_idx + K].cpu().pin_memory()
-    oh = torch.empty((K, L, b, Hq, d), dtype=torch.bfloat16).pin_memory()
+    res = gathered if heads else out  # the step's result: every query head's output
+    oh = torch.empty((K,) + tuple(res.shape), dtype=torch.bfloat16).pin_memory()
     barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(K):
+    def e2e_body(i):
+        nonlocal step_idx
         q_in.copy_(qh[i], non_blocking=True)
         k_in.copy_(kh[i], non_blocking=True)
         v_in.copy_(vh[i], non_blocking=True)
         graph.replay()
-        oh[i].copy_(out, non_blocking=True)
+        oh[i].copy_(res, non_blocking=True)
         step_idx += 1
-    e1.record()
+
+    e2e_ms = dev_timed(e2e_body)
     barrier(world)
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
-    e2e = {"value": world * b * K / (e2e_ms / 1e3), "unit": UNIT,
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    e2e = {"value": jobs * b * K / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(qh[0].numel() + kh[0].numel() + vh[0].numel()) * 2,
            "d2h_bytes_per_step": int(oh[0].numel()) * 2, "ms_per_step": e2e_ms / K}
 
@@ -342,7 +410,7 @@ def main():
 
     def issue_subset(layers):
         for l in layers:
-            ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], flag_out=flags[l])
+            ctx.decode_layer(l, q_in[l], k_own[l], v_own[l], out[l], flag_out=flags[l])
 
     g_ret, g_full = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_ret, stream=cap_stream):
@@ -406,14 +474,14 @@ def main():
     # (rows written 512 B each; host rows cross the link, kept rows are re-read from HBM).
     P = cfg.prompt_len
     t_mid = step_idx - A // 2
-    full_bytes = b * Hkv * (P + t_mid) * 2 * d * 2
+    full_bytes = b * hc * (P + t_mid) * 2 * d * 2
     att_rows, n_units = 0, 0
     kc = -(-(P - cfg.sink_tokens) // cfg.avg_cluster_size)
     for l in range(L):
         if l in full:
             continue
         for bb in range(b):
-            for hh in range(Hkv):
+            for hh in range(hc):
                 _, sizes, _ = ctx.get_units(l, bb, hh)
                 nws = len(ctx.get_working_set(l, bb, hh)[0])
                 att_rows += min(cfg.sink_tokens, P) + nws + (step_idx - int(sizes[kc:].sum()))
@@ -422,7 +490,7 @@ def main():
     unf_bytes = att_rows / n_rl * 512
     h2d_bytes = st_d["bytes_h2d"] - st_c["bytes_h2d"]
     flg_launches = max(len(t_flg), 1)
-    ws_rows_flg = b * Hkv * cfg.budget_tokens  # rows rebuilt per flagged launch (upper bound: B per instance)
+    ws_rows_flg = b * hc * cfg.budget_tokens  # rows rebuilt per flagged launch (upper bound: B per instance)
     flg_bytes = unf_bytes + n_units / n_rl * 256 + ws_rows_flg * 512 + (ws_rows_flg * 512 - h2d_bytes / flg_launches)
     ret_ms = (sum(t_unf) + sum(t_flg)) / max(len(t_unf) + len(t_flg), 1)
     ret_bytes = (unf_bytes * len(t_unf) + flg_bytes * len(t_flg)) / max(len(t_unf) + len(t_flg), 1)
@@ -467,14 +535,19 @@ def main():
     n_ret_layers = L - len(full)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (seeded, planted clusters/segments; no weights on this path)",
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if heads else "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, planted clusters/segments; no weights on this path)",
         "config": {"workload": f"{cfg.name}: Llama-3.1-8B attention shape (L=32, Hq=32, Hkv=8, d=128), "
                                f"{cfg.prompt_len}-token prompt, S={cfg.sink_tokens} W={cfg.window_tokens} "
                                f"B={cfg.budget_tokens} tau={cfg.tau} c={cfg.avg_cluster_size}, layers 0-1 full cache",
-                   "global_batch": b * world, "seq_len": cfg.prompt_len,
-                   "parallelism": f"weak dp{world} (independent sequences per rank, no collective)",
-                   "l2": f"inputs larger than L2: {(full_bytes * 2 + n_ret_layers * b * Hkv * (cfg.sink_tokens + cfg.budget_tokens + cfg.window_tokens) * 512) / 1e6:.0f} MB of KV read per step > 126 MB",
+                   "global_batch": b * jobs, "seq_len": cfg.prompt_len,
+                   "parallelism": (f"kv-head shard x{world} (heads [{hb}, {hb + hc}) on rank {rank}; NCCL "
+                                   f"all-gather of the per-head outputs after every layer)") if heads else
+                                  f"weak dp{world} (independent sequences per rank, no collective)",
+                   "l2": (f"inputs larger than L2: {kv_step_bytes / 1e6:.0f} MB of KV read per step per rank > 2 x 126 MB"
+                          if flush_buf is None else
+                          f"L2 flushed between steps ({kv_step_bytes / 1e6:.0f} MB of KV per step per rank; "
+                          f"per-step event pairs, flush outside the timed spans)"),
                    "cuda_graph": True},
         "e2e": e2e,
         "gpu_launches": launches_per_step * K,

@@ -237,7 +237,10 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
   }
   // split-K: ~2 CTAs per SM when the rows allow it; a split never ends with a tiny tail chunk
   // (rows per split rounded to whole 64-row pipeline chunks)
-  const int64_t want = (296 + n_ctas - 1) / n_ctas;
+#ifndef FA_SPLIT_CTAS
+#define FA_SPLIT_CTAS 296
+#endif
+  const int64_t want = (FA_SPLIT_CTAS + n_ctas - 1) / n_ctas;
   const int64_t chunks = (max_rows + 63) / 64;
   int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
   if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));

@@ -26,7 +26,13 @@ namespace fa {
 constexpr int THREADS = 128;
 constexpr int WARPS = THREADS / 32;
 constexpr int CHUNK = 64;                      // rows per stage (16 per warp)
-constexpr int STAGES = 3;
+#ifndef FA_STAGES
+#define FA_STAGES 3
+#endif
+#ifndef FA_MINB
+#define FA_MINB 2
+#endif
+constexpr int STAGES = FA_STAGES;
 constexpr int BOX_BYTES = CHUNK * 128;         // 64 rows x 64 dims bf16
 constexpr int STAGE_BYTES = 4 * BOX_BYTES;     // K lo, K hi, V lo, V hi
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*1024-B alignment of the swizzled boxes*/ + 128;
@@ -91,7 +97,7 @@ struct FullArgs {
 // LDGSTS: the stage ring is filled by cp.async (16 B per thread-op, coalesced rows, the same 128-B
 // swizzle as the TMA boxes); else by TMA tensor copies.
 template <int G, bool LDGSTS>
-__global__ void __launch_bounds__(THREADS, 2) attn_full_tc_kernel(const __grid_constant__ CUtensorMap tm, FullArgs a) {
+__global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __grid_constant__ CUtensorMap tm, FullArgs a) {
   pdl_wait_trigger();
   const int li = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
   const int b = li / a.hn, h = li % a.hn;

@@ -1,0 +1,49 @@
+"""Probe: device time of the full-cache decode attention (layers 0-1 of C2) alone, graph-replayed.
+
+usage: python tools/probe_full.py [attn_impl] [reps]  (attn_impl 0 = tensor cores (default), 1 = SIMT)
+Environment variables read by the library select load-path experiments (LOUISKV_FA_TMA)."""
+import json, os, sys
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+import torch
+import paper_2510_11292_b200 as lkv
+import synth
+from synth.configs import CONFIGS
+
+impl = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+cfg = CONFIGS["C2"]
+dev = torch.device("cuda", 0)
+ctx = lkv.Context(lkv.make_config(cfg, max_output_len=reps + 64, attn_impl=impl))
+layers = sorted(cfg.full_cache_layers)
+plants = {l: synth.planted(cfg, l, 0, dev) for l in layers}
+for l in layers:
+    ctx.cluster_prompt(l, *synth.prompt_kv(cfg, l, 0, dev, plants[l]))
+torch.cuda.synchronize()
+q = torch.randn((cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.head_dim), device=dev).bfloat16()
+k = torch.randn((cfg.num_layers, cfg.batch, cfg.num_kv_heads, cfg.head_dim), device=dev).bfloat16()
+out = torch.empty_like(q)
+for l in layers:
+    ctx.decode_layer(l, q[l], k[l], k[l], out[l])
+torch.cuda.synchronize()
+s = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    for l in layers:
+        ctx.decode_layer(l, q[l], k[l], k[l], out[l])
+for _ in range(5):
+    g.replay()
+torch.cuda.synchronize()
+ts = []
+for _ in range(reps // 2):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); g.replay(); b.record()
+    torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b) / len(layers))
+ts.sort()
+rows = cfg.prompt_len + reps // 2
+byts = cfg.batch * cfg.num_kv_heads * rows * 512
+med = ts[len(ts) // 2]
+print(json.dumps({"impl": impl, "tma": bool(os.environ.get("LOUISKV_FA_TMA")), "us_per_layer_median": med * 1e3,
+                  "us_min": ts[0] * 1e3, "GBps": byts / (med / 1e3) / 1e9, "bytes": byts}))
+ctx.close()
