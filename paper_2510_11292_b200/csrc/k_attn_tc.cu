@@ -91,7 +91,17 @@ struct FullArgs {
   bf16* out;
   float* out_f32;
   float* part;
-  int* counters;
+  int* counters;          // [n_inst] split tickets, then [1] the layer ticket of the fused step
+  // fused store_cache (louiskv_decode_layer on a full-cache layer): the kernel itself appends
+  // (k_t, v_t) at row P + t - 1, commits the layer's step counter and writes the layer's flags (0)
+  int fused;
+  const bf16* k_t;
+  const bf16* v_t;
+  int64_t stride_kv;
+  int* error;
+  uint8_t* flag_out;
+  double* r_out;
+  int batch;
 };
 
 // LDGSTS: the stage ring is filled by cp.async (16 B per thread-op, coalesced rows, the same 128-B
@@ -107,7 +117,9 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
 
-  const int64_t rows_all = a.full_P + *a.step;
+  // fused: this launch is step t = step + 1 and attends P + t rows, the last one being (k_t, v_t)
+  const int t_new = a.fused ? *a.step + 1 : 0;
+  const int64_t rows_all = a.full_P + (a.fused ? t_new : *a.step);
   const int n_rows = (int)(rows_all < a.full_cap ? rows_all : a.full_cap);
   const int nck = (n_rows + CHUNK - 1) / CHUNK;  // chunk-granular split
   const int c_begin = (int)((int64_t)nck * split / nsplit), c_end = (int)((int64_t)nck * (split + 1) / nsplit);
@@ -126,6 +138,29 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   };
   const bf16* kbase = a.full + (int64_t)li * 2 * a.full_cap * D;
   const bf16* vbase = kbase + a.full_cap * D;
+  if (a.fused) {
+    // store_cache on a full-cache layer: the split that owns the last chunk writes the
+    // new row before it loads anything (CTA barrier + proxy fence: the row is then read back by this
+    // CTA's own cp.async / TMA copies; no other CTA reads it)
+    if (split == nsplit - 1) {
+      const int64_t pos = a.full_P + t_new - 1;
+      if (pos < a.full_cap) {
+        if (tid < 32) {
+          const bf16* src = (tid < 16 ? a.k_t : a.v_t) + (int64_t)b * a.stride_kv + (int64_t)h * D;
+          bf16* dst = const_cast<bf16*>(tid < 16 ? kbase : vbase) + pos * D;
+          reinterpret_cast<uint4*>(dst)[tid & 15] = reinterpret_cast<const uint4*>(src)[tid & 15];
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+      } else if (tid == 0) {
+        *a.error = 1;
+      }
+      __syncthreads();
+    }
+    if (li == 0 && split == 0 && tid < a.batch) {  // full-cache layers never retrieve
+      if (a.flag_out) a.flag_out[tid] = 0;
+      if (a.r_out) a.r_out[tid] = 0.0;
+    }
+  }
   auto load = [&](int c) {  // cp.async path: every thread copies 16 of the chunk's 2048 16-B pieces
     const int st = c % STAGES;
     const uint32_t dst = su32(smem + st * STAGE_BYTES);
@@ -300,38 +335,74 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   if (!s_last) return;
   __threadfence();
   const float* P0 = a.part + (int64_t)li * nsplit * G * (D + 2);
-  float* s_w = s_acc;               // [nsplit][G] weights
-  float* s_l = s_acc + nsplit * G;  // [nsplit][G]
-  for (int t = tid; t < nsplit * G; t += THREADS) {
-    const int y = t / G, j = t % G;
-    s_w[t] = __ldcg(P0 + (y * G + j) * (D + 2) + D);
-    s_l[t] = __ldcg(P0 + (y * G + j) * (D + 2) + D + 1);
-  }
-  __syncthreads();
+  // the splits' partials are staged in shared memory (the idle stage ring) by cp.async in batches
+  // of SB splits — one round trip per batch instead of one dependent L2 load per split and output
+  constexpr int PF = G * (D + 2);                      // floats per split partial (16-B multiple)
+  constexpr int SB = (STAGES * STAGE_BYTES - 1024) / (PF * 4);  // splits per batch
+  float* s_w = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES - 1024);  // [G] running max, sum, ...
+  float* s_part = reinterpret_cast<float*>(smem);      // [SB][PF]
+  float accv[(G * D + THREADS - 1) / THREADS];
+#pragma unroll
+  for (int i = 0; i < (G * D + THREADS - 1) / THREADS; ++i) accv[i] = 0.f;
+  // pass 1: the global max and normaliser per head (the (m, l) pairs only: 2 floats per split-head)
   if (tid < G) {
     const int j = tid;
     float M = -INFINITY;
-    for (int y = 0; y < nsplit; ++y) M = fmaxf(M, s_w[y * G + j]);
+#pragma unroll 8
+    for (int y = 0; y < nsplit; ++y) M = fmaxf(M, __ldcg(P0 + y * PF + j * (D + 2) + D));
     float Lsum = 0.f;
+#pragma unroll 8
     for (int y = 0; y < nsplit; ++y) {
-      const float w = s_w[y * G + j] == -INFINITY ? 0.f : exp2f(s_w[y * G + j] - M);
-      s_w[y * G + j] = w;
-      Lsum += w * s_l[y * G + j];
+      const float m = __ldcg(P0 + y * PF + j * (D + 2) + D);
+      Lsum += (m == -INFINITY ? 0.f : exp2f(m - M)) * __ldcg(P0 + y * PF + j * (D + 2) + D + 1);
     }
-    const float inv = 1.f / Lsum;
-    for (int y = 0; y < nsplit; ++y) s_w[y * G + j] *= inv;
+    s_w[j] = M;
+    s_w[G + j] = 1.f / Lsum;
   }
-  __syncthreads();
-  for (int idx = tid; idx < G * D; idx += THREADS) {
-    const int j = idx / D, e = idx % D;
-    float A = 0.f;
-#pragma unroll 4
-    for (int y = 0; y < nsplit; ++y) A = fmaf(s_w[y * G + j], __ldcg(P0 + (y * G + j) * (D + 2) + e), A);
-    const int64_t oi = ((int64_t)(b * a.hn + h) * G + j) * D + e;
-    a.out[oi] = __float2bfloat16_rn(A);
-    if (a.out_f32) a.out_f32[oi] = A;
+  // pass 2: weighted sum of the partials, split order (deterministic)
+  for (int y0 = 0; y0 < nsplit; y0 += SB) {
+    const int nb = min(SB, nsplit - y0);
+    __syncthreads();  // (previous batch consumed)
+    const uint32_t dst = su32(s_part);
+    for (int i = tid; i < nb * PF / 4; i += THREADS) cp16(dst + i * 16, P0 + (int64_t)y0 * PF + i * 4, true);
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < (G * D + THREADS - 1) / THREADS; ++i) {
+      const int idx = tid + i * THREADS;
+      if (idx < G * D) {
+        const int j = idx / D, e = idx % D;
+        const float M = s_w[j];
+        for (int y = 0; y < nb; ++y) {
+          const float m = s_part[y * PF + j * (D + 2) + D];
+          const float w = m == -INFINITY ? 0.f : exp2f(m - M);
+          accv[i] = fmaf(w, s_part[y * PF + j * (D + 2) + e], accv[i]);
+        }
+      }
+    }
   }
-  if (tid == 0) a.counters[li] = 0;
+#pragma unroll
+  for (int i = 0; i < (G * D + THREADS - 1) / THREADS; ++i) {
+    const int idx = tid + i * THREADS;
+    if (idx < G * D) {
+      const int j = idx / D, e = idx % D;
+      const float A = accv[i] * s_w[G + j];
+      const int64_t oi = ((int64_t)(b * a.hn + h) * G + j) * D + e;
+      a.out[oi] = __float2bfloat16_rn(A);
+      if (a.out_f32) a.out_f32[oi] = A;
+    }
+  }
+  if (tid == 0) {
+    a.counters[li] = 0;
+    if (a.fused) {  // the last instance to finish commits the layer's step (every CTA has read it)
+      __threadfence();
+      const int nl = gridDim.x;
+      if (atomicAdd(&a.counters[nl], 1) == nl - 1) {
+        a.counters[nl] = 0;
+        *const_cast<int*>(a.step) = t_new;
+      }
+    }
+  }
 }
 
 }  // namespace fa
@@ -356,7 +427,7 @@ static cudaError_t launch_full_tc_g(const CUtensorMap& tm, const fa::FullArgs& f
 
 // Full-cache attention on tensor cores; returns cudaErrorNotSupported when the tensor map cannot be
 // built (the caller then uses the SIMT kernel).
-cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_t st) {
+cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_t st, const FullStepArgs* fs) {
   auto enc = tensor_map_encoder();
   if (!enc || a.g > 8 || (reinterpret_cast<uintptr_t>(a.full) & 15)) return cudaErrorNotSupported;
   CUtensorMap tm;
@@ -381,6 +452,16 @@ cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_
   f.out_f32 = a.out_f32;
   f.part = a.part;
   f.counters = a.counters;
+  f.fused = fs != nullptr;
+  if (fs) {
+    f.k_t = fs->k_t;
+    f.v_t = fs->v_t;
+    f.stride_kv = fs->stride_kv;
+    f.error = fs->error;
+    f.flag_out = fs->flag_out;
+    f.r_out = fs->r_out;
+    f.batch = fs->batch;
+  }
   switch (a.g) {
     case 1: return launch_full_tc_g<1>(tm, f, n_inst_layer, a.splits, st);
     case 2: return launch_full_tc_g<2>(tm, f, n_inst_layer, a.splits, st);

@@ -13,8 +13,10 @@ from synth.configs import CONFIGS
 impl = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 cfg = CONFIGS["C2"]
+if len(sys.argv) > 3:
+    cfg = cfg.replace(prompt_len=int(sys.argv[3]))
 dev = torch.device("cuda", 0)
-ctx = lkv.Context(lkv.make_config(cfg, max_output_len=reps + 64, attn_impl=impl))
+ctx = lkv.Context(lkv.make_config(cfg, max_output_len=2 * reps + 64, attn_impl=impl))
 layers = sorted(cfg.full_cache_layers)
 plants = {l: synth.planted(cfg, l, 0, dev) for l in layers}
 for l in layers:
@@ -41,9 +43,37 @@ for _ in range(reps // 2):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) / len(layers))
 ts.sort()
-rows = cfg.prompt_len + reps // 2
+# back to back (no host sync between replays): the device stays busy, as inside a decode step
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(reps // 2):
+    g.replay()
+b.record()
+torch.cuda.synchronize()
+b2b = a.elapsed_time(b) / (reps // 2) / len(layers)
+rows = cfg.prompt_len + reps
 byts = cfg.batch * cfg.num_kv_heads * rows * 512
 med = ts[len(ts) // 2]
-print(json.dumps({"impl": impl, "tma": bool(os.environ.get("LOUISKV_FA_TMA")), "us_per_layer_median": med * 1e3,
-                  "us_min": ts[0] * 1e3, "GBps": byts / (med / 1e3) / 1e9, "bytes": byts}))
+print(json.dumps({"P": cfg.prompt_len, "impl": impl, "tma": bool(os.environ.get("LOUISKV_FA_TMA")), "us_per_layer_median": med * 1e3,
+                  "us_min": ts[0] * 1e3, "us_back_to_back": b2b * 1e3, "GBps_b2b": byts / (b2b / 1e3) / 1e9, "GBps": byts / (med / 1e3) / 1e9, "bytes": byts}))
 ctx.close()
+
+if len(sys.argv) > 4:  # plain torch read of the same byte count, for comparison
+    x = torch.empty(byts // 2, dtype=torch.bfloat16, device=dev).normal_()
+    y = torch.empty(1, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        y = x.sum(dtype=torch.float32)
+    ts = []
+    for _ in range(50):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); y = x.sum(dtype=torch.float32); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(50):
+        y = x.sum(dtype=torch.float32)
+    b.record(); torch.cuda.synchronize()
+    t2 = a.elapsed_time(b) / 50
+    print(json.dumps({"torch_sum_us": ts[25] * 1e3, "GBps": byts / (ts[25] / 1e3) / 1e9, "b2b_us": t2 * 1e3,
+                      "GBps_b2b": byts / (t2 / 1e3) / 1e9}))
