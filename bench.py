@@ -152,6 +152,15 @@ def assemble_heads(gathered):
     return gathered.permute(1, 0, 2, 3).reshape(b, w * gh, d)
 
 
+def ncu_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant kernels from
+    the committed `ncu --set full` capture summary (profiles/r01_traffic.json); {} when absent."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+    except Exception:
+        return {}
+
+
 def max_over_ranks(x: float, world: int) -> float:
     """Max of a per-rank device time over all ranks (nccl on GPUs, gloo in the CPU tests)."""
     if world <= 1:
@@ -328,8 +337,9 @@ def main():
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=cap_stream):
         issue_step()
-    # retrieval layer: one clustered launch; full-cache layer: step kernel + attention
-    launches_per_step = sum(2 if l in full else 1 for l in range(L))
+    # retrieval layer: one clustered launch (layer_kernel); full-cache layer: one launch
+    # (attn_full_tc_kernel with store_cache fused)
+    launches_per_step = L
 
     for _ in range(W):
         load(step_idx)
@@ -466,6 +476,7 @@ def main():
     host_link_gbs = (256 << 20) / (best / 1e3) / 1e9
     del hl, hd
     peaks = measured_peaks()
+    traffic = ncu_traffic()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
     # ---- per-launch algorithmic bytes. Full-cache launch: K+V rows of P+t tokens. Retrieval-layer
@@ -496,17 +507,21 @@ def main():
     ret_bytes = (unf_bytes * len(t_unf) + flg_bytes * len(t_flg)) / max(len(t_unf) + len(t_flg), 1)
     ret_gbs = ret_bytes / (ret_ms / 1e3) / 1e9
     step_ms_attr = sum(phase.values())
+    lk_tr, fa_tr = traffic.get("layer_kernel"), traffic.get("attn_full_tc_kernel")
+    n_l = max(len(t_unf) + len(t_flg), 1)
+    layer_traffic = ((lk_tr["unflagged"] * len(t_unf) + lk_tr["flagged"] * len(t_flg)) / n_l) if lk_tr else None
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"
     roofline_layer = {"kernel": "layer_kernel (retrieval layers: trigger + score/select + gather + append + attention)",
                       "bound": "hbm", "achieved": ret_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ret_gbs / hbm_peak,
-                      "traffic": None, "bytes_per_launch": ret_bytes, "ms_per_launch": ret_ms,
+                      "traffic": layer_traffic, "bytes_per_launch": ret_bytes, "ms_per_launch": ret_ms,
                       "peak_source": peak_src,
                       "share_of_step": (phase["retrieval_layers_unflagged"] + phase["retrieval_layers_flagged"]) / step_ms_attr}
     attn_full_ms = mean(t_full)
     att_full_gbs = full_bytes / (attn_full_ms / 1e3) / 1e9
-    roofline_attn = {"kernel": "full_step_kernel + attn_kernel (full-cache layers, split-K flash-decode)",
+    roofline_attn = {"kernel": "attn_full_tc_kernel (full-cache layers: store_cache + split-K flash-decode, one launch)",
                      "bound": "hbm", "achieved": att_full_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": att_full_gbs / hbm_peak, "traffic": None, "bytes_per_launch": full_bytes,
+                     "frac": att_full_gbs / hbm_peak, "traffic": fa_tr["per_launch"] if fa_tr else None,
+                     "bytes_per_launch": full_bytes,
                      "ms_per_launch": attn_full_ms, "peak_source": peak_src,
                      "share_of_step": phase["full_cache_layers"] / step_ms_attr}
     flag_extra_ms = sum(t_flg) - len(t_flg) * mean(t_unf)
@@ -525,6 +540,9 @@ def main():
     roofline = {"kernel": roofline_layer["kernel"], "bound": "host_link", "achieved": link_gbs,
                 "peak": host_link_gbs, "unit": "GB/s", "frac": link_gbs / host_link_gbs if host_link_gbs else None,
                 "traffic": None, "bytes_per_launch": link_bytes, "ms_per_launch": ret_ms,
+                "traffic_note": "host-link bytes are counted by the kernel itself (stats bytes_h2d); the kernel's "
+                                "DRAM traffic per launch (ncu --set full, profiles/r01_traffic.json, weighted by this "
+                                "run's flagged/unflagged mix) is roofline_layer_hbm.traffic",
                 "lower_bound_us": {"hbm": ret_bytes / (hbm_peak * 1e9) * 1e6,
                                    "host_link": link_bytes / (host_link_gbs * 1e9) * 1e6 if host_link_gbs else None},
                 "peak_source": "pinned 256 MiB cudaMemcpy H2D measured in this run",

@@ -355,7 +355,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
   ok = ok && dalloc(c, &c->d_jobs, (size_t)c->L * nl);
   ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
-  ok = ok && dalloc(c, &c->d_counters, (size_t)nl);
+  ok = ok && dalloc(c, &c->d_counters, (size_t)nl + 1);  // + the fused full-cache step's layer ticket
   ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * (((std::max(c->kmax, 1) + 255) / 256) * 256));
   ok = ok && dalloc(c, &c->d_km_assign, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
   ok = ok && dalloc(c, &c->d_km_dmin, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
@@ -700,6 +700,25 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
   if (layer < 0 || layer >= c->L || !q_all || !k_t || !v_t || !out)
     return fail(c, LOUISKV_ERR_INVALID_ARG, "decode_layer: bad args");
   const void* q_own = reinterpret_cast<const bf16*>(q_all) + (int64_t)c->h0 * c->g * D;
+  if (is_full(c, layer) && c->cfg.attn_impl != LOUISKV_ATTN_SIMT) {
+    // full-cache layer: ONE launch — flags 0, store_cache of (k_t, v_t), dense attention, step commit
+    if (c->P[layer] < 0) return fail(c, LOUISKV_ERR_STATE, "decode_layer before cluster_prompt");
+    if (c->stage[layer] != 0 && c->stage[layer] != 3)
+      return fail(c, LOUISKV_ERR_STATE, "decode_layer: previous step incomplete");
+    if (c->t[layer] >= c->Mmax) return fail(c, LOUISKV_ERR_STATE, "decode_layer: max_output_len reached");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
+    AttnArgs a = attn_args(c, layer, q_own, stride_q, out, out_f32);
+    FullStepArgs fs{reinterpret_cast<const bf16*>(k_t), reinterpret_cast<const bf16*>(v_t), stride_kv, c->d_error,
+                    d_flag_out, d_r_out, c->batch};
+    const cudaError_t e = launch_attn_full_tc(a, c->inst_per_layer, st, &fs);
+    if (e == cudaSuccess) {
+      c->t[layer] += 1;
+      c->stage[layer] = 3;
+      return LOUISKV_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(c, e, "full-cache step (tensor cores)");
+  }
   if (is_full(c, layer) || c->Umax > LAYER_REP_UNITS || std::min(c->Umax, c->Bud) > LAYER_REP_SEL) {
     // full-cache layer (step kernel + attention), or an instance too large for the single launch
     louiskv_status s = louiskv_should_retrieve(c, layer, q_all, stride_q, d_flag_out, d_r_out, stream);

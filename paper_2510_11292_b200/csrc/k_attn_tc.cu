@@ -338,31 +338,44 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   // the splits' partials are staged in shared memory (the idle stage ring) by cp.async in batches
   // of SB splits — one round trip per batch instead of one dependent L2 load per split and output
   constexpr int PF = G * (D + 2);                      // floats per split partial (16-B multiple)
-  constexpr int SB = (STAGES * STAGE_BYTES - 1024) / (PF * 4);  // splits per batch
-  float* s_w = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES - 1024);  // [G] running max, sum, ...
+  constexpr int MAXS = 64;                             // (>= the host's max_splits)
+  constexpr int WB = 2 * MAXS * G * 4 + 2 * G * 4;     // bytes of the per-split weights + (M, 1/L)
+  constexpr int SB = (STAGES * STAGE_BYTES - WB) / (PF * 4);  // splits per staging batch
   float* s_part = reinterpret_cast<float*>(smem);      // [SB][PF]
+  float* s_wt = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES - WB);  // [nsplit][G] m, then weights
+  float* s_l = s_wt + MAXS * G;                        // [nsplit][G] l
+  float* s_w = s_l + MAXS * G;                         // [G] M, [G] 1/L
   float accv[(G * D + THREADS - 1) / THREADS];
 #pragma unroll
   for (int i = 0; i < (G * D + THREADS - 1) / THREADS; ++i) accv[i] = 0.f;
-  // pass 1: the global max and normaliser per head (the (m, l) pairs only: 2 floats per split-head)
-  if (tid < G) {
+  // (m, l) of every split-head, all loads in one round (they overlap the first batch's staging)
+  for (int t = tid; t < nsplit * G; t += THREADS) {
+    const int y = t / G, j = t % G;
+    s_wt[t] = __ldcg(P0 + y * PF + j * (D + 2) + D);
+    s_l[t] = __ldcg(P0 + y * PF + j * (D + 2) + D + 1);
+  }
+  __syncthreads();
+  if (tid < G) {  // global max and normaliser per head, split order
     const int j = tid;
     float M = -INFINITY;
-#pragma unroll 8
-    for (int y = 0; y < nsplit; ++y) M = fmaxf(M, __ldcg(P0 + y * PF + j * (D + 2) + D));
+    for (int y = 0; y < nsplit; ++y) M = fmaxf(M, s_wt[y * G + j]);
     float Lsum = 0.f;
-#pragma unroll 8
     for (int y = 0; y < nsplit; ++y) {
-      const float m = __ldcg(P0 + y * PF + j * (D + 2) + D);
-      Lsum += (m == -INFINITY ? 0.f : exp2f(m - M)) * __ldcg(P0 + y * PF + j * (D + 2) + D + 1);
+      const float m = s_wt[y * G + j];
+      Lsum += (m == -INFINITY ? 0.f : exp2f(m - M)) * s_l[y * G + j];
     }
     s_w[j] = M;
     s_w[G + j] = 1.f / Lsum;
   }
-  // pass 2: weighted sum of the partials, split order (deterministic)
+  __syncthreads();
+  for (int t = tid; t < nsplit * G; t += THREADS) {  // per-split weights 2^(m - M)
+    const float m = s_wt[t];
+    s_wt[t] = m == -INFINITY ? 0.f : exp2f(m - s_w[t % G]);
+  }
+  // weighted sum of the partials, split order (deterministic)
   for (int y0 = 0; y0 < nsplit; y0 += SB) {
     const int nb = min(SB, nsplit - y0);
-    __syncthreads();  // (previous batch consumed)
+    __syncthreads();  // (weights written / previous batch consumed)
     const uint32_t dst = su32(s_part);
     for (int i = tid; i < nb * PF / 4; i += THREADS) cp16(dst + i * 16, P0 + (int64_t)y0 * PF + i * 4, true);
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
@@ -372,12 +385,8 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
       const int idx = tid + i * THREADS;
       if (idx < G * D) {
         const int j = idx / D, e = idx % D;
-        const float M = s_w[j];
-        for (int y = 0; y < nb; ++y) {
-          const float m = s_part[y * PF + j * (D + 2) + D];
-          const float w = m == -INFINITY ? 0.f : exp2f(m - M);
-          accv[i] = fmaf(w, s_part[y * PF + j * (D + 2) + e], accv[i]);
-        }
+#pragma unroll 4
+        for (int y = 0; y < nb; ++y) accv[i] = fmaf(s_wt[(y0 + y) * G + j], s_part[y * PF + j * (D + 2) + e], accv[i]);
       }
     }
   }

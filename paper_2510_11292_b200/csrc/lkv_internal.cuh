@@ -160,7 +160,18 @@ struct AttnArgs {
 };
 cudaError_t launch_attn(const AttnArgs& a, cudaStream_t st);
 // full-cache layers on tensor cores (k_attn_tc.cu); cudaErrorNotSupported -> use launch_attn
-cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_t st);
+// store_cache fused into the full-cache attention (one launch per full-cache layer step)
+struct FullStepArgs {
+  const bf16* k_t;
+  const bf16* v_t;
+  int64_t stride_kv;
+  int* error;
+  uint8_t* flag_out;
+  double* r_out;
+  int batch;
+};
+cudaError_t launch_attn_full_tc(const AttnArgs& a, int n_inst_layer, cudaStream_t st,
+                                const FullStepArgs* fs = nullptr);
 
 // one decode step of one retrieval layer in ONE clustered launch (k_layer.cu): trigger (R1),
 // distributed score + select (R2/R3, greedy), gather, append, attention. r.q_own = q_all.
