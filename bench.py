@@ -297,9 +297,15 @@ def main():
     # ---------------- decode inputs (device resident) and static graph buffers
     q, kk, vv, bset = synth.decode_stream(cfg, T, seed, dev, plants)
     del plants
-    q_in = torch.empty((L, b, Hq, d), dtype=torch.bfloat16, device=dev)
-    k_in = torch.empty((L, b, Hkv, d), dtype=torch.bfloat16, device=dev)
-    v_in = torch.empty((L, b, Hkv, d), dtype=torch.bfloat16, device=dev)
+    # one step's inputs (q of all heads, k_t, v_t of every layer) packed in ONE buffer, so a step's
+    # input is a single copy: qkv [T, n_q + 2 n_kv] on the device (and pinned on the host for e2e)
+    n_q, n_kv = L * b * Hq * d, L * b * Hkv * d
+    qkv = torch.cat([q.reshape(T, -1), kk.reshape(T, -1), vv.reshape(T, -1)], dim=1)
+    del q, kk, vv
+    qkv_in = torch.empty((n_q + 2 * n_kv,), dtype=torch.bfloat16, device=dev)
+    q_in = qkv_in[:n_q].view(L, b, Hq, d)
+    k_in = qkv_in[n_q:n_q + n_kv].view(L, b, Hkv, d)
+    v_in = qkv_in[n_q + n_kv:].view(L, b, Hkv, d)
     out = torch.empty((L, b, gq, d), dtype=torch.bfloat16, device=dev)
     # head sharding: per-layer all-gather of the owned heads' outputs -> [L, world, b, gq, d]
     gathered = torch.empty((L, world, b, gq, d), dtype=torch.bfloat16, device=dev) if heads else None
@@ -323,9 +329,7 @@ def main():
     step_idx = 0
 
     def load(i):
-        q_in.copy_(q[i], non_blocking=True)
-        k_in.copy_(kk[i], non_blocking=True)
-        v_in.copy_(vv[i], non_blocking=True)
+        qkv_in.copy_(qkv[i], non_blocking=True)
 
     # step 1 runs directly (sets kernel attributes, t == 1 retrieval everywhere)
     load(step_idx)
@@ -390,17 +394,13 @@ def main():
     value = jobs * b * K / (ms / 1e3)
 
     # ---------------- e2e: host inputs -> device, graph, outputs -> host, every step
-    qh = q[step_idx:step_idx + K].cpu().pin_memory()
-    kh = kk[step_idx:step_idx + K].cpu().pin_memory()
-    vh = vv[step_idx:step_idx + K].cpu().pin_memory()
+    qkv_h = qkv[step_idx:step_idx + K].cpu().pin_memory()
     res = gathered if heads else out  # the step's result: every query head's output
     oh = torch.empty((K,) + tuple(res.shape), dtype=torch.bfloat16).pin_memory()
     barrier(world)
     def e2e_body(i):
         nonlocal step_idx
-        q_in.copy_(qh[i], non_blocking=True)
-        k_in.copy_(kh[i], non_blocking=True)
-        v_in.copy_(vh[i], non_blocking=True)
+        qkv_in.copy_(qkv_h[i], non_blocking=True)
         graph.replay()
         oh[i].copy_(res, non_blocking=True)
         step_idx += 1
@@ -409,7 +409,7 @@ def main():
     barrier(world)
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e = {"value": jobs * b * K / (e2e_ms / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": int(qh[0].numel() + kh[0].numel() + vh[0].numel()) * 2,
+           "h2d_bytes_per_step": int(qkv_h[0].numel()) * 2,
            "d2h_bytes_per_step": int(oh[0].numel()) * 2, "ms_per_step": e2e_ms / K}
 
     # ---------------- attribution pass: the retrieval layers and the full-cache layers captured as two
