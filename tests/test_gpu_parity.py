@@ -8,7 +8,7 @@ import torch
 import oracle
 import synth
 from oracle.episode import OracleEpisode, PREV_STEP, LAST_RETRIEVAL, PER_LAYER, SHARED
-from synth.configs import Config, C1, C2
+from synth.configs import Config, C1, C2, C3, C4, C5
 
 from _pair import bf16_bits, make_inputs, np32, oracle_assign, planted_assign
 
@@ -404,3 +404,38 @@ def test_c2_kmeans_full_size_properties():
             ref = X[a_g == j].astype(np.float64).mean(0)
             assert np.abs(C_g[j] - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1.0)
     ctx.close()
+
+
+# ------------------------------------------------------------------ the other BASELINE configs (reduced)
+def test_episode_c3_long_output_segments():
+    """C3 (Qwen3-8B short-input long-output): S=500, W=128, B=1024, tau=0.7, segments of mean
+    16 — the output-segment path at the config's own parameters: 1024-token prompt, 2 of its KV heads
+    (all 32 query heads for the trigger, g=4), 200 decode steps, so evicted segments become units and
+    are scored, selected and fetched back (compared every step)."""
+    cfg = C3.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, decode_steps=200)
+    inp = make_inputs(cfg, 200, 5)
+    _, n_flags, st = run_episode(cfg, inp, 200, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer",
+                                 check_every_step=True, compare_ws=True)
+    assert st["segments_evicted"] > 0 and n_flags > 5
+    assert st["units_fetched"] > 0
+
+
+def test_episode_c4_batch_lilo_params():
+    """C4 (long-input long-output): batch > 1 with S=64, W=256, B=1024, tau=0.7 on a reduced
+    prompt (4096) and 2 KV heads; both the per-call ABI sequence and the single-launch layer."""
+    cfg = C4.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, batch=3,
+                     prompt_len=4096, decode_steps=40)
+    inp = make_inputs(cfg, 40, 6)
+    for fused in (False, "layer"):
+        run_episode(cfg, inp, 40, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)
+
+
+def test_episode_c5_g8_qwen3_32b_heads():
+    """C5 (Qwen3-32B: 64 query heads, 8 KV heads, g=8): the GQA group of 8 in scoring (A averaged over
+    8 heads, App. B) and attention, and the 64-head trigger (r_t over all Hq heads), on a
+    reduced prompt (2048) and 2 layers."""
+    cfg = C5.replace(num_layers=2, full_cache_layers=(0,), batch=1, prompt_len=2048, decode_steps=30)
+    inp = make_inputs(cfg, 30, 7)
+    for fused in (False, "layer"):
+        _, n_flags, _ = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)
+        assert n_flags >= 2
