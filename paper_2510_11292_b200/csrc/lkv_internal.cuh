@@ -292,9 +292,11 @@ __device__ __forceinline__ void unpack8(const uint4 u, float* f) {
 // ---- programmatic dependent launch: every kernel waits for its predecessor grid (memory visible)
 // before touching shared state, then lets its dependent grid launch early (the launch latency of the
 // next kernel overlaps this one; the dependent still waits at its own griddepcontrol.wait)
+// (default on: measured -1..3 % on the C2 decode step; -DLKV_PDL_LATE_TRIGGER restores the implicit
+// trigger at grid completion)
 __device__ __forceinline__ void pdl_wait_trigger() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-#ifdef LKV_PDL_EARLY_TRIGGER
+#ifndef LKV_PDL_LATE_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
