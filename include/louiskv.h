@@ -77,6 +77,11 @@ typedef struct {
   int32_t device;            /* CUDA device ordinal */
   int32_t attn_impl;         /* full-cache attention: LOUISKV_ATTN_TC (mma.sync + TMA tensor maps,
                                 default) | LOUISKV_ATTN_SIMT (CUDA cores) */
+  int32_t trigger_stride;    /* 0 (default): the semantic-boundary trigger, flag = (t == 1) || r_t < tau
+                                (Alg. 1). k >= 1: the fixed-stride retrieval of the paper's
+                                ablation ("retrieves every 5 / 16 steps"): flag = (t - 1) % k == 0;
+                                r_t is still computed and reported, segments then span k tokens.
+                                Negative: INVALID_ARG at create. */
 } louiskv_config;
 
 typedef struct {

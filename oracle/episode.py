@@ -53,8 +53,11 @@ class _Inst:
 class OracleEpisode:
     def __init__(self, cfg, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, shared_layer=0,
                  max_open_segment: Optional[int] = None, kmeans_mode: int = 1,
-                 kv_head_begin: int = 0, kv_head_count: Optional[int] = None):
+                 kv_head_begin: int = 0, kv_head_count: Optional[int] = None, trigger_stride: int = 0):
         self.cfg = cfg
+        # trigger_stride k >= 1: the fixed-stride retrieval of the paper's ablation — retrieve
+        # at t = 1, 1 + k, 1 + 2k, ... instead of on r_t < tau; 0: the semantic boundary
+        self.stride = int(trigger_stride)
         self.L, self.Hq, self.Hkv, self.d = cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
         self.g = self.Hq // self.Hkv
         self.b = cfg.batch
@@ -133,6 +136,8 @@ class OracleEpisode:
             return self.flags[layer].copy(), self.r[layer].copy()
         for bb in range(self.b):
             f, r = core.trigger_r1(self.q_ref[layer][bb], q_all[bb], t, self.tau)
+            if self.stride > 0:
+                f = 1 if (t - 1) % self.stride == 0 else 0
             self.flags[layer][bb], self.r[layer][bb] = f, r
             if self.trigger_ref == PREV_STEP or f:
                 self.q_ref[layer][bb] = q_all[bb]

@@ -143,6 +143,7 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   a.Bmax = c->Bmax;
   a.trigger_ref = c->cfg.trigger_ref;
   a.tau = c->cfg.tau;
+  a.stride = c->cfg.trigger_stride;
   a.qref = c->d_qref + (size_t)layer * 2 * c->Bmax * c->Hq * D;
   a.r = c->d_r + (size_t)layer * c->Bmax;
   a.flag = c->d_flag + (size_t)layer * c->Bmax;
@@ -278,7 +279,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       k.num_q_heads % k.num_kv_heads != 0 || k.kv_head_begin < 0 || k.kv_head_count <= 0 ||
       k.kv_head_begin + k.kv_head_count > k.num_kv_heads || k.max_batch <= 0 || k.max_prompt_len <= 0 ||
       k.max_output_len <= 0 || k.budget_tokens < 0 || k.sink_tokens < 0 || k.window_tokens < 1 ||
-      k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) ||
+      k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) || k.trigger_stride < 0 ||
       (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
     return LOUISKV_ERR_INVALID_ARG;
   const int g = k.num_q_heads / k.num_kv_heads;

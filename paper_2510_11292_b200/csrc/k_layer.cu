@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     } else {
       const double rr = trigger_mean(s_cos, a.Hq);
       s_r = rr;
-      flag = (t == 1) || (rr < a.tau);
+      flag = a.stride > 0 ? ((t - 1) % a.stride == 0) : ((t == 1) || (rr < a.tau));
     }
     s_flag = flag;
     // post-store_cache window (the same seal / append / evict rules as append_one, state only)

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(TL_THREADS) trig_logits_kernel(RetrieveArgs a)
     if (tid == 0) {
       const double rr = trigger_mean(s_cos, a.Hq);
       s_r = rr;
-      s_flag = (t == 1) || (rr < a.tau);
+      s_flag = a.stride > 0 ? ((t - 1) % a.stride == 0) : ((t == 1) || (rr < a.tau));
     }
   }
   __syncthreads();

@@ -65,6 +65,7 @@ struct RetrieveArgs {
   // trigger (fused into the logits kernel launched by should_retrieve)
   int Hq, h0, Bmax, trigger_ref, shared_copy;
   double tau;
+  int stride;  // trigger_stride: 0 = semantic boundary (r_t < tau), k >= 1 = every k steps
   bf16* qref;                // layer base [2][Bmax][Hq][D], read buffer (t-1)&1, write t&1
   const uint8_t* flag_src;   // SHARED mode: designated layer's flags / r
   const double* r_src;

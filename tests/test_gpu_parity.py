@@ -32,7 +32,7 @@ def small_cfg(**kw):
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
                 check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False,
-                attn_impl=0):
+                attn_impl=0, trigger_stride=0):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
     fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
     "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
@@ -42,9 +42,9 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     g = cfg.group
     ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
                                       boundary_mode=boundary_mode, max_open_segment=max_open or 0,
-                                      attn_impl=attn_impl))
+                                      attn_impl=attn_impl, trigger_stride=trigger_stride))
     ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
-                       kv_head_begin=h0, kv_head_count=hn)
+                       kv_head_begin=h0, kv_head_count=hn, trigger_stride=trigger_stride)
     L, b = cfg.num_layers, cfg.batch
     for l in range(L):
         Kl = inp.K[l][:, :, h0:h0 + hn]
@@ -439,3 +439,16 @@ def test_episode_c5_g8_qwen3_32b_heads():
     for fused in (False, "layer"):
         _, n_flags, _ = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)
         assert n_flags >= 2
+
+
+def test_episode_fixed_stride_trigger():
+    """trigger_stride (the paper's fixed-stride ablation): retrieval at t = 1, 1+k, ... on every
+    layer, segments of k tokens; both the per-call ABI sequence and the single-launch layer (k = 5, 16)."""
+    for k in (5, 16):
+        cfg = small_cfg(decode_steps=40)
+        inp = make_inputs(cfg, 40, 8)
+        for fused in (False, "layer"):
+            _, n_flags, st = run_episode(cfg, inp, 40, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
+                                         fused=fused, trigger_stride=k)
+            n_ret = cfg.num_layers - len(cfg.full_cache_layers)
+            assert n_flags == n_ret * cfg.batch * len(range(0, 40, k))

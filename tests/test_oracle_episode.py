@@ -209,3 +209,18 @@ def test_offload_fetch_conservation():
     assert ep.stats["bytes_d2h"] == pool_rows * 2 * 2 * cfg.head_dim
     # budget law: retrieved rows <= B at every step
     assert sum(inst.units[u].positions.size for u in inst.selected) <= cfg.budget_tokens
+
+
+
+def test_fixed_stride_trigger_pattern_and_segments():
+    """trigger_stride = k (P:446 fixed-stride ablation): flags exactly at t = 1, 1+k, 1+2k, ...
+    whatever r_t is (the controlled queries put semantic boundaries elsewhere), and every evicted
+    output segment is k tokens long (segments are sealed at the flags)."""
+    cfg = tiny_cfg(decode_steps=30, window_tokens=8)
+    q, k, v = _controlled_queries(cfg, {1, 7, 19})
+    n_prompt_units = -(-(cfg.prompt_len - cfg.sink_tokens) // cfg.avg_cluster_size)
+    for kk in (1, 3, 5):
+        ep, flags, _ = _run(cfg, q, k, v, trigger_stride=kk)
+        assert flags[:, 0, 0].tolist() == [1 if t % kk == 0 else 0 for t in range(cfg.decode_steps)], kk
+        seg_sizes = [u.positions.size for u in ep.units(0, 0, 0)[n_prompt_units:]]
+        assert seg_sizes and all(n == kk for n in seg_sizes), (kk, seg_sizes)
