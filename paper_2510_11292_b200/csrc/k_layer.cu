@@ -690,7 +690,8 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   const int b = li / a.hn, h = li % a.hn, tid = threadIdx.x;
   extern __shared__ __align__(128) uint8_t lk_smem[];
   __shared__ __align__(16) InstState s_S;  // state before this step
-  __shared__ InstState s_post;             // after this step's store_cache (attention window only)
+  __shared__ InstState s_postv[2];         // after this step's store_cache (attention window only),
+                                           // for flag = 0 and flag = 1 (both computed while r_t resolves)
   __shared__ int2 s_fifo[32];
   __shared__ double s_cos[64];
   __shared__ double s_r;
@@ -874,7 +875,10 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
       flag = a.stride > 0 ? ((t - 1) % a.stride == 0) : ((t == 1) || (rr < a.tau));
     }
     s_flag = flag;
-    // post-store_cache window (the same seal / append / evict rules as append_one, state only)
+  } else if (tid == 32 || tid == 64) {
+    // post-store_cache window (the same seal / append / evict rules as append_one, state only), for
+    // both outcomes of the flag while thread 0 resolves r_t
+    const bool flag = tid == 64;
     InstState p = s_S;
     const int dec = p.step;
     int2 pushed = make_int2(0, 0);
@@ -906,7 +910,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
       p.fifo_count--;
       ++k;
     }
-    s_post = p;
+    s_postv[flag] = p;
   }
   prof_stamp(prof, 27);
   __syncthreads();
@@ -915,6 +919,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   if (prof && tid == 0) prof[22] = clock64();
 #endif
   const int flag = s_flag;
+  const InstState& s_post = s_postv[flag];
   if (rank == 0 && h == 0) {
     if (tid == 0) {
       a.flag[b] = (uint8_t)flag;
