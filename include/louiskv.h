@@ -54,6 +54,10 @@ enum { LOUISKV_TRIG_PREV_STEP = 0, LOUISKV_TRIG_LAST_RETRIEVAL = 1 };
 enum { LOUISKV_BOUNDARY_PER_LAYER = 0, LOUISKV_BOUNDARY_SHARED = 1 };
 enum { LOUISKV_FETCH_ZERO_COPY = 0 };
 enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
+/* prompt units: semantic k-means clusters (the method) or contiguous pages (the page units of
+ * the paper's comparison systems, §3.1 P:63 "partition the entire key cache ... into m fixed-size
+ * pages", page size 16 at P:143) */
+enum { LOUISKV_UNITS_KMEANS = 0, LOUISKV_UNITS_PAGES = 1 };
 enum { LOUISKV_ATTN_TC = 0, LOUISKV_ATTN_SIMT = 1 };
 
 typedef struct {
@@ -82,6 +86,11 @@ typedef struct {
                                 ablation ("retrieves every 5 / 16 steps"): flag = (t - 1) % k == 0;
                                 r_t is still computed and reported, segments then span k tokens.
                                 Negative: INVALID_ARG at create. */
+  int32_t prompt_units;      /* LOUISKV_UNITS_KMEANS (default) | LOUISKV_UNITS_PAGES: cluster_prompt
+                                splits [S, P) into k = ceil((P-S)/c) contiguous pages of c =
+                                avg_cluster_size tokens (the last one shorter), centroid = mean of the
+                                page's keys (fp32), no Lloyd iterations; everything downstream (offload,
+                                scoring, selection, gather) is unchanged. Other values: INVALID_ARG. */
 } louiskv_config;
 
 typedef struct {

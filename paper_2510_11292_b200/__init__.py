@@ -22,6 +22,7 @@ OK, ERR_INVALID_ARG, ERR_STATE, ERR_CAPACITY, ERR_OOM_DEVICE, ERR_OOM_HOST, ERR_
 TRIG_PREV_STEP, TRIG_LAST_RETRIEVAL = 0, 1
 BOUNDARY_PER_LAYER, BOUNDARY_SHARED = 0, 1
 KMEANS_TC, KMEANS_SIMT = 0, 1
+UNITS_KMEANS, UNITS_PAGES = 0, 1
 
 _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE", 5: "OOM_HOST", 6: "CUDA",
            7: "NOT_IMPLEMENTED"}
@@ -49,7 +50,7 @@ class Config(ctypes.Structure):
                 ("kmeans_impl", ctypes.c_int32), ("full_cache_layers", ctypes.c_uint64),
                 ("trigger_ref", ctypes.c_int32), ("boundary_mode", ctypes.c_int32), ("shared_layer", ctypes.c_int32),
                 ("max_open_segment", ctypes.c_int32), ("fetch_mode", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("attn_impl", ctypes.c_int32), ("trigger_stride", ctypes.c_int32)]
+                ("attn_impl", ctypes.c_int32), ("trigger_stride", ctypes.c_int32), ("prompt_units", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -122,7 +123,7 @@ def _stream(stream) -> Optional[int]:
 
 def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigger_ref=TRIG_PREV_STEP,
                 boundary_mode=BOUNDARY_PER_LAYER, shared_layer=0, max_open_segment=0, kmeans_impl=KMEANS_TC,
-                device=0, max_output_len=None, attn_impl=0, trigger_stride=0) -> Config:
+                device=0, max_output_len=None, attn_impl=0, trigger_stride=0, prompt_units=0) -> Config:
     """Build the C config from a synth.configs.Config-like object (plain numbers)."""
     mask = 0
     for l in cfg.full_cache_layers:
@@ -136,7 +137,8 @@ def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigge
                   tau=cfg.tau, avg_cluster_size=cfg.avg_cluster_size, kmeans_iters=cfg.kmeans_iters,
                   kmeans_impl=kmeans_impl, full_cache_layers=mask, trigger_ref=trigger_ref,
                   boundary_mode=boundary_mode, shared_layer=shared_layer, max_open_segment=max_open_segment,
-                  fetch_mode=0, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride)
+                  fetch_mode=0, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride,
+                  prompt_units=prompt_units)
 
 
 class Context:

@@ -280,6 +280,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       k.kv_head_begin + k.kv_head_count > k.num_kv_heads || k.max_batch <= 0 || k.max_prompt_len <= 0 ||
       k.max_output_len <= 0 || k.budget_tokens < 0 || k.sink_tokens < 0 || k.window_tokens < 1 ||
       k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) || k.trigger_stride < 0 ||
+      (k.prompt_units != LOUISKV_UNITS_KMEANS && k.prompt_units != LOUISKV_UNITS_PAGES) ||
       (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
     return LOUISKV_ERR_INVALID_ARG;
   const int g = k.num_q_heads / k.num_kv_heads;
@@ -510,6 +511,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.kc = kc;
   a.iters = c->iters;
   a.impl = c->cfg.kmeans_impl;
+  a.page = c->cfg.prompt_units == LOUISKV_UNITS_PAGES ? c->cfg.avg_cluster_size : 0;
   a.cent = c->d_cent + ib * c->Umax * D;
   a.centb = c->d_centb + ib * c->Umax * D;
   a.Umax = c->Umax;

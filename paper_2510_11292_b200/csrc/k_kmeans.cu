@@ -598,6 +598,14 @@ __global__ void __launch_bounds__(128) km_finalize_kernel(KmArgs a) {
   km_write_centroid(a, li, j, s, off[j + 1] - off[j], lane);
 }
 
+// page units (LOUISKV_UNITS_PAGES, §3.1): key i of [S, P) belongs to page i / page
+__global__ void km_page_kernel(KmArgs a) {
+  pdl_wait_trigger();
+  const int li = blockIdx.y;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)a.N; t += (int64_t)gridDim.x * blockDim.x)
+    a.assign[(int64_t)li * a.Nmax + t] = (int32_t)(t / a.page);
+}
+
 // caller-supplied clustering: copy assignment and centroids in
 __global__ void km_ext_kernel(KmArgs a) {
   pdl_wait_trigger();
@@ -732,6 +740,12 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
   if (a.ext_assign) {
     launch_k(km_ext_kernel, dim3(dim3(64, ni)), dim3(256), 0, st, a);
     if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
+  } else if (a.page > 0) {
+    // pages: fixed assignment, one centroid update (mean of each page's keys), no iterations
+    launch_k(km_page_kernel, dim3(dim3(64, ni)), dim3(256), 0, st, a);
+    if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
+    launch_k(km_update_kernel, dim3(dim3((a.task_max + 3) / 4, ni)), dim3(128), 0, st, a);
+    launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
   } else {
     launch_k(km_init_kernel, dim3(gk), dim3(128), 0, st, a);
     launch_k(km_half_pad_kernel, dim3(dim3(1, ni)), dim3(256), 0, st, a);

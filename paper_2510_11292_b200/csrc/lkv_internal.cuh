@@ -230,6 +230,7 @@ struct KmArgs {
   StatsDev* stats;
   const int32_t* ext_assign;   // device copy of caller-provided assignment (set_prompt_units)
   const float* ext_cent;       // device copy of caller-provided centroids
+  int page;                    // > 0: page units of `page` tokens (LOUISKV_UNITS_PAGES), no k-means
 };
 // tc_iters / simt_iters: host counters of which assignment kernel ran
 cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_iters, uint64_t* simt_iters);

@@ -452,3 +452,33 @@ def test_episode_fixed_stride_trigger():
                                          fused=fused, trigger_stride=k)
             n_ret = cfg.num_layers - len(cfg.full_cache_layers)
             assert n_flags == n_ret * cfg.batch * len(range(0, 40, k))
+
+
+@pytest.mark.parametrize("prompt_len,c", [(4096, 16), (1000 + 16, 16), (600, 7)])
+def test_page_units_device(prompt_len, c):
+    """prompt_units = PAGES (the page units of the paper's comparison systems, §3.1; SPEC
+    build_pages S:352-360): [S, P) in contiguous c-token pages (last one shorter), centroid = mean of
+    the page's keys; compared with the oracle's fp64 page means (1e-3 relative, as for k-means), and
+    the cluster-major host pool holds the positions in order."""
+    lkv = _lkv()
+    cfg = C1.replace(num_layers=1, num_kv_heads=2, num_q_heads=8, batch=2, prompt_len=prompt_len,
+                     sink_tokens=16, avg_cluster_size=c)
+    inp = make_inputs(cfg, 1, 3)
+    ctx = lkv.Context(lkv.make_config(cfg, prompt_units=lkv.UNITS_PAGES))
+    ctx.cluster_prompt(0, inp.K[0], inp.V[0])
+    S, N = cfg.sink_tokens, prompt_len - cfg.sink_tokens
+    k = -(-N // c)
+    Kall = np32(inp.K[0])
+    for bb in range(cfg.batch):
+        for hh in range(cfg.num_kv_heads):
+            cen, sizes, first = ctx.get_units(0, bb, hh)
+            assert sizes.tolist() == [c] * (k - 1) + [N - c * (k - 1)]
+            assert first.tolist() == [S + j * c for j in range(k)]
+            pos = ctx.get_unit_positions(0, bb, hh)
+            assert np.array_equal(pos, np.arange(S, prompt_len))
+            assign = (np.arange(N) // c).astype(np.int32)
+            ref = oracle.centroids_of(Kall[bb, S:, hh], assign, k).astype(np.float64)
+            rel = np.abs(cen - ref) / np.maximum(np.abs(ref), 1e-3 * np.abs(ref).max())
+            assert rel.max() < 1e-3
+    assert ctx.stats()["kmeans_tc_iters"] == 0 and ctx.stats()["kmeans_simt_iters"] == 0
+    ctx.close()

@@ -224,3 +224,21 @@ def test_fixed_stride_trigger_pattern_and_segments():
         assert flags[:, 0, 0].tolist() == [1 if t % kk == 0 else 0 for t in range(cfg.decode_steps)], kk
         seg_sizes = [u.positions.size for u in ep.units(0, 0, 0)[n_prompt_units:]]
         assert seg_sizes and all(n == kk for n in seg_sizes), (kk, seg_sizes)
+
+
+@pytest.mark.parametrize("n,p,sizes", [(10, 4, [4, 4, 2]), (32, 16, [16, 16]), (1, 16, [1])])
+def test_page_units_spec_examples(n, p, sizes):
+    """SPEC build_pages (paper §3.1 P:63 fixed-size pages, page size 16 at P:143): n
+    positions in consecutive pages of p (last one short), each centroid the mean of its keys."""
+    cfg = tiny_cfg(prompt_len=n + 4, sink_tokens=4, avg_cluster_size=p)
+    K, V = _prompt(cfg, 3)
+    ep = OracleEpisode(cfg)
+    assign = np.broadcast_to((np.arange(n) // p).astype(np.int32), (1, 1, n)).copy()
+    ep.cluster_prompt(0, K, V, assign=assign)
+    units = ep.units(0, 0, 0)
+    assert [u.positions.size for u in units] == sizes
+    start = 4
+    for u, sz in zip(units, sizes):
+        assert u.positions.tolist() == list(range(start, start + sz))
+        np.testing.assert_allclose(u.centroid, K[0, start:start + sz, 0].astype(np.float64).mean(0), rtol=0, atol=1e-6)
+        start += sz

@@ -6,8 +6,8 @@ side needs the paper's models and datasets).
 Variants (all on louiskv_decode_layer, graph-replayed 32-layer steps, device-resident inputs):
   * semantic boundary trigger (SR) at tau in {0.5, 0.7, 0.85 (C2), 0.95}, and tau = 2 (per-token);
   * fixed-stride retrieval every 5 / 16 steps (trigger_stride, P:446);
-  * page units instead of k-means clusters (the prompt split into contiguous 16-token pages with
-    mean-key centroids, supplied through louiskv_set_prompt_units), semantic trigger at tau = 0.85.
+  * page units instead of k-means clusters (prompt_units = PAGES: the prompt split on the device into
+    contiguous 16-token pages with mean-key centroids), semantic trigger at tau = 0.85.
 usage: python tools/ablation.py [--steps 96] > profiles/r01_ablation.json
 """
 import argparse, json, os, sys
@@ -31,37 +31,17 @@ VARIANTS = [("SR tau=0.5", 0.5, 0, "kmeans"), ("SR tau=0.7", 0.7, 0, "kmeans"), 
             ("pages of 16, SR tau=0.85", 0.85, 0, "pages")]
 
 
-def page_units(cfg, K):
-    """contiguous pages of c tokens over [S, P) with mean-key centroids (the Quest-style unit)."""
-    S, P, c = cfg.sink_tokens, cfg.prompt_len, cfg.avg_cluster_size
-    N = P - S
-    k = -(-N // c)
-    b, hn = K.shape[0], K.shape[2]
-    assign = np.broadcast_to((np.arange(N) // c).astype(np.int32), (b, hn, N)).copy()
-    Kf = K[:, S:].float().permute(0, 2, 1, 3)  # [b, hn, N, d]
-    pad = k * c - N
-    if pad:
-        Kf = torch.cat([Kf, torch.zeros(b, hn, pad, Kf.shape[-1], device=Kf.device)], dim=2)
-    cnt = torch.full((k,), float(c), device=Kf.device)
-    cnt[-1] = c - pad
-    cen = Kf.reshape(b, hn, k, c, -1).sum(3) / cnt[None, None, :, None]
-    return assign, cen.cpu().numpy().astype(np.float32)
-
-
 res = []
 for name, tau, stride, units in VARIANTS:
     cfg = base.replace(tau=tau)
     L, full = cfg.num_layers, set(cfg.full_cache_layers)
     T = 2 + 8 + args.steps
-    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=T + 1, trigger_stride=stride))
+    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=T + 1, trigger_stride=stride,
+                                      prompt_units=lkv.UNITS_PAGES if units == "pages" else lkv.UNITS_KMEANS))
     plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
     for l in range(L):
         K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
-        if units == "pages" and l not in full:
-            a, cen = page_units(cfg, K)
-            ctx.set_prompt_units(l, K, V, a, cen)
-        else:
-            ctx.cluster_prompt(l, K, V)
+        ctx.cluster_prompt(l, K, V)
         del K, V
     ctx.prompt_fence()
     q, kk, vv, _ = synth.decode_stream(cfg, T, 0, dev, plants)
