@@ -588,6 +588,11 @@ def main():
         "retrievals_per_step": retrievals / K / max(n_ret_layers, 1) / b,
         "stats_timed": {k_: st_b[k_] - st_a[k_] for k_ in st_b},
         "host_link_h2d_gbs": host_link_gbs,
+        "memory": dict(ctx.memory(), full_kv_bytes=b * hc * L * (cfg.prompt_len + T) * 512,
+                       note="device_bytes: every device allocation of the context (sinks, working sets, local "
+                            "buffers, centroids, unit tables, the two full-cache layers, scratch); full_kv_bytes: "
+                            "the K+V bf16 of every layer at P + max decode steps (a full-cache engine's device "
+                            "footprint); the offloaded rows live in the pinned host pool (P:404-425)"),
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -222,6 +222,11 @@ louiskv_status louiskv_get_unit_positions(louiskv_ctx* ctx, int32_t layer, int32
 louiskv_status louiskv_get_working_set(louiskv_ctx* ctx, int32_t layer, int32_t b, int32_t h,
                                        uint16_t* k_rows, uint16_t* v_rows, int32_t cap, int32_t* n_rows);
 louiskv_status louiskv_get_stats(louiskv_ctx* ctx, louiskv_stats* out);
+/* Memory held by the context (the paper's memory comparison, Table 3 / P:404-425): device bytes
+ * of every device allocation made at create (sinks, working sets, local buffers, centroids, unit
+ * tables, full-cache layers, scratch) and the pinned host-pool bytes. Either pointer may be NULL.
+ * No synchronisation. Errors: INVALID_ARG (null ctx). */
+louiskv_status louiskv_get_memory(const louiskv_ctx* ctx, uint64_t* device_bytes, uint64_t* host_pool_bytes);
 const char* louiskv_last_error(const louiskv_ctx* ctx);
 /* Library build string (arch, version). */
 const char* louiskv_version(void);

@@ -32,7 +32,7 @@ SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louis
            "louiskv_should_retrieve", "louiskv_retrieve", "louiskv_append_output", "louiskv_sparse_attn",
            "louiskv_append_attn", "louiskv_decode_layer",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
-           "louiskv_get_stats", "louiskv_last_error", "louiskv_version"]
+           "louiskv_get_stats", "louiskv_get_memory", "louiskv_last_error", "louiskv_version"]
 
 
 class LouisKVError(RuntimeError):
@@ -91,6 +91,7 @@ def lib():
         L.louiskv_get_unit_positions.argtypes = [vp, i32, i32, i32, vp, i64, ctypes.POINTER(ctypes.c_int64)]
         L.louiskv_get_working_set.argtypes = [vp, i32, i32, i32, vp, vp, i32, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+        L.louiskv_get_memory.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
         L.louiskv_last_error.argtypes = [vp]
         L.louiskv_last_error.restype = ctypes.c_char_p
         L.louiskv_version.restype = ctypes.c_char_p
@@ -252,6 +253,12 @@ class Context:
         self._chk(self._L.louiskv_get_working_set(self.h, layer, b, h, K.ctypes.data, V.ctypes.data, cap,
                                                   ctypes.byref(n)))
         return K[:n.value].copy(), V[:n.value].copy()
+
+    def memory(self) -> dict:
+        """Device bytes allocated by the context and pinned host-pool bytes (louiskv_get_memory)."""
+        d, h = ctypes.c_uint64(), ctypes.c_uint64()
+        self._chk(self._L.louiskv_get_memory(self.h, ctypes.byref(d), ctypes.byref(h)))
+        return {"device_bytes": d.value, "host_pool_bytes": h.value}
 
     def stats(self) -> dict:
         s = Stats()

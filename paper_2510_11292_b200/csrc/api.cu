@@ -81,6 +81,7 @@ struct louiskv_ctx {
   std::vector<cudaEvent_t> ev_done;  // [L] offload of layer l complete
   std::vector<char> off_pending;     // [L] a decode-path stream has not yet waited on ev_done[l]
   std::vector<void*> allocs;
+  uint64_t dev_bytes = 0, host_bytes = 0;  // louiskv_get_memory
   std::string err;
   bool sticky = false;
 };
@@ -106,6 +107,7 @@ bool dalloc(louiskv_ctx* c, T** p, size_t n) {
   if (cudaMalloc(&v, n * sizeof(T)) != cudaSuccess) return false;
   cudaMemset(v, 0, n * sizeof(T));
   c->allocs.push_back(v);
+  c->dev_bytes += n * sizeof(T);
   *p = reinterpret_cast<T*>(v);
   return true;
 }
@@ -405,6 +407,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       return LOUISKV_ERR_OOM_HOST;
     }
     c->h_pool = reinterpret_cast<uint8_t*>(hp);
+    c->host_bytes = pool_bytes;
     void* dp = nullptr;
     if (cudaHostGetDevicePointer(&dp, hp, 0) != cudaSuccess) {
       louiskv_destroy(c);
@@ -846,6 +849,13 @@ louiskv_status louiskv_get_working_set(louiskv_ctx* c, int32_t layer, int32_t b,
   if (k_rows && m) cudaMemcpy(k_rows, K, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
   if (v_rows && m) cudaMemcpy(v_rows, V, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
   if (n_rows) *n_rows = is.ws_rows;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_memory(const louiskv_ctx* c, uint64_t* device_bytes, uint64_t* host_pool_bytes) {
+  if (!c) return LOUISKV_ERR_INVALID_ARG;
+  if (device_bytes) *device_bytes = c->dev_bytes;
+  if (host_pool_bytes) *host_pool_bytes = c->host_bytes;
   return LOUISKV_OK;
 }
 

@@ -482,3 +482,18 @@ def test_page_units_device(prompt_len, c):
             assert rel.max() < 1e-3
     assert ctx.stats()["kmeans_tc_iters"] == 0 and ctx.stats()["kmeans_simt_iters"] == 0
     ctx.close()
+
+
+def test_memory_accounting():
+    """louiskv_get_memory (the memory side of the method): the pinned pool holds every
+    retrieval instance's offloadable rows (P - S prompt rows + max_output_len, 512 B each); the device
+    footprint at C2 shape is far below the full K+V of every layer."""
+    lkv = _lkv()
+    cfg = C2.replace(num_layers=16, full_cache_layers=(0,))
+    ctx = lkv.Context(lkv.make_config(cfg, max_output_len=64))
+    m = ctx.memory()
+    n_ret = (cfg.num_layers - 1) * cfg.batch * cfg.num_kv_heads
+    assert m["host_pool_bytes"] >= n_ret * (cfg.prompt_len - cfg.sink_tokens) * 512
+    full_kv = cfg.num_layers * cfg.batch * cfg.num_kv_heads * (cfg.prompt_len + 64) * 512
+    assert 0 < m["device_bytes"] < 0.6 * full_kv, (m, full_kv)
+    ctx.close()
