@@ -682,8 +682,13 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   unsigned long long* prof = nullptr;
 #endif
   prof_stamp(prof, 0);
-  pdl_wait_trigger();
-  prof_stamp(prof, 1);
+  // early: the previous kernel is ANOTHER layer's layer kernel (host-tracked, LayerArgs::early), so
+  // this layer's own state — instance state, q_ref, working set, local buffer, sinks, unit tables —
+  // was last written by a kernel that completed before that one passed its own wait: the prologue
+  // below reads it before this kernel's wait and overlaps the previous layer. The step's inputs
+  // (q_t, k_t, v_t: in a model, produced upstream) are read only after the wait.
+  const bool early = A.early != 0;
+  if (!early) pdl_wait_trigger();
   const RetrieveArgs& a = A.r;
   const AppendArgs& app = A.at.app;
   const int li = blockIdx.x / AT_CL, rank = blockIdx.x % AT_CL;
@@ -703,8 +708,8 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   __shared__ int s_own_dst[LK_REP_N / AT_CL];
   InstState* S = a.inst + li;
 
-  // ---- 1. loads: the instance state and (Hq <= 32) the trigger operands: q_t and BOTH q_ref
-  // buffers, so no load waits for the step parity
+  // ---- 1. prologue: the instance state and (Hq <= 32) BOTH q_ref buffers (so no load waits for the
+  // step parity), the L2 prefetch of the retrieval operands and the speculative attention loads
   if (tid < 4) reinterpret_cast<uint4*>(&s_S)[tid] = reinterpret_cast<const uint4*>(S)[tid];
   const int l8 = tid & 7, hh = tid >> 3;
   const bool fast_trig = !a.shared_copy && a.Hq <= AT_THREADS / 8;
@@ -712,17 +717,9 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   const uint4* qc4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b);
   const uint4* qr4[2] = {reinterpret_cast<const uint4*>(a.qref + ((int64_t)0 * a.Bmax + b) * a.Hq * D),
                          reinterpret_cast<const uint4*>(a.qref + ((int64_t)1 * a.Bmax + b) * a.Hq * D)};
-  // the owned heads' q as the attention MMA's A fragments (used at the end; loaded now)
-  uint32_t qa[8][2];
-  mma_q_frags<G>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)(a.h0 + h) * G * D, qa);
   uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0, r00 = c0, r01 = c0, r10 = c0, r11 = c0;
   uint4 nv = c0;  // (last rank, threads < 32) the new token's K / V row pieces, for the attention
-  if (rank == AT_CL - 1 && tid < 32)
-    nv = reinterpret_cast<const uint4*>((tid < 16 ? A.at.app.k_t : A.at.app.v_t) + (int64_t)b * A.at.app.stride_b +
-                                        (int64_t)h * D)[tid & 15];
   if (act) {
-    c0 = qc4[hh * 16 + l8];
-    c1 = qc4[hh * 16 + l8 + 8];
     r00 = qr4[0][hh * 16 + l8];
     r01 = qr4[0][hh * 16 + l8 + 8];
     r10 = qr4[1][hh * 16 + l8];
@@ -794,7 +791,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
                                ws_r1 - ws_r0, sup_head, sup_n);
   int npre = min((pl.rows + am::CHUNK - 1) / am::CHUNK, am::STAGES - 1);
   for (int c = 0; c < npre; ++c) {
-    attn_load_chunk(pl, c, nv);
+    attn_load_chunk(pl, c, nv, /*with_new=*/false);  // (the new token's row: after the wait)
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   prof_stamp(prof, 25);
@@ -807,6 +804,20 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   // speculative attention loads above have landed. (Every rank's reads of the instance state are
   // ordered before the appending rank's commit by the merge barrier, which every rank passes first.)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+
+  // ---- the step's inputs, after the grid-dependency wait
+  if (early) pdl_wait_trigger();
+  prof_stamp(prof, 1);
+  uint32_t qa[8][2];  // the owned heads' q as the attention MMA's A fragments (used at the end)
+  mma_q_frags<G>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)(a.h0 + h) * G * D, qa);
+  if (rank == AT_CL - 1 && tid < 32)
+    nv = reinterpret_cast<const uint4*>((tid < 16 ? A.at.app.k_t : A.at.app.v_t) + (int64_t)b * A.at.app.stride_b +
+                                        (int64_t)h * D)[tid & 15];
+  if (act) {
+    c0 = qc4[hh * 16 + l8];
+    c1 = qc4[hh * 16 + l8 + 8];
+  }
+  for (int c = 0; c < npre; ++c) attn_store_new_row(pl, c, nv);
 
   // ---- 2. trigger r_t (recipe R1), identical on every rank: 8 lanes per head, lane l8 sums dims
   // [8 l8, 8 l8 + 8) and [8 l8 + 64, 8 l8 + 72) sequentially, adds them (the tree's first level),

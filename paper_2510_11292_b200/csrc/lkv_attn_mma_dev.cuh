@@ -76,7 +76,9 @@ struct AttnPlan {
 // t % 16 of rows t/16 + 16m (m < 4), K and V (rows past the end zero-filled). The new-token row is
 // not copied: threads t < 32 of the owning CTA store `nv` (K piece t for t < 16, V piece t - 16) —
 // the row held in registers since entry. Every thread calls; the caller commits the group.
-__device__ __forceinline__ void attn_load_chunk(const AttnPlan& pl, const int c, const uint4 nv) {
+__device__ __forceinline__ void attn_store_new_row(const AttnPlan& pl, const int c, const uint4 nv);
+__device__ __forceinline__ void attn_load_chunk(const AttnPlan& pl, const int c, const uint4 nv,
+                                                const bool with_new = true) {
   using namespace am;
   extern __shared__ __align__(128) uint8_t at_smem[];
   const int tid = threadIdx.x, j = tid & 15;
@@ -108,6 +110,16 @@ __device__ __forceinline__ void attn_load_chunk(const AttnPlan& pl, const int c,
     cp16(dst + swz(r, j), ks, bytes);
     cp16(dst + 2 * HALF + swz(r, j), vs, bytes);
   }
+  if (with_new) attn_store_new_row(pl, c, nv);
+}
+
+// The new token's row of chunk c (if it falls in it), from registers: threads t < 32 of the owning
+// CTA store `nv` (K piece t for t < 16, V piece t - 16) into the chunk's stage.
+__device__ __forceinline__ void attn_store_new_row(const AttnPlan& pl, const int c, const uint4 nv) {
+  using namespace am;
+  extern __shared__ __align__(128) uint8_t at_smem[];
+  const int tid = threadIdx.x, j = tid & 15;
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(at_smem) + (c % STAGES) * STAGE;
   if (pl.new_vr >= c * CHUNK && pl.new_vr < (c + 1) * CHUNK && tid < 32) {
     const uint32_t sdst = dst + (tid >> 4) * 2 * HALF + swz(pl.new_vr - c * CHUNK, j);
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sdst), "r"(nv.x), "r"(nv.y), "r"(nv.z), "r"(nv.w)

@@ -180,6 +180,9 @@ struct LayerArgs {
   RetrieveArgs r;
   AttnArgs at;  // fused = 1, at.app = the append arguments
   int layer;    // (LKV_PROF builds: timestamp rows of this layer)
+  int early;    // 1: the previous kernel in the stream is another layer's layer kernel, so this layer's own
+                // state (written only by kernels that completed before that one passed its wait) may be
+                // read before griddepcontrol.wait — the prologue overlaps the previous layer
 };
 constexpr int PROF_SLOTS = 32;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
 // the single launch handles instances with at most LAYER_REP_UNITS units and at most LAYER_REP_SEL
