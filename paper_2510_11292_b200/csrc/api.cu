@@ -82,6 +82,7 @@ struct louiskv_ctx {
   std::vector<char> off_pending;     // [L] a decode-path stream has not yet waited on ev_done[l]
   std::vector<void*> allocs;
   int last_layer = -1;  // layer of the last launch when it was a one-launch layer step, else -1
+  void* last_stream = nullptr;  // ... and the stream it went to
   uint64_t dev_bytes = 0, host_bytes = 0;  // louiskv_get_memory
   std::string err;
   bool sticky = false;
@@ -709,7 +710,8 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
     return fail(c, LOUISKV_ERR_INVALID_ARG, "decode_layer: bad args");
   const void* q_own = reinterpret_cast<const bf16*>(q_all) + (int64_t)c->h0 * c->g * D;
   // the previous launch on this context was another layer's one-launch step: PDL-early prologue allowed
-  const int early = (c->last_layer >= 0 && c->last_layer != layer) ? 1 : 0;
+  // (same stream only: PDL orders a kernel after its predecessor in its own stream)
+  const int early = (c->last_layer >= 0 && c->last_layer != layer && c->last_stream == stream) ? 1 : 0;
   if (is_full(c, layer) && c->cfg.attn_impl != LOUISKV_ATTN_SIMT) {
     // full-cache layer: ONE launch — flags 0, store_cache of (k_t, v_t), dense attention, step commit
     if (c->P[layer] < 0) return fail(c, LOUISKV_ERR_STATE, "decode_layer before cluster_prompt");
@@ -724,6 +726,7 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
     const cudaError_t e = launch_attn_full_tc(a, c->inst_per_layer, st, &fs);
     if (e == cudaSuccess) {
       c->last_layer = layer;
+      c->last_stream = stream;
       c->t[layer] += 1;
       c->stage[layer] = 3;
       return LOUISKV_OK;
@@ -763,6 +766,7 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
   la.early = early;
   LKV_LAUNCH(c, launch_layer(la, st), "decode_layer");
   c->last_layer = layer;
+  c->last_stream = stream;
   c->t[layer] = t;
   c->stage[layer] = 3;
   return LOUISKV_OK;

@@ -497,3 +497,79 @@ def test_memory_accounting():
     full_kv = cfg.num_layers * cfg.batch * cfg.num_kv_heads * (cfg.prompt_len + 64) * 512
     assert 0 < m["device_bytes"] < 0.6 * full_kv, (m, full_kv)
     ctx.close()
+
+
+def test_graph_replay_parity_with_early_prologue():
+    """The bench's execution mode, checked against the oracle: every step is ONE CUDA-graph replay of
+    louiskv_decode_layer over all layers (no host sync between layers), so consecutive layer kernels
+    overlap through programmatic dependent launch and each retrieval layer runs its own-state
+    prologue before its grid-dependency wait. Flags, r_t and outputs of every layer are compared
+    after every replay (selections through the working set only at the end)."""
+    lkv = _lkv()
+    cfg = small_cfg(num_layers=5, full_cache_layers=(0,), decode_steps=24)
+    inp = make_inputs(cfg, 24, 12)
+    L, b, hn, g = cfg.num_layers, cfg.batch, cfg.num_kv_heads, cfg.group
+    ctx = lkv.Context(lkv.make_config(cfg))
+    ep = OracleEpisode(cfg)
+    for l in range(L):
+        Kn, Vn = np32(inp.K[l]), np32(inp.V[l])
+        if l in cfg.full_cache_layers:
+            ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+            ep.cluster_prompt(l, Kn, Vn)
+        else:
+            a = planted_assign(cfg, inp.labels[l])
+            ep.cluster_prompt(l, Kn, Vn, assign=a)
+            cen = np.stack([[np.stack([u.centroid for u in ep.units(l, bb, hh)]) for hh in range(hn)]
+                            for bb in range(b)])
+            ctx.set_prompt_units(l, inp.K[l], inp.V[l], a, cen)
+    q_in = torch.empty_like(inp.q[0]).contiguous()
+    k_in = torch.empty_like(inp.k[0]).contiguous()
+    v_in = torch.empty_like(inp.v[0]).contiguous()
+    out = torch.zeros((L, b, g * hn, 128), dtype=torch.bfloat16, device="cuda")
+    out32 = torch.zeros((L, b, g * hn, 128), dtype=torch.float32, device="cuda")
+    flags = torch.zeros((L, b), dtype=torch.uint8, device="cuda")
+    rr = torch.zeros((L, b), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+
+    def issue():
+        for l in range(L):
+            ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], out32[l], flags[l], rr[l], stream=s)
+
+    def oracle_step(t):
+        res = []
+        for l in range(L):
+            f, r = ep.should_retrieve(l, np32(inp.q[t, l]))
+            ep.retrieve(l, np32(inp.q[t, l]))
+            ep.append_output(l, np32(inp.k[t, l]), np32(inp.v[t, l]))
+            res.append((f, r, ep.sparse_attn(l, np32(inp.q[t, l]))))
+        return res
+
+    def check(t):
+        torch.cuda.synchronize()
+        for l, (f, r, o) in enumerate(oracle_step(t)):
+            assert np.array_equal(flags[l].cpu().numpy().astype(np.int32), f), (t, l)
+            if l not in cfg.full_cache_layers:
+                assert np.array_equal(rr[l].cpu().numpy().view(np.uint64), r.view(np.uint64)), (t, l)
+            err = np.abs(out32[l].cpu().numpy().astype(np.float64) - o).max()
+            assert err < ATTN_TOL, (t, l, err)
+
+    ctx.prompt_fence(stream=s)
+    with torch.cuda.stream(s):
+        q_in.copy_(inp.q[0]); k_in.copy_(inp.k[0]); v_in.copy_(inp.v[0])
+        issue()
+    check(0)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        issue()
+    for t in range(1, 24):
+        with torch.cuda.stream(s):
+            q_in.copy_(inp.q[t]); k_in.copy_(inp.k[t]); v_in.copy_(inp.v[t])
+            graph.replay()
+        check(t)
+    for l in range(L):
+        if l in cfg.full_cache_layers:
+            continue
+        for bb in range(b):
+            for hh in range(hn):
+                assert np.array_equal(ctx.get_selection(l, bb, hh), np.array(ep.selection(l, bb, hh), np.int32))
+    ctx.close()
