@@ -476,6 +476,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
                                     int64_t st_, int64_t sh, int32_t batch, int64_t P, int32_t n_clusters,
                                     const int32_t* h_assign, const float* h_cent, void* stream) {
   LKV_CHECK_CTX(c);
+  c->last_layer = -1;  // (prefill kernels follow: no early prologue for the next decode launch)
   if (layer < 0 || layer >= c->L || !k || !v || batch <= 0 || batch > c->Bmax || P < 0 || P > c->Pmax)
     return fail(c, LOUISKV_ERR_INVALID_ARG, "cluster_prompt: bad layer/pointer/batch/prompt_len");
   if (c->batch != 0 && batch != c->batch)
