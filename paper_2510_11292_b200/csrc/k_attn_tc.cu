@@ -79,6 +79,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
+// streaming variant: the full cache is read once per step (272 MB > L2), so its lines are marked
+// evict-first and do not push the retrieval layers' reused data (working sets, centroids, host rows
+// cached in L2) out of the 126 MB L2
+__device__ __forceinline__ void cp16_stream(uint32_t dst, const void* src, bool valid, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0), "l"(pol)
+               : "memory");
+}
 
 struct FullArgs {
   const bf16* full;  // layer base [n_inst][K|V][full_cap][D]
@@ -161,6 +169,10 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
       if (a.r_out) a.r_out[tid] = 0.0;
     }
   }
+#ifndef LKV_FA_NO_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
   auto load = [&](int c) {  // cp.async path: every thread copies 16 of the chunk's 2048 16-B pieces
     const int st = c % STAGES;
     const uint32_t dst = su32(smem + st * STAGE_BYTES);
@@ -171,7 +183,11 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
       const int kv = i >> 10, r = (i >> 4) & (CHUNK - 1), j = i & 15;
       const bool ok = y + r < n_rows;
       const bf16* src = (kv ? vbase : kbase) + (int64_t)(ok ? y + r : 0) * D + j * 8;
+#ifndef LKV_FA_NO_EVICT_FIRST
+      cp16_stream(dst + kv * 2 * BOX_BYTES + swz(r, j), src, ok, pol);
+#else
       cp16(dst + kv * 2 * BOX_BYTES + swz(r, j), src, ok);
+#endif
     }
   };
   if (LDGSTS) {
