@@ -241,7 +241,8 @@ int lko_select_greedy(const float* A, const int* sizes, int n, long long B, int*
 /*   mode 1 (bf16 operand, mirrors the GPU's declared precision, R-AMB10):     */
 /*          dist = ||x||^2 - 2 x·bf16(c) + ||c||^2 (fp64, ||c|| of fp32 c).    */
 /* (ii) repair empty clusters (R-AMB9): E = empty ids ascending; for each      */
-/*   E[r] in order pick the point with the largest dmin (ties -> lower index)  */
+/*   E[r] in order pick the point with the largest max(dmin, 0) (ties -> lower */
+/*   index)                                                                    */
 /*   among points whose cluster has >= 2 members at pick time and that were   */
 /*   not picked before; move it to E[r].                                       */
 /* (iii) c_j = mean of members in fp64, stored fp32.                           */
@@ -318,7 +319,9 @@ int lko_kmeans(const float* X, int N, int d, int k, int iters, int mode, int* as
       int donor = -1;
       for (int i = 0; i < N; ++i) {
         if (picked[i] || counts[assign[i]] < 2) continue;
-        if (donor < 0 || dmin[i] > dmin[donor]) donor = i;
+        /* donor key = max(dmin, 0): a squared distance is >= 0; a negative mode-1 value is a
+           rounding artefact of the expanded form (reading R-AMB9) */
+        if (donor < 0 || fmax(dmin[i], 0.0) > fmax(dmin[donor], 0.0)) donor = i;
       }
       if (donor < 0) break; /* cannot happen for k <= N */
       counts[assign[donor]]--;
