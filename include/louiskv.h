@@ -61,7 +61,9 @@ enum { LOUISKV_UNITS_KMEANS = 0, LOUISKV_UNITS_PAGES = 1 };
 enum { LOUISKV_ATTN_TC = 0, LOUISKV_ATTN_SIMT = 1 };
 
 typedef struct {
-  int32_t num_layers, num_q_heads, num_kv_heads, head_dim; /* head_dim must be 128 */
+  int32_t num_layers, num_q_heads, num_kv_heads, head_dim; /* head_dim must be 128; num_q_heads <= 64;
+                                                              g = num_q_heads/num_kv_heads in {1,2,4,8};
+                                                              num_layers <= 64 */
   int32_t kv_head_begin, kv_head_count;                    /* KV-head shard owned by this ctx */
   int32_t max_batch;
   int64_t max_prompt_len, max_output_len;                  /* fix every capacity at create */
@@ -192,10 +194,13 @@ louiskv_status louiskv_append_attn(louiskv_ctx* ctx, int32_t layer, const void* 
  * store_cache, attention), identical in results to should_retrieve -> retrieve ->
  * append_output -> sparse_attn with q_own = q_all + kv_head_begin*g*d (same stride). On a
  * retrieval layer it is ONE clustered launch (8 CTAs per (b, owned head)): every rank recomputes
- * r_t (recipe R1), the flagged instances score and select with their units split over the 8
- * ranks (histograms and minima exchanged through distributed shared memory), the ranks gather
- * the new working set, rank 0 appends, all ranks attend one split each. Instances with more than
- * 16384 units, and full-cache layers, issue the multi-kernel sequence instead. Arguments: q_all
+ * r_t (recipe R1), the flagged instances score with their units split over the 8 ranks and every
+ * rank runs the budgeted selection on the replicated scores (exchanged through distributed shared
+ * memory; instances with more than 8192 LIVE units keep the per-unit select arrays in global
+ * scratch instead — same launch, decided on the device per step), the ranks gather the new working
+ * set, the last rank appends, all ranks attend one split each. A full-cache layer is one launch
+ * too (dense attention with the store_cache fused). Budgets with min(B, unit capacity) > 1024
+ * issue the multi-kernel sequence instead. Arguments: q_all
  * as in should_retrieve (stride_q), k_t/v_t as in append_output (stride_kv), out/out_f32 as in
  * sparse_attn, d_flag_out/d_r_out optional device outputs as in should_retrieve.
  * Errors: INVALID_ARG, STATE (as should_retrieve), CUDA. */

@@ -280,7 +280,8 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   if (!cfg || !out) return LOUISKV_ERR_INVALID_ARG;
   *out = nullptr;
   const louiskv_config& k = *cfg;
-  if (k.head_dim != D || k.num_layers <= 0 || k.num_layers > 64 || k.num_q_heads <= 0 || k.num_kv_heads <= 0 ||
+  if (k.head_dim != D || k.num_layers <= 0 || k.num_layers > 64 || k.num_q_heads <= 0 || k.num_q_heads > 64 ||
+      k.num_kv_heads <= 0 ||
       k.num_q_heads % k.num_kv_heads != 0 || k.kv_head_begin < 0 || k.kv_head_count <= 0 ||
       k.kv_head_begin + k.kv_head_count > k.num_kv_heads || k.max_batch <= 0 || k.max_prompt_len <= 0 ||
       k.max_output_len <= 0 || k.budget_tokens < 0 || k.sink_tokens < 0 || k.window_tokens < 1 ||
@@ -734,8 +735,8 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
     }
     if (e != cudaErrorNotSupported) return cuda_fail(c, e, "full-cache step (tensor cores)");
   }
-  if (is_full(c, layer) || c->Umax > LAYER_REP_UNITS || std::min(c->Umax, c->Bud) > LAYER_REP_SEL) {
-    // full-cache layer (step kernel + attention), or an instance too large for the single launch
+  if (is_full(c, layer) || std::min(c->Umax, c->Bud) > LAYER_REP_SEL || c->Hq > 64) {
+    // full-cache layer (SIMT attention), or a budget / head count beyond the single launch
     louiskv_status s = louiskv_should_retrieve(c, layer, q_all, stride_q, d_flag_out, d_r_out, stream);
     if (s == LOUISKV_OK) s = louiskv_retrieve(c, layer, q_own, stride_q, stream);
     if (s == LOUISKV_OK) s = louiskv_append_attn(c, layer, k_t, v_t, stride_kv, q_own, stride_q, out, out_f32, stream);

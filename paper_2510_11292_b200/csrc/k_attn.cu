@@ -49,12 +49,12 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? 2 : 1) attn_kernel(AttnAr
 
 template <int G>
 static cudaError_t launch_attn_g(const AttnArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    cudaFuncSetAttribute(attn_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ea = once_per_device(attr, [] {
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    return e != cudaSuccess ? e : cudaFuncSetAttribute(attn_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+  });
+  if (ea != cudaSuccess) return ea;
   if (!a.fused) return launch_k(attn_kernel<G, false>, dim3(a.batch * a.hn, a.splits), dim3(AT_THREADS), AT_SMEM, st, a);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.batch * a.hn * AT_CL);

@@ -437,13 +437,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // k_kmeans_tc.cu
 template <int G>
 static cudaError_t launch_full_tc_g(const CUtensorMap& tm, const fa::FullArgs& fa_args, int n_inst, int splits,
                                     cudaStream_t st) {
-  static bool attr = false;
+  static std::atomic<uint64_t> attr{0};
   static const bool tma = getenv("LOUISKV_FA_TMA") != nullptr;  // (load-path experiment)
-  if (!attr) {
-    cudaFuncSetAttribute(fa::attn_full_tc_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
-    cudaFuncSetAttribute(fa::attn_full_tc_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
-    attr = true;
-  }
+  cudaError_t ea = once_per_device(attr, [] {
+    cudaError_t e = cudaFuncSetAttribute(fa::attn_full_tc_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
+    return e != cudaSuccess ? e : cudaFuncSetAttribute(fa::attn_full_tc_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
+  });
+  if (ea != cudaSuccess) return ea;
   if (tma)
     return launch_k(fa::attn_full_tc_kernel<G, false>, dim3(n_inst, splits), dim3(fa::THREADS), fa::SMEM, st, tm,
                     fa_args);

@@ -728,13 +728,14 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
     launch_k(reset_insts_kernel, dim3((ni + 127) / 128), dim3(128), 0, st, a.inst, ni, P, s_eff);
     return cudaGetLastError();
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(km_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(km_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(km_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ea = once_per_device(attr, [] {
+    cudaError_t e = cudaFuncSetAttribute(km_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(km_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(km_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return e;
+  });
+  if (ea != cudaSuccess) return ea;
   const int nchunk = (a.N + KM_CHUNK - 1) / KM_CHUNK;
   const dim3 gk((a.kc + 3) / 4, ni);
   if (a.ext_assign) {

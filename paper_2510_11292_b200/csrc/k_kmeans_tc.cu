@@ -467,11 +467,11 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st) {
   p.dmin = a.dmin;
   p.Nmax = a.Nmax;
   p.hn = a.hn;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::kmeans_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ea = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(tc::kmeans_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+  });
+  if (ea != cudaSuccess) return ea;
   int sms = 148;
   int dev = 0;
   cudaGetDevice(&dev);

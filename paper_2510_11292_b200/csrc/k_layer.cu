@@ -55,11 +55,16 @@ __device__ __forceinline__ int lk_scan(int v, int* s_warp, int& total) {
 
 __device__ __forceinline__ int clamp16(int sz) { return sz > 0xFFFF ? 0xFFFF : sz; }
 
-// ---------------------------------------------------------------- replicated select (n <= LK_REP_N)
+// ---------------------------------------------------------------- replicated select
 // Every rank scores its 1/8 of the units, pushes its A bits to all ranks (DSMEM stores), and then
 // runs the whole greedy selection locally on the replicated keys: three cluster barriers in total
 // (max, normaliser, keys) and every rank knows the complete new layout.
-constexpr int LK_REP_N = LAYER_REP_UNITS;  // units per instance
+// Instances with more than LK_REP_N live units (long outputs: every evicted segment is a unit) run
+// the same code with the A bits, sizes, own logits and own destinations in per-instance global
+// scratch ("big" mode: each rank writes its own range once, the cluster barrier publishes it) and
+// only the taken bits and the work lists in shared memory; the dispatch is on the LIVE unit count
+// read from the instance state, so one launch serves every step of a long generation.
+constexpr int LK_REP_N = LAYER_REP_UNITS;  // units per instance held in shared memory
 constexpr int LK_REP_SEL = LAYER_REP_SEL;  // selected units (<= min(n, B))
 // shared-memory regions of the replicated select (bytes, by n): RA [0, 4n) | SZ [4n, 6n) | TK bits |
 // X (the rest of the idle attention staging area): own logits E, then the radix candidate lists,
@@ -91,22 +96,39 @@ __device__ __forceinline__ unsigned long long rep_key(const uint32_t* RA, int u)
   return ((unsigned long long)(~RA[u]) << 16) | (unsigned)u;
 }
 
-// Returns the row count of the new working set; *nsel = selected units (LIST entries); own_dst[i] =
-// destination row of own unit lo+i (-1: not selected) for the deferred sel/seloff update.
+// big-mode global scratch of instance li (inside the retrieve scratch: [nl][Umax * 26] bytes):
+// A bits [Umax] u32 | sizes [Umax] u16 | own destinations [Umax] i32
+__device__ __forceinline__ uint8_t* big_scratch(const RetrieveArgs& a, int li) {
+  return a.scratch_sort + (int64_t)li * a.Umax * 26;
+}
+// shared-memory offset of the work region X (after the on-chip select arrays)
+__device__ __forceinline__ int rep_x_offset(int n, bool big) {
+  return big ? ((((n + 31) / 32) * 4 + 15) & ~15) : rep_off_x(n);
+}
+
+// Returns the row count of the new working set; *nsel = selected units (LIST entries, at shared
+// offset rep_x_offset(n, big)); own_dst[i] = destination row of own unit lo+i (-1: not selected) for
+// the deferred sel/seloff update.
 template <int G>
 __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li, const int rank, const int n,
                                              const int ws_cur, const float (*sq)[D], uint8_t* dsm, int* nsel,
-                                             int* own_dst, unsigned long long* prof) {
+                                             int* own_dst, const bool big, unsigned long long* prof) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = (n + AT_CL - 1) / AT_CL;
   const int lo = min(n, rank * m), hi = min(n, lo + m), cnt = hi - lo;
-  const int off_x = rep_off_x(n), x_bytes = AT_STAGES * AT_STAGE_BYTES - off_x;
-  uint32_t* RA = reinterpret_cast<uint32_t*>(dsm);             // [n] A bits (replicated)
-  uint16_t* SZ = reinterpret_cast<uint16_t*>(dsm + 4 * n);     // [n] sizes (each rank loads all)
-  uint32_t* TK = reinterpret_cast<uint32_t*>(dsm + rep_off_tk(n));  // [n/32] taken bits
-  float* E = reinterpret_cast<float*>(dsm + off_x);            // [G][m] own logits / exps
+  const int off_x = rep_x_offset(n, big), x_bytes = AT_STAGES * AT_STAGE_BYTES - off_x;
+  uint8_t* gscr = big ? big_scratch(a, li) : nullptr;
+  // [n] A bits (replicated in every rank's shared memory; big: one global copy)
+  uint32_t* RA = big ? reinterpret_cast<uint32_t*>(gscr) : reinterpret_cast<uint32_t*>(dsm);
+  // [n] sizes (each rank loads all; big: each rank stores its own range)
+  uint16_t* SZ = big ? reinterpret_cast<uint16_t*>(gscr + 4 * (int64_t)a.Umax) : reinterpret_cast<uint16_t*>(dsm + 4 * n);
+  uint32_t* TK = reinterpret_cast<uint32_t*>(dsm + (big ? 0 : rep_off_tk(n)));  // [n/32] taken bits (per rank)
+  // [G][m] own logits / exps (big: this rank's slice of the per-instance logits scratch
+  // [G][Umax] floats; m <= Umax / 8 since Umax is a multiple of 256)
+  float* E = big ? a.scratch_e + (int64_t)li * G * a.Umax + (int64_t)rank * G * (a.Umax / AT_CL)
+                 : reinterpret_cast<float*>(dsm + off_x);
   SelEnt* LIST = reinterpret_cast<SelEnt*>(dsm + off_x);       // (after E and the lists are dead)
 
   __shared__ float s_coef[7];
@@ -144,7 +166,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
   {
     constexpr int PITCH = ROW_BYTES + 16;
-    const int e_bytes = (G * m * 4 + 127) & ~127;
+    const int e_bytes = big ? 0 : (G * m * 4 + 127) & ~127;
     uint8_t* CS = dsm + off_x + e_bytes;
     const int RB = min(cnt, max(32, ((x_bytes - e_bytes) / PITCH) & ~31));
     const uint32_t cs_s = (uint32_t)__cvta_generic_to_shared(CS);
@@ -171,12 +193,16 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
       __syncthreads();
     }
   }
+  if (!big) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int u = i * AT_THREADS + tid;
-    if (u < n) SZ[u] = (uint16_t)clamp16(szv[i]);
+    for (int i = 0; i < 8; ++i) {
+      const int u = i * AT_THREADS + tid;
+      if (u < n) SZ[u] = (uint16_t)clamp16(szv[i]);
+    }
+    for (int u = 8 * AT_THREADS + tid; u < n; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
+  } else {
+    for (int u = lo + tid; u < hi; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
   }
-  for (int u = 8 * AT_THREADS + tid; u < n; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     float v = mymax[j];
@@ -239,8 +265,12 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[j * m + i], s_Z[j]));
     A = __fdiv_rn(A, (float)G);
     const uint32_t bits = __float_as_uint(A);
+    if (big) {
+      RA[lo + i] = bits;  // (published to the cluster by the barrier below)
+    } else {
 #pragma unroll
-    for (int r = 0; r < AT_CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+      for (int r = 0; r < AT_CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+    }
   }
   if (tid == 0) {
     s_prefix = 0ull;
@@ -949,7 +979,8 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   // select, gather this rank's 1/8 of the new working set — the rows it then attends itself, so no
   // barrier separates gather and attention — and plan again
   const int n = s_S.n_units, ws_cur = s_S.ws_cur;
-  bool rep = false;
+  bool rep = false, big = false;
+  int* own_dst = s_own_dst;
   int total = 0;
   if (flag) {
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -960,17 +991,20 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     }
     __syncthreads();
     bf16* nxtK = a.ws + (ws_cur ^ 1) * a.ws_buf_stride + gi * a.ws_inst_stride;
-    // (the host launches this kernel only when every instance fits the replicated select:
-    // Umax <= LK_REP_N and min(Umax, B) <= LK_REP_SEL; else the multi-kernel sequence)
+    // (the host launches this kernel only when min(Umax, B) <= LK_REP_SEL; instances with more than
+    // LK_REP_N live units select in big mode, with their per-unit arrays in global scratch)
     rep = true;
+    big = n > LK_REP_N;
+    own_dst = big ? reinterpret_cast<int*>(big_scratch(a, li) + 6 * (int64_t)a.Umax) + (int64_t)min(n, rank * ((n + AT_CL - 1) / AT_CL))
+                  : s_own_dst;
     int nsel;
-    total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, s_own_dst, prof);
+    total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, own_dst, big, prof);
     prof_stamp(prof, 4);
 #ifdef LKV_PROF
     if (prof && tid == 0) prof[23] = clock64();
 #endif
     const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
-    lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_off_x(n)), nsel, R0, R1,
+    lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_x_offset(n, big)), nsel, R0, R1,
                    reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
     make_plan(pl, nxtK + (int64_t)R0 * D, R1 - R0, s_post.ring_head, s_post.buffered);
     npre = 0;
@@ -1033,7 +1067,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     uint8_t* sel = a.sel + (int64_t)li * a.Umax;
     int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
     for (int u = lo + tid; u < hi; u += AT_THREADS) {
-      const int d = s_own_dst[u - lo];
+      const int d = own_dst[u - lo];
       if (d >= 0) {
         sel[u] = 1;
         seloff[u] = d;
@@ -1053,11 +1087,11 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
 
 template <int G>
 static cudaError_t launch_layer_g(const LayerArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(layer_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t ea = once_per_device(attr, [] {
+    return cudaFuncSetAttribute(layer_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+  });
+  if (ea != cudaSuccess) return ea;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.r.batch * a.r.hn * AT_CL);
   cfg.blockDim = dim3(AT_THREADS);
@@ -1076,7 +1110,7 @@ static cudaError_t launch_layer_g(const LayerArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st) {
-  if (a.r.Hq > 64 || a.r.Umax > LK_REP_N || min(a.r.Umax, a.r.budget) > LK_REP_SEL) return cudaErrorInvalidValue;
+  if (a.r.Hq > 64 || min(a.r.Umax, a.r.budget) > LK_REP_SEL) return cudaErrorInvalidValue;
   switch (a.r.g) {
     case 1: return launch_layer_g<1>(a, st);
     case 2: return launch_layer_g<2>(a, st);

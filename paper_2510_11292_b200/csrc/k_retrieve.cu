@@ -420,12 +420,11 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
 }
 
 template <int G>
-static void set_attrs_once() {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(select_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+static cudaError_t set_attrs_once() {
+  static std::atomic<uint64_t> attr{0};
+  return once_per_device(attr, [] {
+    return cudaFuncSetAttribute(select_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
 }
 
 cudaError_t launch_trigger_logits(const RetrieveArgs& a, cudaStream_t st) {
@@ -447,10 +446,10 @@ cudaError_t launch_select_gather(const RetrieveArgs& a, cudaStream_t st) {
       sizeof(uint32_t) * ((((a.Umax + 31) / 32) + 1) & ~1) + 8ull * SORT_CAP + 2ull * cap;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   switch (a.g) {
-    case 1: set_attrs_once<1>(); launch_k(select_kernel<1>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
-    case 2: set_attrs_once<2>(); launch_k(select_kernel<2>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
-    case 4: set_attrs_once<4>(); launch_k(select_kernel<4>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
-    case 8: set_attrs_once<8>(); launch_k(select_kernel<8>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 1: if (cudaError_t ea = set_attrs_once<1>()) return ea; launch_k(select_kernel<1>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 2: if (cudaError_t ea = set_attrs_once<2>()) return ea; launch_k(select_kernel<2>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 4: if (cudaError_t ea = set_attrs_once<4>()) return ea; launch_k(select_kernel<4>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
+    case 8: if (cudaError_t ea = set_attrs_once<8>()) return ea; launch_k(select_kernel<8>, dim3(a.batch * a.hn), dim3(SS_THREADS), smem, st, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

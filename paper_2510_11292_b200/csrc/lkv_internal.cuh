@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <utility>
 #include <vector>
@@ -185,8 +186,9 @@ struct LayerArgs {
                 // read before griddepcontrol.wait — the prologue overlaps the previous layer
 };
 constexpr int PROF_SLOTS = 32;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
-// the single launch handles instances with at most LAYER_REP_UNITS units and at most LAYER_REP_SEL
-// selectable units (min(Umax, B)); larger contexts run the multi-kernel sequence
+// the single launch selects on-chip for instances with at most LAYER_REP_UNITS live units (more: the
+// per-unit select arrays move to global scratch, same launch) and handles at most LAYER_REP_SEL
+// selectable units (min(Umax, B)); larger budgets run the multi-kernel sequence
 constexpr int LAYER_REP_UNITS = 8192;
 constexpr int LAYER_REP_SEL = 1024;
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st);
@@ -258,6 +260,21 @@ inline void r3_coefs(float* c) {
     }
     c[i] = (float)(p / fact);
   }
+}
+
+// Kernel attributes (the >48 KB dynamic shared-memory opt-in) are per device context: set them once
+// per device (bit `dev` of `mask`), checking the result; idempotent, so a race between two threads
+// only sets them twice.
+template <typename F>
+inline cudaError_t once_per_device(std::atomic<uint64_t>& mask, F&& set_attrs) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = set_attrs();
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 // Launch with the programmatic-stream-serialization attribute (PDL); captured into CUDA graphs as
