@@ -1,18 +1,26 @@
 #!/usr/bin/env python
 """LouisKV retrieval hot path on B200 — benchmark (driver contract: one JSON line).
 
-Workload (BASELINE.json configs[1]): Llama-3.1-8B attention shape
-(32 layers, 32 query heads, 8 KV heads GQA, d=128), 32K-token prompt, batch 1,
-S=32 / W=512 / B=512 / tau=0.85 / c=16, first two layers full-cache.
-Synthetic seeded data (synth/), random-init: there are no weights in this path.
+Workloads (BASELINE.json configs; default C2 = configs[1], the one the metric is
+quoted on): C2 Llama-3.1-8B attention shape, 32K prompt, batch 1 (long-input); C3 Qwen3-8B shape, 1K
+prompt + 32K generation (short-input long-output); C4 Qwen3-8B shape, 64K prompt + 16K generation,
+batch 8 (long-input long-output). Synthetic seeded data (synth/): throughput seeds plant k/4 key
+groups scattered over positions (overlapping clusters). There are no weights on this path.
 
-One timed "step" = one decode step through all 32 layers in model order, each layer:
-should_retrieve -> retrieve (score/select/gather on flagged sequences) -> append_output
--> sparse_attn (full-cache layers: dense attention), replayed as one CUDA graph with inputs
-already resident in HBM. The prompt clustering (cluster_prompt, once per layer) is timed
-separately and reported as k-means keys/s. Multi-GPU (torchrun): weak scaling, every rank
-runs its own independent sequence batch (no data-path collective; SURVEY §8(e) partitioning
-by batch). ``--impl reference`` times the CPU oracle (the reference arm of this tier).
+One timed "step" = one decode step through all L layers in model order, each layer ONE
+louiskv_decode_layer call (retrieval layer: trigger -> [score / select / gather] -> store_cache ->
+attention in one clustered launch; full-cache layer: store_cache + dense attention in one launch),
+replayed as one CUDA graph per step with inputs already resident in HBM. The decode state is
+checkpointed (louiskv_state_save) before the timed steps, so the end-to-end run (host inputs copied
+in and outputs copied out every step), the L2-pressure variant and the per-kernel attribution pass
+all replay EXACTLY the timed steps (same retrievals). The prompt clustering (cluster_prompt, once
+per layer) is timed with the library's phase timer: k-means keys/s (Lloyd only) and the assignment
+GEMM's TFLOP/s, with the prompt offload reported separately.
+
+Multi-GPU (torchrun): --shard batch (weak scaling: every rank its own sequences, no collective) or
+--shard heads (the default at N > 1 for C4: ranks own contiguous KV-head ranges of the same batch;
+one NCCL all-gather of the per-head outputs per layer, or one per step with --gather step).
+``--impl reference`` times the CPU oracle (the reference arm of this tier) on the box's host cores.
 """
 from __future__ import annotations
 
@@ -22,7 +30,6 @@ import math
 import os
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -31,25 +38,34 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "decode tok/s with LouisKV retrieval at 32K ctx; k-means keys/s; retrieve µs/step"
 UNIT = "tok/s"
+L2_BYTES = 126 * 2 ** 20
+MODEL = {"C1": "single KV head (BASELINE configs[0])", "C2": "Llama-3.1-8B attention shape",
+         "C3": "Qwen3-8B attention shape", "C4": "Qwen3-8B attention shape", "C5": "Qwen3-32B attention shape"}
+PATTERN = {"C2": "long-input short-output", "C3": "short-input long-output", "C4": "long-input long-output",
+           "C5": "long-input", "C1": "oracle-size case"}
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=256)
     p.add_argument("--warmup", type=int, default=16)
     p.add_argument("--impl", default="product", choices=["product", "reference"])
-    p.add_argument("--config", default="C2")
+    p.add_argument("--config", default="C2", choices=["C2", "C3", "C4"])
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--attr-steps", type=int, default=64, help="steps of the per-phase attribution pass")
-    p.add_argument("--cpu-steps", type=int, default=48, help="oracle decode steps for cpu_baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-l2-variant", action="store_true")
     p.add_argument("--kmeans-impl", type=int, default=0)
-    p.add_argument("--shard", default="batch", choices=["batch", "heads"],
+    p.add_argument("--max-output-len", type=int, default=0,
+                   help="context capacity for generated tokens (default: the config's own generation length)")
+    p.add_argument("--shard", default="auto", choices=["auto", "batch", "heads"],
                    help="multi-GPU partitioning: 'batch' = every rank its own sequences (weak scaling, no "
                         "collective); 'heads' = ranks own contiguous KV-head ranges of the same sequences and "
-                        "all-gather the per-head attention outputs over NCCL after every layer (strong scaling)")
-    return p.parse_args()
+                        "all-gather the per-head attention outputs over NCCL (strong scaling); auto = heads for "
+                        "C4 at N > 1, else batch")
+    p.add_argument("--gather", default="layer", choices=["layer", "step"],
+                   help="heads mode: one all-gather per layer (model-faithful) or one batched per step")
+    return p.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -69,14 +85,14 @@ class ClockSampler:
             self.out = open(os.path.join("/tmp", f"lkv_clocks_{os.getpid()}.csv"), "w+")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.out, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.out, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.15)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -136,9 +152,10 @@ def head_range(rank: int, world: int, num_kv_heads: int):
 
 
 def gather_heads(out_own, gathered, world: int):
-    """All-gather of one layer's per-head attention outputs (north_star: NCCL over NVLink, only for the
-    outputs). out_own [b, g*hc, d] -> gathered [world, b, g*hc, d] (rank-major: rank r holds query heads
-    [r*g*hc, (r+1)*g*hc)). Stream-ordered, so it is captured into the step's CUDA graph."""
+    """All-gather of per-head attention outputs (north_star: NCCL over NVLink, only for the outputs).
+    out_own [..., b, g*hc, d] -> gathered [world, ..., b, g*hc, d] (rank-major). Stream-ordered, so it
+    is captured into the step's CUDA graph. Works for one layer ([b, gq, d]) or a whole step
+    ([L, b, gq, d], the per-step batched variant)."""
     if world > 1:
         import torch.distributed as dist
         dist.all_gather_into_tensor(gathered.view((-1,) + tuple(out_own.shape[1:])), out_own)
@@ -147,18 +164,13 @@ def gather_heads(out_own, gathered, world: int):
 
 
 def assemble_heads(gathered):
-    """[world, b, g*hc, d] -> [b, Hq, d] in model head order (what the O-projection consumes)."""
+    """[world, b, g*hc, d] -> [b, Hq, d] in model head order (what the O-projection consumes); a step's
+    [world, L, b, g*hc, d] -> [L, b, Hq, d]."""
+    if gathered.dim() == 5:
+        w, L, b, gh, d = gathered.shape
+        return gathered.permute(1, 2, 0, 3, 4).reshape(L, b, w * gh, d)
     w, b, gh, d = gathered.shape
     return gathered.permute(1, 0, 2, 3).reshape(b, w * gh, d)
-
-
-def ncu_traffic():
-    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant kernels from
-    the committed `ncu --set full` capture summary (profiles/r01_traffic.json); {} when absent."""
-    try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-    except Exception:
-        return {}
 
 
 def max_over_ranks(x: float, world: int) -> float:
@@ -181,214 +193,352 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
-# ----------------------------------------------------------------------------- oracle (CPU) leg
-def oracle_sample(cfg, seed: int, steps: int):
-    """Time the CPU oracle, as it stands, on a bounded sample of the workload: one retrieval-layer
-    instance (1 KV head, its g query heads) and one full-cache instance of the C2 shape, `steps`
-    decode steps. Returns per-instance-step seconds and the extrapolated full decode-step time
-    (inst counts of the config: b*L_r*Hkv retrieval + b*L_f*Hkv full-cache instances)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def n_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def throughput_cfg(name: str):
+    """The config as benchmarked: throughput seeds plant k/4 key groups."""
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[name]
+    return cfg.replace(k_planted=max(cfg.n_clusters // 4, 2 * cfg.n_targets))
+
+
+def workload_label(cfg, T_steps=None) -> str:
+    full = ",".join(str(l) for l in cfg.full_cache_layers)
+    return (f"{cfg.name} {PATTERN.get(cfg.name, '')}: {MODEL.get(cfg.name, cfg.name)} (L={cfg.num_layers}, "
+            f"Hq={cfg.num_q_heads}, Hkv={cfg.num_kv_heads}, d={cfg.head_dim}), {cfg.prompt_len}-token prompt, "
+            f"{cfg.decode_steps}-token generation, batch {cfg.batch}, S={cfg.sink_tokens} W={cfg.window_tokens} "
+            f"B={cfg.budget_tokens} tau={cfg.tau} c={cfg.avg_cluster_size}, full-cache layers {full}; "
+            f"k-means {cfg.kmeans_iters} iters; planted key groups k/4 = {cfg.k_planted}")
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+# Only bench's cpu_baseline leg and --impl reference execute anything under oracle/ (tier rule ③).
+def _oracle_worker(args):
+    """One process: run the oracle decode (Algorithm 1 order per instance) for the given
+    (layer, kv-head) instances over `steps` steps. Returns seconds per phase of the run."""
+    (cfg_name, kp, seed, insts, steps, warm, start_evt, plen) = args
     import numpy as np
     import torch
     import synth
+    from synth.configs import CONFIGS
     from oracle.episode import OracleEpisode
     from _pair import planted_assign
+    torch.set_num_threads(1)
+    cfg = CONFIGS[cfg_name].replace(k_planted=kp)
+    if plen:
+        cfg = cfg.replace(prompt_len=plen, k_planted=kp)
+    T = warm + steps
+    layers = sorted({l for l, _ in insts})
+    plants = {l: synth.planted(cfg, l, seed, "cpu") for l in layers}
+    eps = {}
+    for l, h in insts:
+        ep = OracleEpisode(cfg, kv_head_begin=h, kv_head_count=1)
+        K, V, lab = synth.prompt_kv(cfg, l, seed, "cpu", plants[l], return_labels=True)
+        Kn = K[:, :, h:h + 1].float().numpy()
+        Vn = V[:, :, h:h + 1].float().numpy()
+        if l in cfg.full_cache_layers:
+            ep.cluster_prompt(l, Kn, Vn)
+        else:
+            ep.cluster_prompt(l, Kn, Vn, assign=planted_assign(cfg, lab[:, :, h:h + 1]))
+        eps[(l, h)] = ep
+    # decode inputs of the needed layers only (same generator as the product arm)
+    one = cfg.replace(num_layers=max(layers) + 1, k_planted=kp)
+    q, k, v, _ = synth.decode_stream(one, T, seed, "cpu", [plants.get(l) or synth.planted(one, l, seed, "cpu")
+                                                           for l in range(max(layers) + 1)])
+    qn, kn, vn = q.float().numpy(), k.float().numpy(), v.float().numpy()
+    g = cfg.group
+    if start_evt is not None:
+        start_evt.wait()
 
-    one = cfg.replace(num_layers=2, full_cache_layers=(0,), num_kv_heads=1, num_q_heads=cfg.group, batch=1,
-                      decode_steps=steps, k_planted=cfg.k_planted)
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    plants = [synth.planted(one, l, seed, dev) for l in range(2)]
-    KV = [synth.prompt_kv(one, l, seed, dev, plants[l], return_labels=True) for l in range(2)]
-    q, k, v, _ = synth.decode_stream(one, steps, seed, dev, plants)
-    ep = OracleEpisode(one)
-    ep.cluster_prompt(0, KV[0][0].float().cpu().numpy(), KV[0][1].float().cpu().numpy())
-    a = planted_assign(one, KV[1][2])
-    ep.cluster_prompt(1, KV[1][0].float().cpu().numpy(), KV[1][1].float().cpu().numpy(), assign=a)
-    qn, kn, vn = q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy()
-    t_full = t_ret = 0.0
-    for t in range(steps):
-        for l in range(2):
-            t0 = time.perf_counter()
+    def run(t):
+        for (l, h), ep in eps.items():
             ep.should_retrieve(l, qn[t, l])
-            ep.retrieve(l, qn[t, l])
-            ep.append_output(l, kn[t, l], vn[t, l])
-            ep.sparse_attn(l, qn[t, l])
-            dt = time.perf_counter() - t0
-            if l == 0:
-                t_full += dt
-            else:
-                t_ret += dt
-    n_full = cfg.batch * len(cfg.full_cache_layers) * cfg.num_kv_heads
-    n_ret = cfg.batch * (cfg.num_layers - len(cfg.full_cache_layers)) * cfg.num_kv_heads
-    step_s = (n_ret * t_ret + n_full * t_full) / steps
-    return dict(t_ret=t_ret / steps, t_full=t_full / steps, step_s=step_s, n_ret=n_ret, n_full=n_full)
+            ep.retrieve(l, qn[t, l][:, h * g:(h + 1) * g])
+            ep.append_output(l, kn[t, l][:, h:h + 1], vn[t, l][:, h:h + 1])
+            ep.sparse_attn(l, qn[t, l][:, h * g:(h + 1) * g])
+
+    for t in range(warm):
+        run(t)
+    t0 = time.perf_counter()
+    for t in range(warm, T):
+        run(t)
+    return time.perf_counter() - t0
+
+
+def _kmeans_worker(args):
+    """One Lloyd iteration of the oracle k-means on one instance of the config (seconds)."""
+    cfg_name, kp, seed, layer, head = args
+    import synth
+    import oracle
+    from synth.configs import CONFIGS
+    cfg = CONFIGS[cfg_name].replace(k_planted=kp)
+    K, _ = synth.prompt_kv(cfg, layer, seed, "cpu")
+    X = K[0, cfg.sink_tokens:, head].float().numpy().copy()
+    k = cfg.n_clusters
+    t0 = time.perf_counter()
+    oracle.kmeans(X, k, 1, mode=1)
+    return time.perf_counter() - t0
+
+
+def _pool(n):
+    import multiprocessing as mp
+    return mp.get_context("fork").Pool(n)
+
+
+def cpu_baseline(cfg, seed: int, steps: int = 12, warm: int = 2):
+    """The oracle as it stands on the host cores, bounded samples of the same workload:
+    decode — one retrieval-layer instance + one full-cache instance per process for `steps` steps,
+    alone (1 thread) and one process per core concurrently (different instances); k-means — one Lloyd
+    iteration of one instance, alone and one per core. Extrapolated to whole steps / all iterations."""
+    import oracle  # noqa: F401  (builds the C oracle once before forking)
+    oracle.build_oracle()
+    nc = n_cores()
+    full = sorted(cfg.full_cache_layers)
+    ret = [l for l in range(cfg.num_layers) if l not in cfg.full_cache_layers]
+    plen = 0
+    t1 = _oracle_worker((cfg.name, cfg.k_planted, seed, [(ret[0], 0), (full[0], 0)], steps, warm, None, plen))
+    jobs = [(cfg.name, cfg.k_planted, seed, [(ret[i % len(ret)], i % cfg.num_kv_heads),
+                                             (full[i % len(full)], (i + 1) % cfg.num_kv_heads)], steps, warm, None, plen)
+            for i in range(nc)]
+    w0 = time.perf_counter()
+    with _pool(nc) as p:
+        tn = p.map(_oracle_worker, jobs)
+    wall = time.perf_counter() - w0
+    # per-step work of the full config: n_ret retrieval + n_full full-cache instance-steps; the pair
+    # sample is split into its parts with a second 1-thread sample of the retrieval instance alone
+    n_ret = cfg.batch * len(ret) * cfg.num_kv_heads
+    n_full = cfg.batch * len(full) * cfg.num_kv_heads
+    per_pair_1t = t1 / steps  # one retrieval + one full-cache instance-step, one thread
+    t_ret = _oracle_worker((cfg.name, cfg.k_planted, seed, [(ret[0], 0)], steps, warm, None, plen)) / steps
+    t_full = max(per_pair_1t - t_ret, 0.0)
+    step_1t = n_ret * t_ret + n_full * t_full
+    # all cores: every process does 1/nc of the instances, each slowed by the measured contention
+    # (mean time of the concurrent samples over the same sample alone)
+    par_eff = (sum(tn) / len(tn)) / t1
+    step_nc = step_1t * par_eff / nc
+    # k-means: one iteration of one instance
+    kt1 = _kmeans_worker((cfg.name, cfg.k_planted, seed, ret[0], 0))
+    w0 = time.perf_counter()
+    with _pool(nc) as p:
+        ktn = p.map(_kmeans_worker, [(cfg.name, cfg.k_planted, seed, ret[i % len(ret)], i % cfg.num_kv_heads)
+                                     for i in range(nc)])
+    kwall = time.perf_counter() - w0
+    N = cfg.prompt_len - cfg.sink_tokens
+    return {
+        "value": cfg.batch / (step_nc if nc > 1 else step_1t), "unit": UNIT, "cores": nc, "kind": "oracle",
+        "cpu_model": cpu_model(),
+        "value_1_thread": cfg.batch / step_1t,
+        "ms_per_step_1_thread": step_1t * 1e3, "ms_per_step_all_cores": step_nc * 1e3,
+        "per_instance_step_ms": {"retrieval": t_ret * 1e3, "full_cache": t_full * 1e3},
+        "concurrent_slowdown": par_eff, "concurrent_wall_s": wall,
+        "kmeans_keys_per_s_1_thread": N / (kt1 * cfg.kmeans_iters),
+        "kmeans_keys_per_s_all_cores": nc * N / (max(ktn) * cfg.kmeans_iters),
+        "kmeans_iter_s_1_thread": kt1, "kmeans_wall_s_all_cores": kwall,
+        "sample": (f"decode: {steps} steps ({warm} warm-up) of one retrieval-layer + one full-cache instance "
+                   f"(1 KV head, {cfg.group} q heads) at {cfg.name} sizes, alone (1 thread) and one process per "
+                   f"core concurrently ({nc} processes, different instances), extrapolated x{n_ret} retrieval / "
+                   f"x{n_full} full-cache instances to one {cfg.num_layers}-layer step (all cores: x parallel "
+                   f"efficiency / {nc}); k-means: one Lloyd iteration (N={N}, k={cfg.n_clusters}, d=128, fp64) of "
+                   f"one instance alone and {nc} concurrently, x{cfg.kmeans_iters} iterations"),
+    }
 
 
 def run_reference(args):
-    import torch
+    """--impl reference: the CPU oracle, as it stands, on the box's host cores (rank 0 only). C2: FULL
+    decode steps — every (layer, kv-head) instance of the config, spread over one process per core;
+    C3/C4: a sample of instances (stated), extrapolated by instance count."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from synth.configs import CONFIGS
-    cfg = CONFIGS[args.config]
-    total = args.warmup + args.steps
-    s = oracle_sample(cfg, args.seed, total)
-    value = cfg.batch / s["step_s"]
-    sample = (f"per step: 1 retrieval-layer instance (1 KV head, {cfg.group} q heads) + 1 full-cache instance of "
-              f"{cfg.name}, extrapolated x{s['n_ret']} / x{s['n_full']} instances; {total} steps")
+    import multiprocessing as mp
+    import oracle
+    oracle.build_oracle()
+    cfg = throughput_cfg(args.config)
+    nc = n_cores()
+    L, H = cfg.num_layers, cfg.num_kv_heads
+    all_inst = [(l, h) for l in range(L) for h in range(H)]
+    if cfg.name == "C2":
+        chosen, scale, kind = all_inst, 1.0, "full steps"
+    else:
+        # sample: every layer kind, one KV head per layer, batch as configured
+        chosen = [(l, l % H) for l in range(L)]
+        scale, kind = len(all_inst) / len(chosen), f"sampled {len(chosen)} of {len(all_inst)} (layer, kv-head) instances"
+    # balance: full-cache instances (expensive) dealt first, round robin
+    full = [i for i in chosen if i[0] in cfg.full_cache_layers]
+    rest = [i for i in chosen if i[0] not in cfg.full_cache_layers]
+    nw = min(nc, len(chosen))
+    buckets = [[] for _ in range(nw)]
+    for j, inst in enumerate(full + rest):
+        buckets[j % nw].append(inst)
+    K, W = max(args.steps, 1), max(args.warmup, 0)
+    t0 = time.perf_counter()
+    with _pool(nw) as p:
+        times = p.map(_oracle_worker, [(cfg.name, cfg.k_planted, args.seed, bk, K, W, None, 0) for bk in buckets])
+    wall = time.perf_counter() - t0
+    step_s = max(times) / K * scale  # the slowest process bounds a step
+    value = cfg.batch / step_s
+    sample = (f"{kind}: {len(chosen)} instances of {cfg.name} (batch {cfg.batch}) on {nw} processes "
+              f"(one per core), {W} warm-up + {K} timed decode steps each; step time = slowest process"
+              + ("" if scale == 1.0 else f", x{scale:.1f} instances (extrapolated)"))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s["step_s"] * 1e3,
+            "steps": K, "warmup": W, "ms_per_step": step_s * 1e3, "ms_per_step_extrapolated": scale != 1.0,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{cfg.name}", "global_batch": cfg.batch * args.gpus,
-                                            "seq_len": cfg.prompt_len},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic (seeded, planted clusters/segments; the product arm's recipe, CPU random stream)",
+            "config": {"workload": workload_label(cfg), "global_batch": cfg.batch, "seq_len": cfg.prompt_len},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nw, "kind": "oracle", "cpu_model": cpu_model(),
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ----------------------------------------------------------------------------- product leg
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
     import numpy as np
     import torch
     import synth
-    from synth.configs import CONFIGS
     import paper_2510_11292_b200 as lkv
 
     world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    cfg = CONFIGS[args.config]
+    cfg = throughput_cfg(args.config)
     L, b, Hq, Hkv, d, g = cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.group
     full = set(cfg.full_cache_layers)
+    ret_layers = [l for l in range(L) if l not in full]
     K, W = args.steps, args.warmup
-    A = args.attr_steps
-    T = 1 + W + K + K + A + 2  # direct step + warmup + timed + e2e + attribution (+slack)
-    heads = args.shard == "heads"
-    # batch sharding: every rank its own sequences; head sharding: the same sequences, own KV heads
+    T = 1 + W + K + 2
+    shard = args.shard if args.shard != "auto" else ("heads" if (world > 1 and cfg.name == "C4") else "batch")
+    heads = shard == "heads"
     seed = args.seed if heads else rank_seed(args.seed, rank)
     hb, hc = head_range(rank, world, Hkv) if heads else (0, Hkv)
-    gq = g * hc  # query heads owned by this rank
-    jobs = 1 if heads else world  # independent sequence batches processed by the whole job
-    ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=hb, kv_head_count=hc,
-                                      max_output_len=max(cfg.max_output_len, T + 1), device=local,
+    gq = g * hc
+    jobs = 1 if heads else world
+    cap_out = args.max_output_len or max(cfg.max_output_len, T + 1)
+    ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=hb, kv_head_count=hc, max_output_len=cap_out, device=local,
                                       kmeans_impl=args.kmeans_impl))
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
 
-    # ---------------- prefill: cluster_prompt for every layer, timed as one region ending at the
-    # prompt fence (k-means keys/s; the copy-engine offload of layer l overlaps layer l+1's k-means)
+    # ---------------- prefill: cluster_prompt per layer (inputs generated per layer, so C4's 73 GB
+    # prompt never sits on the device at once); phase timer on
+    ctx.set_prefill_timing(True)
     plants = [synth.planted(cfg, l, seed, dev) for l in range(L)]
-    prompts = [tuple(t[:, :, hb:hb + hc] for t in synth.prompt_kv(cfg, l, seed, dev, plants[l])) for l in range(L)]
-    km_keys = sum(b * hc * (cfg.prompt_len - cfg.sink_tokens) for l in range(L) if l not in full)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    km_ms_calls = 0.0
+    km_keys = 0
     for l in range(L):
-        ctx.cluster_prompt(l, *prompts[l])
+        Kl, Vl = synth.prompt_kv(cfg, l, seed, dev, plants[l])
+        Kl, Vl = Kl[:, :, hb:hb + hc], Vl[:, :, hb:hb + hc]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.cluster_prompt(l, Kl, Vl)
+        e1.record()
+        torch.cuda.synchronize()
+        km_ms_calls += e0.elapsed_time(e1)
+        if l not in full:
+            km_keys += b * hc * (cfg.prompt_len - cfg.sink_tokens)
+        del Kl, Vl
     ctx.prompt_fence()
-    e1.record()
     torch.cuda.synchronize()
-    km_ms = max_over_ranks(e0.elapsed_time(e1), world)
-    km_keys *= world  # keys clustered by the whole job (every rank: its own heads or sequences)
-    del prompts
+    pt = ctx.prefill_times()
+    ctx.set_prefill_timing(False)
     st0 = ctx.stats()
 
     # ---------------- decode inputs (device resident) and static graph buffers
-    q, kk, vv, bset = synth.decode_stream(cfg, T, seed, dev, plants)
+    q, kk, vv, _ = synth.decode_stream(cfg, T, seed, dev, plants)
     del plants
-    # one step's inputs (q of all heads, k_t, v_t of every layer) packed in ONE buffer, so a step's
-    # input is a single copy: qkv [T, n_q + 2 n_kv] on the device (and pinned on the host for e2e)
     n_q, n_kv = L * b * Hq * d, L * b * Hkv * d
     qkv = torch.cat([q.reshape(T, -1), kk.reshape(T, -1), vv.reshape(T, -1)], dim=1)
     del q, kk, vv
     qkv_in = torch.empty((n_q + 2 * n_kv,), dtype=torch.bfloat16, device=dev)
-    q_in = qkv_in[:n_q].view(L, b, Hq, d)
-    k_in = qkv_in[n_q:n_q + n_kv].view(L, b, Hkv, d)
-    v_in = qkv_in[n_q + n_kv:].view(L, b, Hkv, d)
     out = torch.empty((L, b, gq, d), dtype=torch.bfloat16, device=dev)
-    # head sharding: per-layer all-gather of the owned heads' outputs -> [L, world, b, gq, d]
-    gathered = torch.empty((L, world, b, gq, d), dtype=torch.bfloat16, device=dev) if heads else None
-    k_own = k_in[:, :, hb:hb + hc]
-    v_own = v_in[:, :, hb:hb + hc]
-
+    gathered = torch.empty((world, L, b, gq, d), dtype=torch.bfloat16, device=dev) if heads else None
     flags = torch.zeros((L, b), dtype=torch.uint8, device=dev)
 
-    def issue_step(events=None, src=None):
-        # one louiskv_decode_layer call per layer: trigger -> retrieve -> store_cache -> attention
-        # (one clustered launch on a retrieval layer; one launch on a full-cache layer). src: a step's
-        # packed inputs read in place (else the static input buffer)
-        qs, ks, vs = q_in, k_own, v_own
-        if src is not None:
-            qs = src[:n_q].view(L, b, Hq, d)
-            ks = src[n_q:n_q + n_kv].view(L, b, Hkv, d)[:, :, hb:hb + hc]
-            vs = src[n_q + n_kv:].view(L, b, Hkv, d)[:, :, hb:hb + hc]
-        for l in range(L):
-            if events is not None:
-                events[l].record()
+    def views(src):
+        qs = src[:n_q].view(L, b, Hq, d)
+        ks = src[n_q:n_q + n_kv].view(L, b, Hkv, d)[:, :, hb:hb + hc]
+        vs = src[n_q + n_kv:].view(L, b, Hkv, d)[:, :, hb:hb + hc]
+        return qs, ks, vs
+
+    def issue_layers(layers, src=None, between=None):
+        qs, ks, vs = views(qkv_in if src is None else src)
+        for l in layers:
             ctx.decode_layer(l, qs[l], ks[l], vs[l], out[l], flag_out=flags[l])
-            if heads:
-                gather_heads(out[l], gathered[l], world)
-        if events is not None:
-            events[L].record()
+            if heads and args.gather == "layer":
+                gather_heads(out[l], gathered[:, l], world)
+            if between is not None:
+                between()
+        if heads and args.gather == "step" and len(layers) == L:
+            gather_heads(out, gathered, world)
+
+    def issue_step(src=None, between=None):
+        issue_layers(range(L), src, between)
 
     step_idx = 0
-
-    def load(i):
-        qkv_in.copy_(qkv[i], non_blocking=True)
-
-    # step 1 runs directly (sets kernel attributes, t == 1 retrieval everywhere)
-    load(step_idx)
-    issue_step()
+    qkv_in.copy_(qkv[step_idx])
+    issue_step()  # step 1 runs directly (t == 1: retrieval everywhere)
     step_idx += 1
     torch.cuda.synchronize()
-
     cap_stream = torch.cuda.Stream(device=dev)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=cap_stream):
         issue_step()
-    # retrieval layer: one clustered launch (layer_kernel); full-cache layer: one launch
-    # (attn_full_tc_kernel with store_cache fused)
-    launches_per_step = L
-
     for _ in range(W):
-        load(step_idx)
+        qkv_in.copy_(qkv[step_idx])
         graph.replay()
         step_idx += 1
-    # the timed region replays one graph per step, each reading its step's inputs in place (already
-    # resident in HBM: no per-step copy); captured before the clock starts
+    s0 = step_idx  # first timed step
     step_graphs = []
     for i in range(K):
         gi = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gi, stream=cap_stream):
-            issue_step(src=qkv[step_idx + i])
+            issue_step(src=qkv[s0 + i])
         step_graphs.append(gi)
+    torch.cuda.synchronize()
+    ctx.state_save()  # the timed steps are replayed exactly by e2e / L2 / attribution below
     torch.cuda.synchronize()
 
     # ---------------- timed region (device-resident inputs)
-    P_, nr_ = cfg.prompt_len, L - len(full)
-    kv_step_bytes = (len(full) * b * hc * (P_ + T) + nr_ * b * hc * (cfg.sink_tokens + cfg.budget_tokens
-                                                                      + cfg.window_tokens)) * 512
-    L2_BYTES = 126 * 2 ** 20
+    P_ = cfg.prompt_len
+    kv_step_bytes = (len(full) * b * hc * (P_ + s0) + len(ret_layers) * b * hc *
+                     (cfg.sink_tokens + cfg.budget_tokens + cfg.window_tokens)) * 512
     flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if kv_step_bytes < 2 * L2_BYTES else None
-    clocks = ClockSampler(local)
-    barrier(world)
-    clocks.start()
-    st_a = ctx.stats()
-    barrier(world)
-    def dev_timed(body):
-        """Device time of K calls of body(i). When the rank's per-step KV bytes fit in L2 (head sharding
-        over many GPUs), L2 is flushed between steps, outside the timed spans (per-step event pairs)."""
+
+    def dev_timed(body, n):
+        """Device time of n calls of body(i); L2 flushed between steps (outside the timed spans) when the
+        rank's per-step KV bytes fit in L2."""
         if flush_buf is None:
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record()
-            for i in range(K):
+            for i in range(n):
                 body(i)
             t1.record()
             torch.cuda.synchronize()
             return t0.elapsed_time(t1)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-        for i in range(K):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for i in range(n):
             flush_buf.add_(1)
             evs[i][0].record()
             body(i)
@@ -396,61 +546,89 @@ def main():
         torch.cuda.synchronize()
         return sum(a.elapsed_time(z) for a, z in evs)
 
-    def timed_body(i):
-        nonlocal step_idx
-        step_graphs[i].replay()
-        step_idx += 1
-
-    ms = dev_timed(timed_body)
+    clocks = ClockSampler(local)
+    barrier(world)
+    clocks.start()
+    st_a = ctx.stats()
+    barrier(world)
+    ms = dev_timed(lambda i: step_graphs[i].replay(), K)
     barrier(world)
     clk = clocks.stop()
     ms = max_over_ranks(ms, world)
     st_b = ctx.stats()
+    stats_timed = {k_: st_b[k_] - st_a[k_] for k_ in st_b if not k_.startswith("kmeans")}
     value = jobs * b * K / (ms / 1e3)
+    del step_graphs
 
-    # ---------------- e2e: host inputs -> device, graph, outputs -> host, every step
-    qkv_h = qkv[step_idx:step_idx + K].cpu().pin_memory()
-    res = gathered if heads else out  # the step's result: every query head's output
+    # ---------------- e2e: the SAME steps again from the checkpoint, host inputs -> device, graph,
+    # outputs -> host, every step (through the public API: louiskv_decode_layer per layer)
+    ctx.state_restore()
+    qkv_h = qkv[s0:s0 + K].cpu().pin_memory()
+    res = gathered if heads else out
     oh = torch.empty((K,) + tuple(res.shape), dtype=torch.bfloat16).pin_memory()
     barrier(world)
+
     def e2e_body(i):
-        nonlocal step_idx
         qkv_in.copy_(qkv_h[i], non_blocking=True)
         graph.replay()
         oh[i].copy_(res, non_blocking=True)
-        step_idx += 1
 
     st_e0 = ctx.stats()
-    e2e_ms = dev_timed(e2e_body)
+    e2e_ms = dev_timed(e2e_body, K)
     barrier(world)
     st_e1 = ctx.stats()
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e = {"value": jobs * b * K / (e2e_ms / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": int(qkv_h[0].numel()) * 2,
-           "d2h_bytes_per_step": int(oh[0].numel()) * 2, "ms_per_step": e2e_ms / K,
-           # (the e2e steps are the K decode steps after the timed ones: their retrieval rate differs)
-           "retrievals_per_step": (st_e1["retrievals"] - st_e0["retrievals"]) / K / max(L - len(full), 1) / b}
+           "h2d_bytes_per_step": int(qkv_h[0].numel()) * 2, "d2h_bytes_per_step": int(oh[0].numel()) * 2,
+           "ms_per_step": e2e_ms / K, "same_steps_as_value": True,
+           "retrievals_same": (st_e1["retrievals"] - st_e0["retrievals"]) == stats_timed["retrievals"]}
+    del qkv_h, oh
 
-    # ---------------- attribution pass: the retrieval layers and the full-cache layers captured as two
-    # separate graphs (layers are independent, so each keeps its own step sequence; PDL edges intact,
-    # no event nodes inside), each replay timed on the device; the retrieval-layer time per launch is
-    # split into unflagged / flagged by a least-squares fit over replays (flags read back per replay)
-    ret_layers = [l for l in range(L) if l not in full]
+    # ---------------- L2-pressure variant: the same steps with a 2 x L2 buffer rewritten between layers
+    # (stand-in for the weight traffic of a real model between attention layers; no PDL edge across it);
+    # attention-side time = (steps with flushes) - (the flushes alone)
+    l2v = None
+    if not args.no_l2_variant:
+        ctx.state_restore()
+        fl_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+        gl2, gfl = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gl2, stream=cap_stream):
+            issue_step(between=lambda: fl_buf.add_(1))
+        with torch.cuda.graph(gfl, stream=cap_stream):
+            for _ in range(L):
+                fl_buf.add_(1)
+        K2 = K
 
-    def issue_subset(layers):
-        for l in layers:
-            ctx.decode_layer(l, q_in[l], k_own[l], v_own[l], out[l], flag_out=flags[l])
+        def l2_body(i):
+            qkv_in.copy_(qkv[s0 + i], non_blocking=True)
+            gl2.replay()
 
+        def fl_body(i):
+            qkv_in.copy_(qkv[s0 + i], non_blocking=True)
+            gfl.replay()
+
+        ms_l2 = max_over_ranks(dev_timed(l2_body, K2), world)
+        ms_fl = max_over_ranks(dev_timed(fl_body, K2), world)
+        att_ms = (ms_l2 - ms_fl) / K2
+        l2v = {"ms_per_step_with_flushes": ms_l2 / K2, "flush_ms_per_step": ms_fl / K2,
+               "attention_side_ms_per_step": att_ms, "value": jobs * b / (att_ms / 1e3),
+               "unit": UNIT, "flush_bytes_per_layer": 2 * fl_buf.numel() * 4,
+               "note": "same timed steps (checkpoint restore); a 252 MB read+write between every two layers "
+                       "evicts L2, so every layer starts cold; value = attention-side tok/s"}
+        del gl2, gfl, fl_buf
+
+    # ---------------- attribution: the same steps again, the retrieval layers and the full-cache layers
+    # as two graphs (each replay timed on the device); least squares on the per-replay flag counts
+    ctx.state_restore()
     g_ret, g_full = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_ret, stream=cap_stream):
-        issue_subset(ret_layers)
+        issue_layers(ret_layers)
     with torch.cuda.graph(g_full, stream=cap_stream):
-        issue_subset(sorted(full))
-    st_c = ctx.stats()
+        issue_layers(sorted(full))
     rows_fit, t_full = [], []
-    for i in range(A):
-        load(step_idx)
-        step_idx += 1
+    st_c = ctx.stats()
+    for i in range(K):
+        qkv_in.copy_(qkv[s0 + i])
         a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a0.record()
         g_ret.replay()
@@ -472,16 +650,15 @@ def main():
     else:
         coef = np.array([y.sum() / max(n_unf_tot, 1), 0.0])
     u_ms, f_ms = float(coef[0]), float(coef[1])
-    mean = lambda xs: sum(xs) / len(xs) if xs else 0.0
-    t_unf = [u_ms] * n_unf_tot
-    t_flg = [f_ms] * n_flg_tot
-    phase = {"retrieval_layers_unflagged": u_ms * n_unf_tot / A, "retrieval_layers_flagged": f_ms * n_flg_tot / A,
-             "full_cache_layers": mean(t_full) * len(full)}  # ms per step
-    layer_us = {"retrieval_unflagged": u_ms * 1e3, "retrieval_flagged": f_ms * 1e3, "full_cache": mean(t_full) * 1e3,
-                "n_flagged": n_flg_tot, "n_unflagged": n_unf_tot,
-                "method": "per-replay device time of a retrieval-layers-only graph, least squares on flag counts"}
+    full_ms = float(np.mean(t_full)) if full else 0.0
+    ret_ms_attr = float(y.mean())  # retrieval layers per step (attribution replays)
+    layer_us = {"retrieval_unflagged": u_ms * 1e3, "retrieval_flagged": f_ms * 1e3, "full_cache": full_ms * 1e3,
+                "n_flagged_launches": n_flg_tot, "n_unflagged_launches": n_unf_tot,
+                "method": "the timed steps replayed from the checkpoint as a retrieval-layers-only graph and a "
+                          "full-cache-layers-only graph, each replay timed on the device; flagged / unflagged "
+                          "per-launch time by least squares on the per-replay flag counts"}
 
-    # ---------------- host-link peak (pinned H2D copy) and HBM / tensor peaks
+    # ---------------- host-link peak (pinned H2D copy)
     hl = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     hd = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     best = 1e9
@@ -494,135 +671,136 @@ def main():
         best = min(best, a0.elapsed_time(a1))
     host_link_gbs = (256 << 20) / (best / 1e3) / 1e9
     del hl, hd
-    peaks = measured_peaks()
-    traffic = ncu_traffic()
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
-    # ---- per-launch algorithmic bytes. Full-cache launch: K+V rows of P+t tokens. Retrieval-layer
-    # launch: the attended rows (sinks + working set + local buffer; buffered = t - evicted tokens),
-    # plus on a flagged launch the centroid reads (n_units x 256 B) and the working-set rebuild
-    # (rows written 512 B each; host rows cross the link, kept rows are re-read from HBM).
-    P = cfg.prompt_len
-    t_mid = step_idx - A // 2
-    full_bytes = b * hc * (P + t_mid) * 2 * d * 2
-    att_rows, n_units = 0, 0
-    kc = -(-(P - cfg.sink_tokens) // cfg.avg_cluster_size)
-    for l in range(L):
-        if l in full:
-            continue
+    # ---------------- rooflines, from the TIMED window: the full-cache layers' share is their
+    # attribution time (flag independent), the retrieval layers get the rest of the timed step
+    ms_step = ms / K
+    full_ms_step = full_ms * len(full)
+    ret_ms_step = max(ms_step - full_ms_step, 1e-9)
+    n_ret_launch = len(ret_layers) * K
+    # algorithmic bytes of the retrieval-layer launches over the timed window: attended rows (sinks +
+    # working set + local buffer, from the unit tables at the window's end, 512 B each) per launch, plus
+    # on flagged launches the centroid reads (units scored x 256 B) and the working-set rebuild
+    # (new rows read over the link and written, kept rows read and written: <= B rows per instance)
+    att_rows = 0
+    kc = cfg.n_clusters
+    t_end = s0 + K
+    for l in ret_layers:
         for bb in range(b):
             for hh in range(hc):
                 _, sizes, _ = ctx.get_units(l, bb, hh)
                 nws = len(ctx.get_working_set(l, bb, hh)[0])
-                att_rows += min(cfg.sink_tokens, P) + nws + (step_idx - int(sizes[kc:].sum()))
-                n_units += len(sizes)
-    n_rl = L - len(full)
-    unf_bytes = att_rows / n_rl * 512
-    h2d_bytes = st_d["bytes_h2d"] - st_c["bytes_h2d"]
-    flg_launches = max(len(t_flg), 1)
-    ws_rows_flg = b * hc * cfg.budget_tokens  # rows rebuilt per flagged launch (upper bound: B per instance)
-    flg_bytes = unf_bytes + n_units / n_rl * 256 + ws_rows_flg * 512 + (ws_rows_flg * 512 - h2d_bytes / flg_launches)
-    ret_ms = (sum(t_unf) + sum(t_flg)) / max(len(t_unf) + len(t_flg), 1)
-    ret_bytes = (unf_bytes * len(t_unf) + flg_bytes * len(t_flg)) / max(len(t_unf) + len(t_flg), 1)
-    ret_gbs = ret_bytes / (ret_ms / 1e3) / 1e9
-    step_ms_attr = sum(phase.values())
-    lk_tr, fa_tr = traffic.get("layer_kernel"), traffic.get("attn_full_tc_kernel")
-    n_l = max(len(t_unf) + len(t_flg), 1)
-    layer_traffic = ((lk_tr["unflagged"] * len(t_unf) + lk_tr["flagged"] * len(t_flg)) / n_l) if lk_tr else None
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"
-    roofline_layer = {"kernel": "layer_kernel (retrieval layers: trigger + score/select + gather + append + attention)",
-                      "bound": "hbm", "achieved": ret_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ret_gbs / hbm_peak,
-                      "traffic": layer_traffic, "bytes_per_launch": ret_bytes, "ms_per_launch": ret_ms,
-                      "peak_source": peak_src,
-                      "share_of_step": (phase["retrieval_layers_unflagged"] + phase["retrieval_layers_flagged"]) / step_ms_attr}
-    attn_full_ms = mean(t_full)
-    att_full_gbs = full_bytes / (attn_full_ms / 1e3) / 1e9
-    roofline_attn = {"kernel": "attn_full_tc_kernel (full-cache layers: store_cache + split-K flash-decode, one launch)",
-                     "bound": "hbm", "achieved": att_full_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": att_full_gbs / hbm_peak, "traffic": fa_tr["per_launch"] if fa_tr else None,
-                     "bytes_per_launch": full_bytes,
-                     "ms_per_launch": attn_full_ms, "peak_source": peak_src,
-                     "share_of_step": phase["full_cache_layers"] / step_ms_attr}
-    flag_extra_ms = sum(t_flg) - len(t_flg) * mean(t_unf)
-    gather_gbs = h2d_bytes / (flag_extra_ms / 1e3) / 1e9 if flag_extra_ms > 0 else 0.0
-    roofline_gather = {"kernel": "layer_kernel flagged-launch excess (score/select + host gather)", "bound": "host_link",
-                       "achieved": gather_gbs, "peak": host_link_gbs, "unit": "GB/s",
-                       "frac": gather_gbs / host_link_gbs if host_link_gbs else None,
-                       "traffic": h2d_bytes / max(A, 1),
-                       "share_of_step": phase["retrieval_layers_flagged"] / step_ms_attr,
-                       "peak_source": "pinned 256 MiB cudaMemcpy H2D measured in this run"}
-    # The retrieval-layer kernel's binding roofline is the host link, not HBM: per launch it moves
-    # ret_bytes through HBM (~1 us at peak) but h2d_bytes / launches over PCIe (several us at peak).
-    n_launch = max(len(t_unf) + len(t_flg), 1)
-    link_bytes = h2d_bytes / n_launch
-    link_gbs = link_bytes / (ret_ms / 1e3) / 1e9
-    roofline = {"kernel": roofline_layer["kernel"], "bound": "host_link", "achieved": link_gbs,
-                "peak": host_link_gbs, "unit": "GB/s", "frac": link_gbs / host_link_gbs if host_link_gbs else None,
-                "traffic": None, "bytes_per_launch": link_bytes, "ms_per_launch": ret_ms,
-                "traffic_note": "host-link bytes are counted by the kernel itself (stats bytes_h2d); the kernel's "
-                                "DRAM traffic per launch (ncu --set full, profiles/r01_traffic.json, weighted by this "
-                                "run's flagged/unflagged mix) is roofline_layer_hbm.traffic",
-                "lower_bound_us": {"hbm": ret_bytes / (hbm_peak * 1e9) * 1e6,
-                                   "host_link": link_bytes / (host_link_gbs * 1e9) * 1e6 if host_link_gbs else None},
-                "peak_source": "pinned 256 MiB cudaMemcpy H2D measured in this run",
-                "share_of_step": roofline_layer["share_of_step"]}
-    retr_ms_total = flag_extra_ms
+                att_rows += min(cfg.sink_tokens, P_) + nws + max(0, t_end - int(sizes[kc:].sum()))
+    att_bytes_launch = att_rows / max(len(ret_layers), 1) * 512
+    ret_bytes = att_bytes_launch * n_ret_launch + stats_timed["units_scored"] * 256 + stats_timed["bytes_h2d"]
+    # working-set rows written per retrieval (upper bound: B rows per (sequence, owned head))
+    ws_rebuild = stats_timed["retrievals"] * hc * cfg.budget_tokens * 512
+    ret_bytes += ws_rebuild
+    ret_gbs = ret_bytes / (ret_ms_step * K / 1e3) / 1e9
+    link_bytes = stats_timed["bytes_h2d"]
+    link_gbs = link_bytes / (ret_ms_step * K / 1e3) / 1e9
+    full_bytes_launch = b * hc * (P_ + s0 + K // 2) * 2 * d * 2
+    full_gbs = full_bytes_launch / (full_ms / 1e3) / 1e9 if full_ms > 0 else 0.0
+    share_ret, share_full = ret_ms_step / ms_step, full_ms_step / ms_step
+    roof_layer_link = {"kernel": "layer_kernel (retrieval layers: trigger + score/select + host gather + append + "
+                                 "attention, one clustered launch)",
+                       "bound": "host_link", "achieved": link_gbs, "peak": host_link_gbs, "unit": "GB/s",
+                       "frac": link_gbs / host_link_gbs if host_link_gbs else None, "traffic": None,
+                       "bytes_per_launch": link_bytes / max(n_ret_launch, 1),
+                       "ms_per_launch": ret_ms_step / max(len(ret_layers), 1),
+                       "peak_source": "pinned 256 MiB cudaMemcpy H2D measured in this run",
+                       "share_of_step": share_ret,
+                       "note": "timed window: host-pool bytes the gathers read (kernel stats) / the retrieval "
+                               "layers' share of the timed step time"}
+    roof_layer_hbm = {"kernel": roof_layer_link["kernel"], "bound": "hbm", "achieved": ret_gbs, "peak": hbm_peak,
+                      "unit": "GB/s", "frac": ret_gbs / hbm_peak, "traffic": None,
+                      "bytes_per_launch": ret_bytes / max(n_ret_launch, 1),
+                      "ms_per_launch": ret_ms_step / max(len(ret_layers), 1), "peak_source": peak_src,
+                      "share_of_step": share_ret}
+    roof_full = {"kernel": "attn_full_tc_kernel (full-cache layers: store_cache + split-K flash-decode, one launch)",
+                 "bound": "hbm", "achieved": full_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": full_gbs / hbm_peak,
+                 "traffic": None, "bytes_per_launch": full_bytes_launch, "ms_per_launch": full_ms,
+                 "peak_source": peak_src, "share_of_step": share_full}
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(cfg.name, {})
+    except Exception:
+        tr = {}
+    if "attn_full_tc_kernel" in tr:
+        roof_full["traffic"] = tr["attn_full_tc_kernel"]
+    if "layer_kernel" in tr:
+        roof_layer_hbm["traffic"] = tr["layer_kernel"]
+    dominant = roof_full if share_full > share_ret else roof_layer_link
+    # k-means: the assignment GEMM (tensor pipe) and the Lloyd loop, from the phase timer
+    lloyd_ms = pt["init_ms"] + pt["assign_ms"] + pt["sort_ms"] + pt["update_ms"]
+    gemm_tf = pt["assign_flops"] / (pt["assign_ms"] / 1e3) / 1e12 if pt["assign_ms"] > 0 else 0.0
+    tf_sus = peaks.get("bf16_tflops_sustained", 1364.5)
+    tf_burst = peaks.get("bf16_tflops", 1604.9)
+    roof_km = {"kernel": "kmeans_assign_tc_kernel (tcgen05 GEMM X.C^T + fused argmax epilogue)", "bound": "tensor",
+               "achieved": gemm_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": gemm_tf / tf_sus,
+               "frac_of_burst_peak": gemm_tf / tf_burst, "traffic": None,
+               "flops": pt["assign_flops"], "ms": pt["assign_ms"], "passes": pt["assign_passes"],
+               "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (the prefill runs for tens of ms to "
+                              "seconds); frac_of_burst_peak against bf16_tflops",
+               "note": "algorithmic flops 2 N k d per instance-iteration / device time of the assignment passes "
+                       "(CUDA events of the library's prefill phase timer)"}
+    kmeans = {"keys_per_s_lloyd": pt["keys"] / (lloyd_ms / 1e3) if lloyd_ms > 0 else None,
+              "keys_per_s_incl_offload_staging": km_keys * jobs / (km_ms_calls / 1e3) if km_ms_calls > 0 else None,
+              "iters": cfg.kmeans_iters, "keys": pt["keys"],
+              "phase_ms": {k_: pt[k_] for k_ in ("init_ms", "assign_ms", "sort_ms", "update_ms", "stage_ms", "d2h_ms")},
+              "non_gemm_share_of_iteration": (pt["sort_ms"] + pt["update_ms"]) / max(pt["assign_ms"] + pt["sort_ms"] +
+                                                                                    pt["update_ms"], 1e-9),
+              "offload": {"bytes": pt["d2h_bytes"], "d2h_ms": pt["d2h_ms"],
+                          "gbs": pt["d2h_bytes"] / (pt["d2h_ms"] / 1e3) / 1e9 if pt["d2h_ms"] > 0 else None,
+                          "note": "copy-engine D2H of the cluster-major rows into the pinned pool, on the "
+                                  "library's copy stream (overlaps the next layer's clustering)"},
+              "impl": "tcgen05" if args.kmeans_impl == 0 else "simt"}
 
-    retrievals = st_b["retrievals"] - st_a["retrievals"]
-    n_ret_layers = L - len(full)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if heads else "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, planted clusters/segments; no weights on this path)",
-        "config": {"workload": f"{cfg.name}: Llama-3.1-8B attention shape (L=32, Hq=32, Hkv=8, d=128), "
-                               f"{cfg.prompt_len}-token prompt, S={cfg.sink_tokens} W={cfg.window_tokens} "
-                               f"B={cfg.budget_tokens} tau={cfg.tau} c={cfg.avg_cluster_size}, layers 0-1 full cache",
-                   "global_batch": b * jobs, "seq_len": cfg.prompt_len,
-                   "parallelism": (f"kv-head shard x{world} (heads [{hb}, {hb + hc}) on rank {rank}; NCCL "
-                                   f"all-gather of the per-head outputs after every layer)") if heads else
-                                  f"weak dp{world} (independent sequences per rank, no collective)",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded; k/4 planted key groups scattered over positions, planted query segments; "
+                "no weights on this path)",
+        "config": {"workload": workload_label(cfg), "global_batch": b * jobs, "seq_len": cfg.prompt_len,
+                   "decode_window": f"steps t = {s0 + 1}..{s0 + K} of the generation (after {W} warm-up steps)",
+                   "capacity_max_output_len": cap_out,
+                   "parallelism": (f"kv-head shard x{world} (heads [{hb}, {hb + hc}) on rank {rank}; NCCL all-gather "
+                                   f"of the per-head outputs {'per layer' if args.gather == 'layer' else 'once per step'})")
+                   if heads else f"weak dp{world} (independent sequences per rank, no collective)",
                    "l2": (f"inputs larger than L2: {kv_step_bytes / 1e6:.0f} MB of KV read per step per rank > 2 x 126 MB"
                           if flush_buf is None else
-                          f"L2 flushed between steps ({kv_step_bytes / 1e6:.0f} MB of KV per step per rank; "
-                          f"per-step event pairs, flush outside the timed spans)"),
+                          f"L2 flushed between steps ({kv_step_bytes / 1e6:.0f} MB of KV per step per rank)"),
                    "cuda_graph": True},
         "e2e": e2e,
-        "gpu_launches": launches_per_step * K,
+        "gpu_launches": L * K,
         "clocks": clk,
-        "roofline": roofline,
-        "roofline_layer_hbm": roofline_layer,
-        "roofline_full_cache": roofline_attn,
-        "roofline_gather": roofline_gather,
-        "phases_ms_per_step": phase,
+        "roofline": dominant,
+        "roofline_layer_link": roof_layer_link,
+        "roofline_layer_hbm": roof_layer_hbm,
+        "roofline_full_cache": roof_full,
+        "roofline_kmeans": roof_km,
+        "kmeans_keys_per_s": kmeans["keys_per_s_lloyd"],
+        "kmeans": kmeans,
         "layer_us": layer_us,
-        "kmeans_keys_per_s": km_keys / (km_ms / 1e3) if km_ms > 0 else None,
-        "kmeans": {"ms_total": km_ms, "keys": km_keys, "iters": cfg.kmeans_iters,
-                   "impl": "tcgen05" if args.kmeans_impl == 0 else "simt",
-                   "timed": "all layers' cluster_prompt (k-means + cluster-major offload to the pinned pool; full-cache "
-                            "layers: device copy) up to louiskv_prompt_fence, one event pair",
-                   "prompt_offload_bytes": st0["bytes_d2h"],
-                   "prompt_offload_gbs": st0["bytes_d2h"] / (km_ms / 1e3) / 1e9 if km_ms > 0 else None},
-        "retrieve_us_per_step": {"per_flagged_layer_call": (retr_ms_total * 1e3 / max(1, st_d['retrievals'] - st_c['retrievals'])),
-                                 "amortized_per_step": flag_extra_ms * 1e3 / max(A, 1)},
-        "retrievals_per_step": retrievals / K / max(n_ret_layers, 1) / b,
-        "stats_timed": {k_: st_b[k_] - st_a[k_] for k_ in st_b},
+        "phases_ms_per_step": {"retrieval_layers": ret_ms_step, "full_cache_layers": full_ms_step,
+                               "retrieval_layers_attribution": ret_ms_attr},
+        "retrieve_us_per_step": {"per_flagged_launch_excess": (f_ms - u_ms) * 1e3,
+                                 "amortized_per_step": (f_ms - u_ms) * 1e3 * n_flg_tot / K},
+        "retrievals_per_layer_step": stats_timed["retrievals"] / K / max(len(ret_layers), 1) / b,
+        "stats_timed": stats_timed,
+        "l2_pressure": l2v,
         "host_link_h2d_gbs": host_link_gbs,
-        "memory": dict(ctx.memory(), full_kv_bytes=b * hc * L * (cfg.prompt_len + T) * 512,
-                       note="device_bytes: every device allocation of the context (sinks, working sets, local "
-                            "buffers, centroids, unit tables, the two full-cache layers, scratch); full_kv_bytes: "
-                            "the K+V bf16 of every layer at P + max decode steps (a full-cache engine's device "
-                            "footprint); the offloaded rows live in the pinned host pool (P:404-425)"),
+        "memory": dict(ctx.memory(), full_kv_bytes=b * hc * L * (cfg.prompt_len + cap_out) * 512,
+                       note="device_bytes: every device allocation of the context; full_kv_bytes: the K+V bf16 of "
+                            "every layer at P + capacity (a full-cache engine's device footprint); the offloaded "
+                            "rows live in the pinned host pool (P:404-425)"),
     }
-
+    ctx.close()
+    del graph
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s = oracle_sample(cfg, args.seed, args.cpu_steps)
-        line["cpu_baseline"] = {"value": b / s["step_s"], "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": (f"{args.cpu_steps} decode steps of 1 retrieval-layer instance (1 KV head, "
-                                           f"{g} q heads) + 1 full-cache instance at {cfg.name} sizes, extrapolated "
-                                           f"x{s['n_ret']} / x{s['n_full']} instances to one 32-layer step")}
+        line["cpu_baseline"] = cpu_baseline(cfg, args.seed)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -232,6 +232,43 @@ louiskv_status louiskv_get_stats(louiskv_ctx* ctx, louiskv_stats* out);
  * tables, full-cache layers, scratch) and the pinned host-pool bytes. Either pointer may be NULL.
  * No synchronisation. Errors: INVALID_ARG (null ctx). */
 louiskv_status louiskv_get_memory(const louiskv_ctx* ctx, uint64_t* device_bytes, uint64_t* host_pool_bytes);
+
+/* ---- prefill phase timer (the per-phase breakdown of cluster_prompt; SURVEY §5 tracing) ----
+ * When enabled, every later cluster_prompt records stream-ordered CUDA events between its phases:
+ * init (sinks, centroid init), assign (the tcgen05 assignment GEMM + fused argmax, one per Lloyd
+ * iteration), sort (cluster histogram, scan, empty-cluster repair, stable scatter), update (centroid
+ * means), stage (cluster-major permute into the device staging buffer + unit table) and, on the
+ * library's copy stream, the D2H copies into the pinned pool. Times are device elapsed times between
+ * consecutive marks (the phases run back to back on the caller's stream). Costs one event record per
+ * phase boundary; off by default. */
+typedef struct {
+  double init_ms, assign_ms, sort_ms, update_ms, stage_ms, d2h_ms;
+  uint64_t assign_flops;   /* algorithmic: 2 * N * k * d per instance per assignment pass */
+  uint64_t keys;           /* clustered keys (N per instance per cluster_prompt call) */
+  uint64_t d2h_bytes;      /* bytes copied into the host pool */
+  uint64_t assign_passes;  /* assignment passes (Lloyd iterations x calls) */
+  int32_t calls;           /* cluster_prompt calls timed */
+} louiskv_prefill_times;
+/* Enable (1) / disable (0) the timer and reset its accumulators. Synchronises the device.
+ * Errors: INVALID_ARG, CUDA. */
+louiskv_status louiskv_set_prefill_timing(louiskv_ctx* ctx, int32_t enable);
+/* Accumulated phase times since the last set_prefill_timing. Synchronises the device.
+ * Errors: INVALID_ARG (null out), CUDA. */
+louiskv_status louiskv_get_prefill_times(louiskv_ctx* ctx, louiskv_prefill_times* out);
+
+/* ---- decode-state checkpoint (device resident) ----
+ * state_save copies, stream-ordered on `stream`, every device buffer the decode path mutates
+ * (instance states, selections, both working-set buffers, local buffers and segment FIFOs, q_ref,
+ * flags, r, step counters, pending gather jobs, stats counters) into checkpoint buffers owned by the
+ * context (allocated on the first save). state_restore copies them back and restores the host-side
+ * step counters, so the decode continues exactly from the saved step (rows appended to unit tables,
+ * the host pool or the full cache after the save are beyond the restored counters and get rewritten).
+ * Use: replaying the same decode steps (e.g. A/B measurement, speculative-decoding rollback).
+ * Must be called between steps (every layer's step complete) after cluster_prompt on every layer.
+ * Errors: STATE (no prefill / inside a step / restore without save), OOM_DEVICE, CUDA. */
+louiskv_status louiskv_state_save(louiskv_ctx* ctx, void* stream);
+louiskv_status louiskv_state_restore(louiskv_ctx* ctx, void* stream);
+
 const char* louiskv_last_error(const louiskv_ctx* ctx);
 /* Library build string (arch, version). */
 const char* louiskv_version(void);

@@ -32,7 +32,8 @@ SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louis
            "louiskv_should_retrieve", "louiskv_retrieve", "louiskv_append_output", "louiskv_sparse_attn",
            "louiskv_append_attn", "louiskv_decode_layer",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
-           "louiskv_get_stats", "louiskv_get_memory", "louiskv_last_error", "louiskv_version"]
+           "louiskv_get_stats", "louiskv_get_memory", "louiskv_set_prefill_timing", "louiskv_get_prefill_times",
+           "louiskv_state_save", "louiskv_state_restore", "louiskv_last_error", "louiskv_version"]
 
 
 class LouisKVError(RuntimeError):
@@ -60,6 +61,16 @@ class Stats(ctypes.Structure):
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class PrefillTimes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("init_ms", "assign_ms", "sort_ms", "update_ms", "stage_ms", "d2h_ms")] + \
+               [(n, ctypes.c_uint64) for n in ("assign_flops", "keys", "d2h_bytes", "assign_passes")] + \
+               [("calls", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {n: (float(getattr(self, n)) if t is ctypes.c_double else int(getattr(self, n)))
+                for n, t in self._fields_}
 
 
 _lib = None
@@ -92,6 +103,10 @@ def lib():
         L.louiskv_get_working_set.argtypes = [vp, i32, i32, i32, vp, vp, i32, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
         L.louiskv_get_memory.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+        L.louiskv_set_prefill_timing.argtypes = [vp, i32]
+        L.louiskv_get_prefill_times.argtypes = [vp, ctypes.POINTER(PrefillTimes)]
+        L.louiskv_state_save.argtypes = [vp, vp]
+        L.louiskv_state_restore.argtypes = [vp, vp]
         L.louiskv_last_error.argtypes = [vp]
         L.louiskv_last_error.restype = ctypes.c_char_p
         L.louiskv_version.restype = ctypes.c_char_p
@@ -259,6 +274,22 @@ class Context:
         d, h = ctypes.c_uint64(), ctypes.c_uint64()
         self._chk(self._L.louiskv_get_memory(self.h, ctypes.byref(d), ctypes.byref(h)))
         return {"device_bytes": d.value, "host_pool_bytes": h.value}
+
+    def set_prefill_timing(self, enable: bool = True):
+        """Enable/disable (and reset) the cluster_prompt phase timer (louiskv_set_prefill_timing)."""
+        self._chk(self._L.louiskv_set_prefill_timing(self.h, 1 if enable else 0))
+
+    def prefill_times(self) -> dict:
+        t = PrefillTimes()
+        self._chk(self._L.louiskv_get_prefill_times(self.h, ctypes.byref(t)))
+        return t.as_dict()
+
+    def state_save(self, stream=None):
+        """Checkpoint the decode state (device resident, stream ordered)."""
+        self._chk(self._L.louiskv_state_save(self.h, _stream(stream)))
+
+    def state_restore(self, stream=None):
+        self._chk(self._L.louiskv_state_restore(self.h, _stream(stream)))
 
     def stats(self) -> dict:
         s = Stats()

@@ -84,6 +84,17 @@ struct louiskv_ctx {
   int last_layer = -1;  // layer of the last launch when it was a one-launch layer step, else -1
   void* last_stream = nullptr;  // ... and the stream it went to
   uint64_t dev_bytes = 0, host_bytes = 0;  // louiskv_get_memory
+  PhaseRec prec;                            // louiskv_set_prefill_timing
+  // decode-state checkpoint (louiskv_state_save / _restore): device copies of every buffer the decode
+  // path writes that is not dead beyond the saved counters
+  struct SnapBuf {
+    void* src;
+    size_t bytes;
+    void* dst;
+  };
+  std::vector<SnapBuf> snap;
+  bool snap_valid = false;
+  std::vector<int> snap_t, snap_stage;
   std::string err;
   bool sticky = false;
 };
@@ -271,6 +282,10 @@ void louiskv_destroy(louiskv_ctx* ctx) {
   for (cudaEvent_t e : {ctx->ev_free[0], ctx->ev_free[1], ctx->ev_staged})
     if (e) cudaEventDestroy(e);
   if (ctx->off_stream) cudaStreamDestroy(ctx->off_stream);
+  for (cudaEvent_t e : ctx->prec.pool)
+    if (e) cudaEventDestroy(e);
+  for (auto& sb : ctx->snap)
+    if (sb.dst) cudaFree(sb.dst);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->h_pool) cudaFreeHost(ctx->h_pool);
   delete ctx;
@@ -434,6 +449,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
 static cudaError_t offload_prompt(louiskv_ctx* c, int layer, const KmArgs& a, cudaStream_t st) {
   cudaError_t e;
   const int ni = a.batch * a.hn;
+  c->prec.mark(st, PH_STAGE);
   if (a.N > 0 && a.kc > 0) {
     const int64_t inst_b = (int64_t)a.N * POOL_ROW_BYTES;
     const int per = (int)std::max<int64_t>(1, std::min<int64_t>(ni, c->stage_bytes / inst_b));
@@ -446,15 +462,23 @@ static cudaError_t offload_prompt(louiskv_ctx* c, int layer, const KmArgs& a, cu
       if ((e = launch_km_offload(a, li0, nli, c->d_stage[buf], inst_b, st)) != cudaSuccess) return e;
       if ((e = cudaEventRecord(c->ev_staged, st)) != cudaSuccess) return e;
       if ((e = cudaStreamWaitEvent(c->off_stream, c->ev_staged, 0)) != cudaSuccess) return e;
+      cudaEvent_t d0 = nullptr, d1 = nullptr;
+      if (c->prec.on && (d0 = c->prec.ev()) && (d1 = c->prec.ev())) cudaEventRecord(d0, c->off_stream);
       if ((e = cudaMemcpy2DAsync(c->h_pool + (ib + li0) * c->pool_inst_bytes, (size_t)c->pool_inst_bytes,
                                  c->d_stage[buf], (size_t)inst_b, (size_t)inst_b, (size_t)nli,
                                  cudaMemcpyDeviceToHost, c->off_stream)) != cudaSuccess)
         return e;
+      if (d0 && d1) {
+        cudaEventRecord(d1, c->off_stream);
+        c->prec.d2h.push_back({d0, d1});
+        c->prec.d2h_bytes += (uint64_t)inst_b * nli;
+      }
       if ((e = cudaEventRecord(c->ev_free[buf], c->off_stream)) != cudaSuccess) return e;
       c->stage_used[buf] = true;
     }
     if ((e = launch_km_units(a, st)) != cudaSuccess) return e;
   }
+  c->prec.mark(st, PH_END);
   if ((e = cudaEventRecord(c->ev_done[layer], c->off_stream)) != cudaSuccess) return e;
   c->off_pending[layer] = 1;
   return cudaSuccess;
@@ -566,6 +590,12 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
     cudaMemcpy(d_ec, h_cent, nc * 4, cudaMemcpyHostToDevice);
     a.ext_assign = d_ea;
     a.ext_cent = d_ec;
+  }
+  if (c->prec.on) {
+    a.rec = &c->prec;
+    c->prec.mark(st, PH_INIT);
+    c->prec.keys += (uint64_t)batch * c->hn * N;
+    c->prec.calls += 1;
   }
   cudaError_t e = run_kmeans_prompt(a, st, &c->km_tc_iters, &c->km_simt_iters);
   if (e == cudaSuccess) e = offload_prompt(c, layer, a, st);
@@ -862,6 +892,114 @@ louiskv_status louiskv_get_working_set(louiskv_ctx* c, int32_t layer, int32_t b,
   if (k_rows && m) cudaMemcpy(k_rows, K, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
   if (v_rows && m) cudaMemcpy(v_rows, V, sizeof(bf16) * m * D, cudaMemcpyDeviceToHost);
   if (n_rows) *n_rows = is.ws_rows;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_set_prefill_timing(louiskv_ctx* c, int32_t enable) {
+  LKV_CHECK_CTX(c);
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "set_prefill_timing");
+  PhaseRec& r = c->prec;
+  r.on = enable != 0;
+  r.marks.clear();
+  r.d2h.clear();
+  r.used = 0;
+  r.assign_flops = r.keys = r.d2h_bytes = r.assign_passes = 0;
+  r.calls = 0;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_prefill_times(louiskv_ctx* c, louiskv_prefill_times* out) {
+  LKV_CHECK_CTX(c);
+  if (!out) return fail(c, LOUISKV_ERR_INVALID_ARG, "get_prefill_times: null");
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "get_prefill_times");
+  const PhaseRec& r = c->prec;
+  double acc[PH_N] = {0};
+  for (size_t i = 0; i + 1 < r.marks.size(); ++i) {
+    if (r.marks[i].first == PH_END) continue;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.marks[i].second, r.marks[i + 1].second) != cudaSuccess)
+      return cuda_fail(c, cudaGetLastError(), "get_prefill_times: events");
+    acc[r.marks[i].first] += ms;
+  }
+  double d2h = 0.0;
+  for (const auto& pr : r.d2h) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) d2h += ms;
+  }
+  *out = louiskv_prefill_times{};
+  out->init_ms = acc[PH_INIT];
+  out->assign_ms = acc[PH_ASSIGN];
+  out->sort_ms = acc[PH_SORT];
+  out->update_ms = acc[PH_UPDATE];
+  out->stage_ms = acc[PH_STAGE];
+  out->d2h_ms = d2h;
+  out->assign_flops = r.assign_flops;
+  out->keys = r.keys;
+  out->d2h_bytes = r.d2h_bytes;
+  out->assign_passes = r.assign_passes;
+  out->calls = r.calls;
+  return LOUISKV_OK;
+}
+
+// decode-state checkpoint: everything the decode path writes whose validity is not bounded by the
+// saved instance counters (rows appended beyond n_units / pool_rows / the full-cache step are dead
+// after a restore and are rewritten by the next steps)
+static void snap_list(louiskv_ctx* c, std::vector<std::pair<void*, size_t>>& v) {
+  const int64_t ni = c->n_inst, nl = c->inst_per_layer;
+  v.push_back({c->d_inst, sizeof(InstState) * (size_t)std::max<int64_t>(ni, 1)});
+  v.push_back({c->d_sel, (size_t)std::max<int64_t>(ni, 1) * c->Umax});
+  v.push_back({c->d_seloff, sizeof(int32_t) * (size_t)std::max<int64_t>(ni, 1) * c->Umax});
+  v.push_back({c->d_ws, sizeof(bf16) * (size_t)2 * c->ws_buf_stride});
+  v.push_back({c->d_ring, sizeof(bf16) * (size_t)std::max<int64_t>(ni, 1) * 2 * c->ring_cap * D});
+  v.push_back({c->d_fifo, sizeof(int2) * (size_t)std::max<int64_t>(ni, 1) * c->ring_cap});
+  v.push_back({c->d_flag, (size_t)c->L * c->Bmax});
+  v.push_back({c->d_r, sizeof(double) * (size_t)c->L * c->Bmax});
+  v.push_back({c->d_qref, sizeof(bf16) * (size_t)c->L * 2 * c->Bmax * c->Hq * D});
+  v.push_back({c->d_step, sizeof(int) * (size_t)c->L});
+  v.push_back({c->d_jobs, sizeof(GatherJob) * (size_t)c->L * nl});
+  v.push_back({c->d_stats, sizeof(StatsDev)});
+  v.push_back({c->d_error, sizeof(int)});
+}
+
+louiskv_status louiskv_state_save(louiskv_ctx* c, void* stream) {
+  LKV_CHECK_CTX(c);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int l = 0; l < c->L; ++l) {
+    if (c->P[l] < 0) return fail(c, LOUISKV_ERR_STATE, "state_save before cluster_prompt on every layer");
+    if (c->stage[l] != 0 && c->stage[l] != 3) return fail(c, LOUISKV_ERR_STATE, "state_save inside a step");
+    LKV_LAUNCH(c, offload_wait(c, l, st), "state_save: prompt offload wait");
+  }
+  std::vector<std::pair<void*, size_t>> v;
+  snap_list(c, v);
+  if (c->snap.empty()) {
+    for (auto& pr : v) {
+      void* d = nullptr;
+      if (cudaMalloc(&d, pr.second) != cudaSuccess) {
+        cudaGetLastError();
+        for (auto& sb : c->snap) cudaFree(sb.dst);
+        c->snap.clear();
+        return fail(c, LOUISKV_ERR_OOM_DEVICE, "state_save: checkpoint buffers");
+      }
+      c->snap.push_back({pr.first, pr.second, d});
+    }
+  }
+  for (auto& sb : c->snap)
+    LKV_LAUNCH(c, cudaMemcpyAsync(sb.dst, sb.src, sb.bytes, cudaMemcpyDeviceToDevice, st), "state_save copy");
+  c->snap_t = c->t;
+  c->snap_stage = c->stage;
+  c->snap_valid = true;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_state_restore(louiskv_ctx* c, void* stream) {
+  LKV_CHECK_CTX(c);
+  if (!c->snap_valid) return fail(c, LOUISKV_ERR_STATE, "state_restore without state_save");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (auto& sb : c->snap)
+    LKV_LAUNCH(c, cudaMemcpyAsync(sb.src, sb.dst, sb.bytes, cudaMemcpyDeviceToDevice, st), "state_restore copy");
+  c->t = c->snap_t;
+  c->stage = c->snap_stage;
+  c->last_layer = -1;
   return LOUISKV_OK;
 }
 

@@ -751,6 +751,11 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
     launch_k(km_init_kernel, dim3(gk), dim3(128), 0, st, a);
     launch_k(km_half_pad_kernel, dim3(dim3(1, ni)), dim3(256), 0, st, a);
     for (int it = 0; it < a.iters; ++it) {
+      if (a.rec) {
+        a.rec->mark(st, PH_ASSIGN);
+        a.rec->assign_flops += (uint64_t)ni * a.N * a.kc * 2ull * D;
+        a.rec->assign_passes += 1;
+      }
       bool done = false;
       if (a.impl == LOUISKV_KMEANS_TC && kmeans_tc_available()) {
         e = launch_assign_tc(a, st);
@@ -760,7 +765,9 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
       }
       if (!done) launch_k(km_assign_simt_kernel, dim3(dim3((a.N + 127) / 128, ni)), dim3(128), 0, st, a);
       ++*(done ? tc_iters : simt_iters);
+      if (a.rec) a.rec->mark(st, PH_SORT);
       if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
+      if (a.rec) a.rec->mark(st, PH_UPDATE);
       launch_k(km_update_kernel, dim3(dim3((a.task_max + 3) / 4, ni)), dim3(128), 0, st, a);
       launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
     }

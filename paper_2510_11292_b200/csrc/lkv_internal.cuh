@@ -193,6 +193,32 @@ constexpr int LAYER_REP_UNITS = 8192;
 constexpr int LAYER_REP_SEL = 1024;
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st);
 
+// Prefill phase timer (louiskv_set_prefill_timing): stream-ordered CUDA events between the phases of
+// cluster_prompt; the time from one mark to the next is charged to the earlier mark's phase.
+enum { PH_INIT = 0, PH_ASSIGN, PH_SORT, PH_UPDATE, PH_STAGE, PH_END, PH_N };
+struct PhaseRec {
+  bool on = false;
+  std::vector<std::pair<int, cudaEvent_t>> marks;       // main (caller) stream
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> d2h;  // copy-engine offload on the library's stream
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  uint64_t assign_flops = 0, keys = 0, d2h_bytes = 0, assign_passes = 0;
+  int calls = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void mark(cudaStream_t st, int ph) {
+    if (!on) return;
+    cudaEvent_t e = ev();
+    if (e && cudaEventRecord(e, st) == cudaSuccess) marks.push_back({ph, e});
+  }
+};
+
 // k-means / prompt (k_kmeans.cu)
 struct KmArgs {
   const bf16* k;
@@ -236,6 +262,7 @@ struct KmArgs {
   const int32_t* ext_assign;   // device copy of caller-provided assignment (set_prompt_units)
   const float* ext_cent;       // device copy of caller-provided centroids
   int page;                    // > 0: page units of `page` tokens (LOUISKV_UNITS_PAGES), no k-means
+  PhaseRec* rec;               // optional phase timer (null: no events)
 };
 // tc_iters / simt_iters: host counters of which assignment kernel ran
 cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_iters, uint64_t* simt_iters);

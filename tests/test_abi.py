@@ -46,9 +46,10 @@ def test_ctypes_struct_layout_matches_c(lkv):
 #include <stddef.h>
 #include "louiskv.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
          offsetof(louiskv_config, full_cache_layers), offsetof(louiskv_config, device),
-         sizeof(louiskv_stats), offsetof(louiskv_stats, segments_evicted));
+         sizeof(louiskv_stats), offsetof(louiskv_stats, segments_evicted), sizeof(louiskv_prefill_times),
+         offsetof(louiskv_prefill_times, assign_flops), offsetof(louiskv_prefill_times, calls));
   return 0;
 }
 '''
@@ -58,9 +59,10 @@ int main(void) {
         exe = os.path.join(d, "t")
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
         vals = list(map(int, subprocess.check_output([exe]).split()))
-    C, S = lkv.Config, lkv.Stats
+    C, S, T = lkv.Config, lkv.Stats, lkv.PrefillTimes
     assert vals == [ctypes.sizeof(C), C.tau.offset, C.full_cache_layers.offset, C.device.offset,
-                    ctypes.sizeof(S), S.segments_evicted.offset]
+                    ctypes.sizeof(S), S.segments_evicted.offset, ctypes.sizeof(T), T.assign_flops.offset,
+                    T.calls.offset]
 
 
 def test_invalid_config_rejected_synchronously(lkv):
@@ -73,6 +75,10 @@ def test_invalid_config_rejected_synchronously(lkv):
     bad.num_q_heads = 3  # not a multiple of num_kv_heads... (3 % 1 == 0 but g=3 unsupported)
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     assert L.louiskv_create(None, ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    bad.num_q_heads = 128  # both trigger paths hold at most 64 query heads
+    bad.num_kv_heads = 16
+    assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    assert L.louiskv_state_restore(None, None) == lkv.ERR_INVALID_ARG
     assert L.louiskv_cluster_prompt(None, 0, None, None, 0, 0, 0, 1, 1, None) == lkv.ERR_INVALID_ARG
 
 
