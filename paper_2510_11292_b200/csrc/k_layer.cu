@@ -71,14 +71,24 @@ constexpr int LK_REP_SEL = LAYER_REP_SEL;  // selected units (<= min(n, B))
 // then the tail candidates, then the selected-unit LIST
 __host__ __device__ constexpr int rep_off_tk(int n) { return (6 * n + 15) & ~15; }
 __host__ __device__ constexpr int rep_off_x(int n) { return (rep_off_tk(n) + ((n + 31) / 32) * 4 + 15) & ~15; }
-constexpr int REP_X_MIN = AT_STAGES * AT_STAGE_BYTES - rep_off_x(LK_REP_N);
+// The layer kernel runs one CTA per SM (register budget), so it takes a large dynamic shared-memory
+// arena: the attention ring uses its first AT_STAGES x 32 KB, the select (which runs while no
+// attention load is in flight) all of it.
+constexpr int LK_SMEM = 192 * 1024;
+static_assert(LK_SMEM >= AT_SMEM, "layer arena");
+constexpr int REP_X_MIN = LK_SMEM - rep_off_x(LK_REP_N);
 struct SelEnt {  // one selected unit, in id (= destination) order
   int dst, sz, u, pad;
   const uint8_t* kb;  // first K row (current working set, or the host pool span)
   const uint8_t* vb;
 };
 static_assert(LK_REP_SEL * (int)sizeof(SelEnt) <= REP_X_MIN, "rep LIST smem");
-static_assert(8 * (LK_REP_N / AT_CL) * 4 <= REP_X_MIN, "rep E smem");
+static_assert(8 * (LK_REP_N / 8) * 4 <= REP_X_MIN, "rep E smem (CL = 8)");
+// shared-memory select possible for n units with G heads over CL ranks: the replicated arrays, the
+// rank's logits E and at least 32 staged centroid rows fit the staging area (else big mode)
+__host__ __device__ constexpr bool rep_fits(int n, int G, int CL) {
+  return n <= LK_REP_N && LK_SMEM - rep_off_x(n) >= 4 * 64 * (ROW_BYTES + 16) + 0 * G * CL;
+}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -109,16 +119,16 @@ __device__ __forceinline__ int rep_x_offset(int n, bool big) {
 // Returns the row count of the new working set; *nsel = selected units (LIST entries, at shared
 // offset rep_x_offset(n, big)); own_dst[i] = destination row of own unit lo+i (-1: not selected) for
 // the deferred sel/seloff update.
-template <int G>
+template <int G, int CL>
 __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li, const int rank, const int n,
                                              const int ws_cur, const float (*sq)[D], uint8_t* dsm, int* nsel,
                                              int* own_dst, const bool big, unsigned long long* prof) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = (n + AT_CL - 1) / AT_CL;
+  const int m = (n + CL - 1) / CL;
   const int lo = min(n, rank * m), hi = min(n, lo + m), cnt = hi - lo;
-  const int off_x = rep_x_offset(n, big), x_bytes = AT_STAGES * AT_STAGE_BYTES - off_x;
+  const int off_x = rep_x_offset(n, big), x_bytes = LK_SMEM - off_x;
   uint8_t* gscr = big ? big_scratch(a, li) : nullptr;
   // [n] A bits (replicated in every rank's shared memory; big: one global copy)
   uint32_t* RA = big ? reinterpret_cast<uint32_t*>(gscr) : reinterpret_cast<uint32_t*>(dsm);
@@ -126,14 +136,24 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   uint16_t* SZ = big ? reinterpret_cast<uint16_t*>(gscr + 4 * (int64_t)a.Umax) : reinterpret_cast<uint16_t*>(dsm + 4 * n);
   uint32_t* TK = reinterpret_cast<uint32_t*>(dsm + (big ? 0 : rep_off_tk(n)));  // [n/32] taken bits (per rank)
   // [G][m] own logits / exps (big: this rank's slice of the per-instance logits scratch
-  // [G][Umax] floats; m <= Umax / 8 since Umax is a multiple of 256)
-  float* E = big ? a.scratch_e + (int64_t)li * G * a.Umax + (int64_t)rank * G * (a.Umax / AT_CL)
-                 : reinterpret_cast<float*>(dsm + off_x);
+  // [G][Umax] floats; m <= Umax / CL since Umax is a multiple of 256)
+  // Logits staging (below): up to 6 buffers of RB centroid rows after E (the own logits) in X; E
+  // moves to global scratch when that leaves room for more buffers
+  constexpr int PITCH = ROW_BYTES + 16;
+  constexpr int HPT = G < 2 ? G : 2;       // heads per thread: two independent fmaf chains (ILP 2)
+  constexpr int RB = AT_THREADS * HPT / G;  // rows per round: every thread busy
+  const int e_bytes_s = (G * m * 4 + 127) & ~127;
+  const int nb_s = big ? 0 : min(6, (x_bytes - e_bytes_s) / (RB * PITCH));
+  const int nb_g = min(6, x_bytes / (RB * PITCH));
+  const bool e_smem = nb_s >= 2 && nb_s >= min(nb_g, 4);
+  const int NBUF = e_smem ? nb_s : nb_g;  // (>= 2: rep_fits / big mode leave >= 4 x 64 rows of X)
+  float* E = e_smem ? reinterpret_cast<float*>(dsm + off_x)
+                    : a.scratch_e + (int64_t)li * G * a.Umax + (int64_t)rank * G * (a.Umax / CL);
   SelEnt* LIST = reinterpret_cast<SelEnt*>(dsm + off_x);       // (after E and the lists are dead)
 
   __shared__ float s_coef[7];
-  __shared__ float x_max[AT_CL][G];               // pushed by every rank
-  __shared__ unsigned long long x_z[AT_CL][G];    // pushed by every rank
+  __shared__ float x_max[CL][G];               // pushed by every rank
+  __shared__ unsigned long long x_z[CL][G];    // pushed by every rank
   __shared__ unsigned long long s_zl[G];
   __shared__ float s_red[LK_W][G];
   __shared__ float s_M[G], s_Z[G];
@@ -148,12 +168,16 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   for (int i = tid; i < (n + 31) / 32; i += AT_THREADS) TK[i] = 0u;
   for (int i = tid; i < cnt; i += AT_THREADS) own_dst[i] = -1;
   const int32_t* usize = a.usize + (int64_t)li * a.Umax;
-  // sizes: the first 8 x 256 loads stay in flight across the logits below
-  int szv[8];
+  // sizes (smem mode: all units; big mode: the own range), 4 per 16-B load: the first 4 x 256 loads
+  // (4096 units) stay in flight across the logits below, the rest is loaded in batches of 4 after
+  const int sz0 = big ? lo : 0, sz1 = big ? hi : n;          // (lo, hi multiples of 4? not in general:
+  const int q0 = sz0 >> 2, q1 = (sz1 + 3) >> 2;             //  whole 16-B words, clipped per element)
+  const int4* us4 = reinterpret_cast<const int4*>(usize);  // (a.usize rows are 1 KB aligned: Umax % 256 == 0)
+  int4 szv[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int u = i * AT_THREADS + tid;
-    szv[i] = u < n ? usize[u] : 0;
+  for (int i = 0; i < 4; ++i) {
+    const int q = q0 + i * AT_THREADS + tid;
+    szv[i] = q < q1 ? us4[q] : make_int4(0, 0, 0, 0);
   }
   prof_stamp(prof, 20);
 
@@ -165,43 +189,81 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
 #pragma unroll
   for (int j = 0; j < G; ++j) mymax[j] = -INFINITY;
   {
-    constexpr int PITCH = ROW_BYTES + 16;
-    const int e_bytes = big ? 0 : (G * m * 4 + 127) & ~127;
-    uint8_t* CS = dsm + off_x + e_bytes;
-    const int RB = min(cnt, max(32, ((x_bytes - e_bytes) / PITCH) & ~31));
+    // RB = 256 HPT / g rows per round, thread t scores row t % RB for heads [HPT hd, HPT hd + HPT),
+    // hd = t / RB (one sequential fmaf chain per (unit, head): recipe R2), NBUF buffers: NBUF - 1
+    // rounds of rows in flight while one is scored (an empty group is committed past the end, so the
+    // wait count is a constant)
+    uint8_t* CS = dsm + off_x + (e_smem ? e_bytes_s : 0);
     const uint32_t cs_s = (uint32_t)__cvta_generic_to_shared(CS);
+    const int row = tid % RB, hd = tid / RB;
+    const int nround = (cnt + RB - 1) / RB;
+    auto issue = [&](int r) {
+      if (r < nround) {
+        const int b0 = r * RB, nb = min(RB, cnt - b0);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(centb + (int64_t)(lo + b0) * D);
+        const uint32_t dst = cs_s + (uint32_t)((r % NBUF) * RB * PITCH);
+        for (int i = tid; i < nb * 16; i += AT_THREADS)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (i >> 4) * PITCH + (i & 15) * 16),
+                       "l"(src + (int64_t)i * 16)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 #pragma unroll 1
-    for (int b0 = 0; b0 < cnt; b0 += RB) {
-      const int nb = min(RB, cnt - b0);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(centb + (int64_t)(lo + b0) * D);
-      for (int i = tid; i < nb * 16; i += AT_THREADS)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cs_s + (i >> 4) * PITCH + (i & 15) * 16),
-                     "l"(src + (int64_t)i * 16)
-                     : "memory");
-      asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+    for (int r = 0; r < NBUF - 1; ++r) issue(r);
+#pragma unroll 1
+    for (int r = 0; r < nround; ++r) {
+      issue(r + NBUF - 1);  // into the buffer scored in round r - 1 (freed by its closing barrier)
+      switch (NBUF) {       // (the wait count is an immediate)
+        case 2: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+      }
       __syncthreads();
-#pragma unroll 1
-      for (int i = tid; i < nb; i += AT_THREADS) {
-        float l[G];
-        logits_row_smem<G>(sq, reinterpret_cast<const uint4*>(CS + i * PITCH), a.inv_sqrt_d, l);
+      const int b0 = r * RB, nb = min(RB, cnt - b0);
+      if (row < nb) {
+        const uint4* crow = reinterpret_cast<const uint4*>(CS + (r % NBUF) * RB * PITCH + row * PITCH);
+        float l[HPT];
+        logits_row_smem<HPT>(sq + hd * HPT, crow, a.inv_sqrt_d, l);
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          E[j * m + b0 + i] = l[j];
-          mymax[j] = fmaxf(mymax[j], l[j]);
-        }
+        for (int k = 0; k < HPT; ++k) E[(hd * HPT + k) * m + b0 + row] = l[k];
+        // (the heads' running maxima; compile-time indices only — no dynamically indexed registers)
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+          for (int k = 0; k < HPT; ++k)
+            if (j == hd * HPT + k) mymax[j] = fmaxf(mymax[j], l[k]);
       }
       __syncthreads();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
-  if (!big) {
+  {
+    auto put4 = [&](int q, const int4 v) {
+      const int u = 4 * q;
+      if (u >= sz0 && u < sz1) SZ[u] = (uint16_t)clamp16(v.x);
+      if (u + 1 >= sz0 && u + 1 < sz1) SZ[u + 1] = (uint16_t)clamp16(v.y);
+      if (u + 2 >= sz0 && u + 2 < sz1) SZ[u + 2] = (uint16_t)clamp16(v.z);
+      if (u + 3 >= sz0 && u + 3 < sz1) SZ[u + 3] = (uint16_t)clamp16(v.w);
+    };
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int u = i * AT_THREADS + tid;
-      if (u < n) SZ[u] = (uint16_t)clamp16(szv[i]);
+    for (int i = 0; i < 4; ++i) {
+      const int q = q0 + i * AT_THREADS + tid;
+      if (q < q1) put4(q, szv[i]);
     }
-    for (int u = 8 * AT_THREADS + tid; u < n; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
-  } else {
-    for (int u = lo + tid; u < hi; u += AT_THREADS) SZ[u] = (uint16_t)clamp16(usize[u]);
+    for (int qb = q0 + 4 * AT_THREADS + tid; qb < q1; qb += 4 * AT_THREADS) {
+      int4 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = qb + i * AT_THREADS;
+        v[i] = q < q1 ? us4[q] : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (qb + i * AT_THREADS < q1) put4(qb + i * AT_THREADS, v[i]);
+    }
   }
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -210,7 +272,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     if (lane == 0) s_red[warp][j] = v;
   }
   __syncthreads();
-  if (tid < G * AT_CL) {
+  if (tid < G * CL) {
     const int j = tid % G, r = tid / G;
     float v = -INFINITY;
     for (int w = 0; w < LK_W; ++w) v = fmaxf(v, s_red[w][j]);
@@ -221,7 +283,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   if (tid < G) {
     float v = -INFINITY;
 #pragma unroll
-    for (int r = 0; r < AT_CL; ++r) v = fmaxf(v, x_max[r][tid]);
+    for (int r = 0; r < CL; ++r) v = fmaxf(v, x_max[r][tid]);
     s_M[tid] = v;
   }
   __syncthreads();
@@ -245,7 +307,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     if (lane == 0 && z) atomicAdd(&s_zl[j], z);
   }
   __syncthreads();
-  if (tid < G * AT_CL) {
+  if (tid < G * CL) {
     const int j = tid % G, r = tid / G;
     *cl.map_shared_rank(&x_z[rank][j], r) = s_zl[j];
   }
@@ -253,7 +315,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   if (tid < G) {
     unsigned long long z = 0ull;
 #pragma unroll
-    for (int r = 0; r < AT_CL; ++r) z += x_z[r][tid];
+    for (int r = 0; r < CL; ++r) z += x_z[r][tid];
     s_Z[tid] = __fmul_rn(__ull2float_rn(z), __int_as_float((127 - 40) << 23));
   }
   __syncthreads();
@@ -269,7 +331,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
       RA[lo + i] = bits;  // (published to the cluster by the barrier below)
     } else {
 #pragma unroll
-      for (int r = 0; r < AT_CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+      for (int r = 0; r < CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
     }
   }
   if (tid == 0) {
@@ -703,7 +765,7 @@ __device__ unsigned long long g_lkv_prof[64][2048][PROF_SLOTS];
 #ifndef LKV_LAYER_MINB
 #define LKV_LAYER_MINB 1
 #endif
-template <int G>
+template <int G, int CL>
 __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer_kernel(LayerArgs A) {
   namespace cg = cooperative_groups;
 #ifdef LKV_PROF
@@ -721,7 +783,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   if (!early) pdl_wait_trigger();
   const RetrieveArgs& a = A.r;
   const AppendArgs& app = A.at.app;
-  const int li = blockIdx.x / AT_CL, rank = blockIdx.x % AT_CL;
+  const int li = blockIdx.x / CL, rank = blockIdx.x % CL;
   const int b = li / a.hn, h = li % a.hn, tid = threadIdx.x;
   extern __shared__ __align__(128) uint8_t lk_smem[];
   __shared__ __align__(16) InstState s_S;  // state before this step
@@ -732,10 +794,10 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   __shared__ double s_r;
   __shared__ int s_flag;
   __shared__ __align__(16) float sq[G][D];
-  constexpr int DS = D / AT_CL;  // output dims finalised by each rank
-  __shared__ float mg_acc[AT_CL][G][DS];
-  __shared__ float mg_ml[AT_CL][G][2];
-  __shared__ int s_own_dst[LK_REP_N / AT_CL];
+  constexpr int DS = D / CL;  // output dims finalised by each rank
+  __shared__ float mg_acc[CL][G][DS];
+  __shared__ float mg_ml[CL][G][2];
+  __shared__ int s_own_dst[LK_REP_N / CL];
   InstState* S = a.inst + li;
 
   // ---- 1. prologue: the instance state and (Hq <= 32) BOTH q_ref buffers (so no load waits for the
@@ -760,7 +822,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   if (tid == 0) {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/8): centroid
      // rows, sizes and the old selection / pool offsets — five bulk prefetches (TMA unit, no LSU
      // traffic). The trigger resolves in ~2 us; on an unflagged step the lines are simply not used.
-    const int nu = s_S.n_units, mu = (nu + AT_CL - 1) / AT_CL;
+    const int nu = s_S.n_units, mu = (nu + CL - 1) / CL;
     const int plo = min(nu, rank * mu), phi = min(nu, plo + mu);
     const int64_t ib = (int64_t)li * a.Umax;
     if (phi > plo) {
@@ -784,9 +846,9 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     // always the same four pieces at fixed indices (possibly empty: the piece lookup takes the
     // last piece starting at or before a row), so the plan stays in registers
     const int se = s_S.s_eff;
-    const int s0 = se * rank / AT_CL, s1 = se * (rank + 1) / AT_CL;
+    const int s0 = se * rank / CL, s1 = se * (rank + 1) / CL;
     const bf16* sk = at.sinks + (int64_t)li * 2 * at.S * D;
-    const int w0 = win_n * rank / AT_CL, w1 = win_n * (rank + 1) / AT_CL;
+    const int w0 = win_n * rank / CL, w1 = win_n * (rank + 1) / CL;
     const int hs = (win_head + w0) % cap;
     const int first = min(w1 - w0, cap - hs);
     pl.P.np = 4;
@@ -808,7 +870,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     pl.P.v[3] = ringV;
     pl.rows = (s1 - s0) + ws_rows_r + (w1 - w0);
     pl.mask_lo = pl.mask_hi = 0;
-    pl.new_vr = (rank == AT_CL - 1 && w1 > w0) ? pl.rows - 1 : -1;
+    pl.new_vr = (rank == CL - 1 && w1 > w0) ? pl.rows - 1 : -1;
     return w0;
   };
   // speculative (no retrieval) plan, issued now so the loads overlap the trigger: current working
@@ -816,7 +878,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   AttnPlan pl;
   const int dec0 = s_S.step;
   const int sup_head = s_S.buffered > 0 ? s_S.ring_head : dec0, sup_n = dec0 - sup_head + 1;
-  int ws_r0 = s_S.ws_rows * rank / AT_CL, ws_r1 = s_S.ws_rows * (rank + 1) / AT_CL;
+  int ws_r0 = s_S.ws_rows * rank / CL, ws_r1 = s_S.ws_rows * (rank + 1) / CL;
   const int sup_w0 = make_plan(pl, a.ws + s_S.ws_cur * a.ws_buf_stride + gi * a.ws_inst_stride + (int64_t)ws_r0 * D,
                                ws_r1 - ws_r0, sup_head, sup_n);
   int npre = min((pl.rows + am::CHUNK - 1) / am::CHUNK, am::STAGES - 1);
@@ -840,7 +902,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   prof_stamp(prof, 1);
   uint32_t qa[8][2];  // the owned heads' q as the attention MMA's A fragments (used at the end)
   mma_q_frags<G>(reinterpret_cast<const uint16_t*>(a.q_own) + (int64_t)b * a.stride_b + (int64_t)(a.h0 + h) * G * D, qa);
-  if (rank == AT_CL - 1 && tid < 32)
+  if (rank == CL - 1 && tid < 32)
     nv = reinterpret_cast<const uint4*>((tid < 16 ? A.at.app.k_t : A.at.app.v_t) + (int64_t)b * A.at.app.stride_b +
                                         (int64_t)h * D)[tid & 15];
   if (act) {
@@ -994,16 +1056,16 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     // (the host launches this kernel only when min(Umax, B) <= LK_REP_SEL; instances with more than
     // LK_REP_N live units select in big mode, with their per-unit arrays in global scratch)
     rep = true;
-    big = n > LK_REP_N;
-    own_dst = big ? reinterpret_cast<int*>(big_scratch(a, li) + 6 * (int64_t)a.Umax) + (int64_t)min(n, rank * ((n + AT_CL - 1) / AT_CL))
+    big = !rep_fits(n, G, CL);
+    own_dst = big ? reinterpret_cast<int*>(big_scratch(a, li) + 6 * (int64_t)a.Umax) + (int64_t)min(n, rank * ((n + CL - 1) / CL))
                   : s_own_dst;
     int nsel;
-    total = lk_select_rep<G>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, own_dst, big, prof);
+    total = lk_select_rep<G, CL>(a, li, rank, n, ws_cur, sq, lk_smem, &nsel, own_dst, big, prof);
     prof_stamp(prof, 4);
 #ifdef LKV_PROF
     if (prof && tid == 0) prof[23] = clock64();
 #endif
-    const int R0 = total * rank / AT_CL, R1 = total * (rank + 1) / AT_CL;
+    const int R0 = total * rank / CL, R1 = total * (rank + 1) / CL;
     lk_gather_list(reinterpret_cast<const SelEnt*>(lk_smem + rep_x_offset(n, big)), nsel, R0, R1,
                    reinterpret_cast<uint8_t*>(nxtK), reinterpret_cast<uint8_t*>(nxtK + (int64_t)a.budget * D));
     make_plan(pl, nxtK + (int64_t)R0 * D, R1 - R0, s_post.ring_head, s_post.buffered);
@@ -1011,7 +1073,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   } else {
     // the post-store_cache window is a suffix of the speculative one: mask the evicted front rows
     const int ex = s_post.ring_head - sup_head;  // rows evicted from the front of the superset
-    const int w1 = sup_n * (rank + 1) / AT_CL;
+    const int w1 = sup_n * (rank + 1) / CL;
     const int v_ring = pl.rows - (w1 - sup_w0);  // (the window rows come last in the plan)
     pl.mask_lo = v_ring;
     pl.mask_hi = v_ring + max(0, min(ex, w1) - sup_w0);
@@ -1032,7 +1094,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     const int j = idx / D, e = idx % D;
     *cl.map_shared_rank(&mg_acc[rank][j][e % DS], e / DS) = part[j * (D + 2) + e];
   }
-  if (tid < G * AT_CL) {
+  if (tid < G * CL) {
     const int j = tid % G, r = tid / G;
     float* dm = cl.map_shared_rank(&mg_ml[rank][j][0], r);
     dm[0] = part[j * (D + 2) + D];
@@ -1041,14 +1103,14 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   prof_stamp(prof, 10);
   cl.sync();
   prof_stamp(prof, 11);
-  if (tid < G * DS) {
-    const int j = tid / DS, e = tid % DS;
+  for (int idx = tid; idx < G * DS; idx += AT_THREADS) {
+    const int j = idx / DS, e = idx % DS;
     float M = -INFINITY;
 #pragma unroll
-    for (int y = 0; y < AT_CL; ++y) M = fmaxf(M, mg_ml[y][j][0]);
+    for (int y = 0; y < CL; ++y) M = fmaxf(M, mg_ml[y][j][0]);
     float Lsum = 0.f, Acc = 0.f;
 #pragma unroll
-    for (int y = 0; y < AT_CL; ++y) {
+    for (int y = 0; y < CL; ++y) {
       const float w = mg_ml[y][j][0] == -INFINITY ? 0.f : exp2f(mg_ml[y][j][0] - M);
       Lsum = fmaf(w, mg_ml[y][j][1], Lsum);
       Acc = fmaf(w, mg_acc[y][j][e], Acc);
@@ -1062,7 +1124,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
 
   // ---- 6. deferred state updates (every rank has read the old selection by now)
   if (flag && rep) {
-    const int m = (n + AT_CL - 1) / AT_CL;
+    const int m = (n + CL - 1) / CL;
     const int lo = min(n, rank * m), hi = min(n, lo + m);
     uint8_t* sel = a.sel + (int64_t)li * a.Umax;
     int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
@@ -1081,41 +1143,70 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     }
   }
   // store_cache side effects (seal / append / evict) by the last rank; commits the step
-  if (rank == AT_CL - 1) append_one(app, li, flag, &s_S);
+  if (rank == CL - 1) append_one(app, li, flag, &s_S);
   prof_stamp(prof, 14);
 }
 
-template <int G>
-static cudaError_t launch_layer_g(const LayerArgs& a, cudaStream_t st) {
+template <int G, int CL>
+static cudaError_t launch_layer_gc(const LayerArgs& a, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   cudaError_t ea = once_per_device(attr, [] {
-    return cudaFuncSetAttribute(layer_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    return cudaFuncSetAttribute(layer_kernel<G, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, LK_SMEM);
   });
   if (ea != cudaSuccess) return ea;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.r.batch * a.r.hn * AT_CL);
+  cfg.gridDim = dim3(a.r.batch * a.r.hn * CL);
   cfg.blockDim = dim3(AT_THREADS);
-  cfg.dynamicSmemBytes = AT_SMEM;
+  cfg.dynamicSmemBytes = LK_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = AT_CL;
+  attrs[0].val.clusterDim.x = CL;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, layer_kernel<G>, a);
+  return cudaLaunchKernelEx(&cfg, layer_kernel<G, CL>, a);
+}
+
+template <int G>
+static cudaError_t launch_layer_g(const LayerArgs& a, int cl, cudaStream_t st) {
+  switch (cl) {
+    case 2: return launch_layer_gc<G, 2>(a, st);
+    case 4: return launch_layer_gc<G, 4>(a, st);
+    default: return launch_layer_gc<G, 8>(a, st);
+  }
+}
+
+// CTAs per instance: the kernel holds one CTA per SM (its register budget); 8 when every instance's
+// cluster is resident in one wave, else 4 while two waves suffice, else 2 (measured at C4, 64
+// instances: CL 8 / 4 / 2 -> 2529 / 2866 / 2766 tok/s). LOUISKV_LAYER_CL overrides (2, 4 or 8).
+int layer_cluster_size(int n_inst) {
+  const char* es = getenv("LOUISKV_LAYER_CL");  // (read per launch: tests switch it in-process)
+  const int env = es ? atoi(es) : 0;
+  if (env == 2 || env == 4 || env == 8) return env;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  if (n_inst * 8 <= sms) return 8;
+  if (n_inst * 4 <= 2 * sms) return 4;  // (two waves of 4-CTA clusters beat one of 2-CTA clusters: the
+                                        // flagged instances' select and gather get twice the SMs)
+  return 2;
 }
 
 cudaError_t launch_layer(const LayerArgs& a, cudaStream_t st) {
   if (a.r.Hq > 64 || min(a.r.Umax, a.r.budget) > LK_REP_SEL) return cudaErrorInvalidValue;
+  const int cl = layer_cluster_size(a.r.batch * a.r.hn);
   switch (a.r.g) {
-    case 1: return launch_layer_g<1>(a, st);
-    case 2: return launch_layer_g<2>(a, st);
-    case 4: return launch_layer_g<4>(a, st);
-    case 8: return launch_layer_g<8>(a, st);
+    case 1: return launch_layer_g<1>(a, cl, st);
+    case 2: return launch_layer_g<2>(a, cl, st);
+    case 4: return launch_layer_g<4>(a, cl, st);
+    case 8: return launch_layer_g<8>(a, cl, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -590,3 +590,31 @@ def test_graph_replay_parity_with_early_prologue():
             for hh in range(hn):
                 assert np.array_equal(ctx.get_selection(l, bb, hh), np.array(ep.selection(l, bb, hh), np.int32))
     ctx.close()
+
+
+@pytest.mark.parametrize("cl", [2, 4])
+def test_layer_kernel_cluster_sizes(cl, monkeypatch):
+    """The single-launch layer kernel with 2 / 4 CTAs per instance (the batch configurations: the
+    cluster size shrinks so every instance's cluster is resident in one wave): the small episode, the
+    C4-parameter batch episode, the C3 long-output episode and many units (big-mode select),
+    all compared with the oracle every step."""
+    monkeypatch.setenv("LOUISKV_LAYER_CL", str(cl))
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, 0)
+    run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer")
+    cfg = C4.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, batch=3,
+                     prompt_len=4096, decode_steps=40)
+    inp = make_inputs(cfg, 40, 6)
+    run_episode(cfg, inp, 40, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused="layer")
+    cfg = C3.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, decode_steps=120,
+                     max_output_len=32768)
+    inp = make_inputs(cfg, 120, 5)
+    run_episode(cfg, inp, 120, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer")
+    cfg = C5.replace(num_layers=2, full_cache_layers=(0,), batch=1, prompt_len=2048, decode_steps=20)
+    inp = make_inputs(cfg, 20, 7)
+    run_episode(cfg, inp, 20, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused="layer")
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=6, batch=1, num_kv_heads=1, num_q_heads=4,
+                    prompt_len=9000 + 16, avg_cluster_size=1, budget_tokens=300, tau=0.95)
+    inp = make_inputs(cfg, 6, 10)
+    a = np.arange(9000, dtype=np.int32)[None, None, :]
+    run_episode(cfg, inp, 6, lambda l, Kn: a, fused="layer")

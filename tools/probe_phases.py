@@ -54,7 +54,8 @@ clr = lkv.lib().louiskv_prof_clear
 ORDER = [0, 1, 2, 24, 25, 26, 27, 3, 20, 6, 13, 16, 17, 15, 18, 19, 4, 5, 7, 8, 9, 10, 11, 12, 14]
 deltas = {"unflagged": [], "flagged": []}
 buf = np.zeros((64, 2048, 32), np.uint64)
-n_cta = b * Hkv * 8
+CL = int(os.environ.get("LOUISKV_LAYER_CL", "0")) or (8 if b * Hkv * 8 <= 148 else 4 if b * Hkv * 4 <= 148 else 2)
+n_cta = b * Hkv * CL
 rows = {"unflagged": [], "flagged": []}
 gaps = []
 for i in range(1, STEPS + 1):
@@ -80,10 +81,14 @@ for i in range(1, STEPS + 1):
         ok = (t[:, 23] > t[:, 22]) & (t[:, 4] > t[:, 3])
         rel[:, 22] = np.where(ok, (t[:, 23] - t[:, 22]) / np.maximum(t[:, 4] - t[:, 3], 1), np.nan)  # SM GHz
         rel[:, 23] = np.nan
-        key = "flagged" if fl[l].any() else "unflagged"
-        # per CTA: time from the previous present stamp (program order), median over CTAs
-        dl = {}
-        for c in range(n_cta):
+        # per CTA: time from the previous present stamp (program order), median over the CTAs of the
+        # flagged (resp. unflagged) instances of this launch
+        cta_flag = np.array([fl[l][(c // CL) // Hkv] for c in range(n_cta)], bool)
+        for key, sel in (("flagged", cta_flag), ("unflagged", ~cta_flag)):
+          if not sel.any():
+            continue
+          dl = {}
+          for c in np.nonzero(sel)[0]:
             prev = None
             for sl in ORDER:
                 if t[c, sl] == 0:
@@ -91,8 +96,8 @@ for i in range(1, STEPS + 1):
                 if prev is not None:
                     dl.setdefault(f"{prev}->{sl}", []).append(int(t[c, sl] - t[c, prev]))
                 prev = sl
-        deltas[key].append({k_: float(np.median(v_)) for k_, v_ in dl.items()})
-        rows[key].append(np.nanmedian(rel, axis=0).tolist() + [np.nanmax(rel[:, 14])])
+          deltas[key].append({k_: float(np.median(v_)) for k_, v_ in dl.items()})
+          rows[key].append(np.nanmedian(rel[sel], axis=0).tolist() + [np.nanmax(rel[sel][:, 14])])
         buf[l] = 0
         if prev_end is not None:
             gaps.append(t0 - prev_end)
