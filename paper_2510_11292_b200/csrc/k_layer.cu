@@ -448,6 +448,7 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
       const int excl = incl - ls;
       const int need = s_need;
       const unsigned hit = __ballot_sync(0xffffffffu, incl > need);
+      __syncwarp();  // (every lane has read s_need before lane `first` rewrites it)
       if (lane == 0) s_nc = 0;
       if (hit == 0u) {
         if (lane == 0) s_all = 1;  // (only possible on the first pass) the whole set fits the budget
@@ -519,8 +520,10 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
     nc = s_nc;
     if (nc <= DIRECT) {
       // direct finish: the pivot is the candidate whose running size sum (in key order) crosses need
+      // (need read by every thread before the barrier; the one matching thread publishes after it)
       const unsigned long long* L = LB + cb * LCAP;
       const int need = s_need;
+      __syncthreads();
       for (int ci = tid; ci < nc; ci += AT_THREADS) {
         const unsigned long long e = L[ci], k = e & M48;
         int below = 0;

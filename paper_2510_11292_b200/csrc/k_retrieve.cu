@@ -262,6 +262,7 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
         const int excl = incl - ls;
         const int need = s_need;
         const unsigned hit = __ballot_sync(0xffffffffu, incl > need);
+        __syncwarp();  // (every lane has read s_need before lane `first` rewrites it)
         if (hit == 0u) {
           if (lane == 0) s_all = 1;  // (pass 0 sees everything) the whole set fits the budget
         } else {
