@@ -62,6 +62,7 @@ struct louiskv_ctx {
   int32_t* d_km_perm = nullptr;
   int32_t* d_km_flags = nullptr;
   int32_t* d_km_toff = nullptr;
+  int4* d_km_tcl = nullptr;
   int32_t* d_km_ccT = nullptr;
   uint16_t* d_km_bext = nullptr;
   float* d_km_upart = nullptr;
@@ -389,6 +390,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_km_flags, (size_t)nl);
   c->km_task_max = std::max(c->kmax, 1) + (int)((c->Nmax + 31) / 32);
   ok = ok && dalloc(c, &c->d_km_toff, (size_t)nl * (c->kmax + 1));
+  ok = ok && dalloc(c, &c->d_km_tcl, (size_t)nl * c->km_task_max);
   ok = ok && dalloc(c, &c->d_km_bext, (size_t)nl * c->Umax * 8);
   ok = ok && dalloc(c, &c->d_km_ccT, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
   ok = ok && dalloc(c, &c->d_km_upart, (size_t)nl * c->km_task_max * D);
@@ -568,6 +570,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.perm = c->d_km_perm;
   a.flags = c->d_km_flags;
   a.toff = c->d_km_toff;
+  a.tcl = c->d_km_tcl;
   a.ccT = c->d_km_ccT;
   a.bext = c->d_km_bext;
   a.upart = c->d_km_upart;

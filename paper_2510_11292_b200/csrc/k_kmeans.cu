@@ -186,6 +186,7 @@ __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
   int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
   int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
   int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  int4* tcl = a.tcl + (int64_t)li * a.task_max;
   if (threadIdx.x == 0) s_empty = 0;
   __syncthreads();
   for (int j = threadIdx.x; j < a.kc; j += blockDim.x) {
@@ -219,9 +220,14 @@ __device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
   int trun = km_block_excl_scan(tloc, ttotal);
   for (int j = j0; j < j1; ++j) {
     off[j] = run;
-    run += cnt[j];
     toff[j] = trun;
-    trun += (cnt[j] + KM_TASK - 1) / KM_TASK;
+    {  // the update tasks of cluster j: (cluster, first member, end member, tasks of the cluster)
+      const int nt = (cnt[j] + KM_TASK - 1) / KM_TASK;
+      for (int q = 0; q < nt; ++q)
+        tcl[trun + q] = make_int4(j, run + q * KM_TASK, min(run + cnt[j], run + (q + 1) * KM_TASK), nt);
+      trun += nt;
+    }
+    run += cnt[j];
   }
   if (threadIdx.x == 0) {
     off[a.kc] = a.N;
@@ -269,6 +275,7 @@ __global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dir
   const int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
   int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
   int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  int4* tcl = a.tcl + (int64_t)li * a.task_max;
   const int per = (a.kc + blockDim.x - 1) / blockDim.x;
   const int j0 = threadIdx.x * per, j1 = min(a.kc, j0 + per);
   int local = 0, tloc = 0, empty = 0;
@@ -284,9 +291,14 @@ __global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dir
   const int any_empty = __syncthreads_or(empty);
   for (int j = j0; j < j1; ++j) {
     off[j] = run;
-    run += cnt[j];
     toff[j] = trun;
-    trun += (cnt[j] + KM_TASK - 1) / KM_TASK;
+    {  // the update tasks of cluster j: (cluster, first member, end member, tasks of the cluster)
+      const int nt = (cnt[j] + KM_TASK - 1) / KM_TASK;
+      for (int q = 0; q < nt; ++q)
+        tcl[trun + q] = make_int4(j, run + q * KM_TASK, min(run + cnt[j], run + (q + 1) * KM_TASK), nt);
+      trun += nt;
+    }
+    run += cnt[j];
   }
   if (threadIdx.x == 0) {
     off[a.kc] = a.N;
@@ -303,6 +315,15 @@ __global__ void __launch_bounds__(1024) km_offsets_kernel(KmArgs a, int only_dir
 // bitonic-sort them in shared memory, walk them once with cluster counts in shared memory.
 // If the walk runs out of candidates (many ineligible), the slow per-empty scan finishes the job.
 constexpr int RP_CAND = 2048;
+constexpr int RP_SMEM_MAX = 200 * 1024;
+__host__ __device__ inline size_t repair_smem_base(int kc) {
+  return sizeof(int) * (2 * (size_t)kc) + RP_CAND * (sizeof(unsigned long long) + sizeof(int));
+}
+// the eligible-donor keys of all N points are kept in shared memory when they fit (one pass over
+// global memory instead of five: the four threshold passes and the compaction read them on chip)
+__host__ __device__ inline bool repair_keys_in_smem(int kc, int N) {
+  return repair_smem_base(kc) + sizeof(unsigned) * (size_t)N <= RP_SMEM_MAX;
+}
 __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
   pdl_wait_trigger();
   const int li = blockIdx.x;
@@ -312,6 +333,8 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
   int* s_empty = s_cnt + a.kc;                                            // [kc]
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_empty + a.kc + (a.kc & 1 ? 0 : 0));  // [RP_CAND] (2*kc ints: 8-B aligned)
   int* s_cl = reinterpret_cast<int*>(s_key + RP_CAND);                    // [RP_CAND]
+  unsigned* s_dk = reinterpret_cast<unsigned*>(s_cl + RP_CAND);           // [N] donor keys (if they fit)
+  const bool keys_smem = repair_keys_in_smem(a.kc, a.N);
   __shared__ int s_hist[256];
   __shared__ int s_n, s_E, s_filled, s_need;
   __shared__ unsigned s_prefix;
@@ -333,12 +356,27 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
   int pos = km_block_excl_scan(ne, E);
   for (int j = j0; j < j1; ++j)
     if (s_cnt[j] == 0) s_empty[pos++] = j;
-  // dmin key of an eligible point: bits of max(dmin, 0) (monotone for non-negative floats)
-  auto dkey = [&](int i) -> unsigned {
-    const float d = dm[i];
-    if (d == -INFINITY) return 0u;  // already a donor
-    return __float_as_uint(fmaxf(d, 0.f)) + 1u;  // 0 is reserved for "not eligible"
-  };
+  // dmin key of an eligible point: bits of max(dmin, 0) + 1 (monotone for non-negative floats; 0 is
+  // reserved for "not eligible"; dmin = -inf marks a point already taken as a donor)
+  if (keys_smem) {  // (s_cnt is complete: the block scan above ended with a barrier)
+    for (int i0 = tid; i0 < a.N; i0 += 8 * blockDim.x) {
+      int ai[8];
+      float di[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r * blockDim.x;
+        ai[r] = i < a.N ? as[i] : 0;
+        di[r] = i < a.N ? dm[i] : -INFINITY;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r * blockDim.x;
+        if (i < a.N)
+          s_dk[i] = (di[r] != -INFINITY && s_cnt[ai[r]] >= 2) ? __float_as_uint(fmaxf(di[r], 0.f)) + 1u : 0u;
+      }
+    }
+    __syncthreads();
+  }
   // ---- threshold: the T-th largest eligible key, T = min(1.5E + 32, RP_CAND / 2)
   const int T = min(E + E / 2 + 32, RP_CAND / 2);
   if (tid == 0) {
@@ -352,9 +390,27 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
     for (int i = tid; i < 256; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const unsigned prefix = s_prefix;
-    for (int i = tid; i < a.N; i += blockDim.x) {
-      const unsigned k = s_cnt[as[i]] >= 2 ? dkey(i) : 0u;
-      if (k != 0u && (k & hi_mask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+    if (keys_smem) {
+      for (int i = tid; i < a.N; i += blockDim.x) {
+        const unsigned k = s_dk[i];
+        if (k != 0u && (k & hi_mask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+      }
+    } else
+    // 8 keys per thread in flight per batch (assignment and dmin loads issued before any use)
+    for (int i0 = tid; i0 < a.N; i0 += 8 * blockDim.x) {
+      int ai[8];
+      float di[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r * blockDim.x;
+        ai[r] = i < a.N ? as[i] : 0;
+        di[r] = i < a.N ? dm[i] : -INFINITY;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const unsigned k = (di[r] != -INFINITY && s_cnt[ai[r]] >= 2) ? __float_as_uint(fmaxf(di[r], 0.f)) + 1u : 0u;
+        if (k != 0u && (k & hi_mask) == prefix) atomicAdd(&s_hist[(k >> shift) & 255], 1);
+      }
     }
     __syncthreads();
     if (tid == 0) {
@@ -373,11 +429,31 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
   // ---- compact candidates (key >= thr) and sort them by (key desc, index asc)
   if (tid == 0) s_n = 0;
   __syncthreads();
-  for (int i = tid; i < a.N; i += blockDim.x) {
-    const unsigned k = s_cnt[as[i]] >= 2 ? dkey(i) : 0u;
-    if (k != 0u && k >= thr) {
-      const int slot = atomicAdd(&s_n, 1);
-      if (slot < RP_CAND) s_key[slot] = ((unsigned long long)(~k) << 32) | (unsigned)i;
+  if (keys_smem) {
+    for (int i = tid; i < a.N; i += blockDim.x) {
+      const unsigned k = s_dk[i];
+      if (k != 0u && k >= thr) {
+        const int slot = atomicAdd(&s_n, 1);
+        if (slot < RP_CAND) s_key[slot] = ((unsigned long long)(~k) << 32) | (unsigned)i;
+      }
+    }
+  } else
+  for (int i0 = tid; i0 < a.N; i0 += 8 * blockDim.x) {
+    int ai[8];
+    float di[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = i0 + r * blockDim.x;
+      ai[r] = i < a.N ? as[i] : 0;
+      di[r] = i < a.N ? dm[i] : -INFINITY;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const unsigned k = (di[r] != -INFINITY && s_cnt[ai[r]] >= 2) ? __float_as_uint(fmaxf(di[r], 0.f)) + 1u : 0u;
+      if (k != 0u && k >= thr) {
+        const int slot = atomicAdd(&s_n, 1);
+        if (slot < RP_CAND) s_key[slot] = ((unsigned long long)(~k) << 32) | (unsigned)(i0 + r * blockDim.x);
+      }
     }
   }
   __syncthreads();
@@ -482,7 +558,18 @@ __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   const int li = blockIdx.y, c = blockIdx.x, lane = threadIdx.x;
   const int32_t* ccT = a.ccT + ((int64_t)li * a.nchunk_max + c) * a.kmax;
   const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
-  for (int j = lane; j < a.kc; j += 32) base[j] = ccT[j] + off[j];
+  for (int j0 = lane; j0 < a.kc; j0 += 8 * 32) {  // 16 loads per lane in flight per batch
+    int cv[8], ov[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int j = j0 + r * 32;
+      cv[r] = j < a.kc ? ccT[j] : 0;
+      ov[r] = j < a.kc ? off[j] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (j0 + r * 32 < a.kc) base[j0 + r * 32] = cv[r] + ov[r];
+  }
   __syncwarp();
   const int32_t* as = a.assign + (int64_t)li * a.Nmax;
   int32_t* perm = a.perm + (int64_t)li * a.Nmax;
@@ -541,36 +628,35 @@ __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
   const int t = blockIdx.x * 4 + warp;
   const int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
   if (t >= toff[a.kc]) return;
-  // cluster of task t: the last j with toff[j] <= t
-  int lo = 0, hi = a.kc - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (toff[mid] <= t) lo = mid;
-    else hi = mid - 1;
-  }
-  const int j = lo;
-  const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
+  // the task (written with the offsets): cluster j, members [m0, m1) of the cluster-sorted order,
+  // tasks of j; lane i holds member m0 + i's position, so all <= 32 member rows are loaded in two
+  // batches of 16 (three round trips in all), summed in member order (deterministic)
+  const int4 tk = a.tcl[(int64_t)li * a.task_max + t];
+  const int j = tk.x, m0 = tk.y, m1 = tk.z, ntask = tk.w;
   const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
-  const int q = t - toff[j];
-  const int m0 = off[j] + q * KM_TASK, m1 = min(off[j + 1], m0 + KM_TASK);
+  const int nm = m1 - m0;
+  const int pi = lane < nm ? perm[m0 + lane] : 0;
   float s[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int m = m0; m < m1; m += 8) {
-    uint2 u[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (m + r < m1) u[r] = reinterpret_cast<const uint2*>(xrow(a, li, perm[m + r]))[lane];
+  for (int rb = 0; rb < KM_TASK; rb += 16) {
+    if (rb >= nm) break;
+    uint2 u[16];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (m + r < m1) {
+    for (int r = 0; r < 16; ++r) {
+      const int idx = __shfl_sync(0xffffffffu, pi, rb + r);
+      if (rb + r < nm) u[r] = reinterpret_cast<const uint2*>(xrow(a, li, idx))[lane];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (rb + r < nm) {
         s[0] = __fadd_rn(s[0], __uint_as_float(u[r].x << 16));
         s[1] = __fadd_rn(s[1], __uint_as_float(u[r].x & 0xFFFF0000u));
         s[2] = __fadd_rn(s[2], __uint_as_float(u[r].y << 16));
         s[3] = __fadd_rn(s[3], __uint_as_float(u[r].y & 0xFFFF0000u));
       }
   }
-  const int ntask = toff[j + 1] - toff[j];
   if (ntask == 1) {
-    km_write_centroid(a, li, j, s, off[j + 1] - off[j], lane);
+    km_write_centroid(a, li, j, s, nm, lane);
   } else {
     float4* P = reinterpret_cast<float4*>(a.upart + ((int64_t)li * a.task_max + t) * D);
     P[lane] = make_float4(s[0], s[1], s[2], s[3]);
@@ -709,7 +795,7 @@ static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool rep
   launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 0);
   launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 0);
   if (repair) {
-    const size_t rsm = sizeof(int) * (2 * a.kc) + RP_CAND * (sizeof(unsigned long long) + sizeof(int));
+    const size_t rsm = repair_smem_base(a.kc) + (repair_keys_in_smem(a.kc, a.N) ? sizeof(unsigned) * (size_t)a.N : 0);
     launch_k(km_repair_kernel, dim3(ni), dim3(1024), rsm, st, a, nchunk);
     launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 1);
     launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);

@@ -249,6 +249,7 @@ struct KmArgs {
   int32_t* cc;       // [ni][kmax][nchunk_max] (transposed chunk histograms)
   int32_t* ccT;      // [ni][nchunk_max][kmax] chunk-major exclusive prefixes (scatter bases)
   int32_t* toff;     // [ni][kmax+1] update-task offsets
+  int4* tcl;         // [ni][task_max] update tasks: (cluster, first member, end member, tasks of the cluster)
   float* upart;      // [ni][task_max][D] partial sums of multi-task clusters
   int task_max;      // kmax + ceil(Nmax / 32)
   int32_t* off;      // [ni][kmax+1]
