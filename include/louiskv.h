@@ -232,6 +232,12 @@ louiskv_status louiskv_get_stats(louiskv_ctx* ctx, louiskv_stats* out);
  * tables, full-cache layers, scratch) and the pinned host-pool bytes. Either pointer may be NULL.
  * No synchronisation. Errors: INVALID_ARG (null ctx). */
 louiskv_status louiskv_get_memory(const louiskv_ctx* ctx, uint64_t* device_bytes, uint64_t* host_pool_bytes);
+/* NUMA placement of the pinned host pool: on hosts with more than one NUMA node the pool is
+ * allocated on the GPU's own node (sysfs numa_node of its PCI device; anonymous mmap bound with mbind,
+ * then pinned and mapped with cudaHostRegister), so each GPU's host-link traffic stays on its socket;
+ * otherwise cudaHostAlloc. Env LOUISKV_POOL_NUMA=0 disables, =1 forces the bound allocation on a
+ * single-node host. *node = the bound node, or -1 (cudaHostAlloc). Errors: INVALID_ARG. */
+louiskv_status louiskv_get_pool_numa_node(const louiskv_ctx* ctx, int32_t* node);
 
 /* ---- prefill phase timer (the per-phase breakdown of cluster_prompt; SURVEY §5 tracing) ----
  * When enabled, every later cluster_prompt records stream-ordered CUDA events between its phases:

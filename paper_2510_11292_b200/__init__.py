@@ -33,7 +33,8 @@ SYMBOLS = ["louiskv_create", "louiskv_destroy", "louiskv_cluster_prompt", "louis
            "louiskv_append_attn", "louiskv_decode_layer",
            "louiskv_get_selection", "louiskv_get_units", "louiskv_get_unit_positions", "louiskv_get_working_set",
            "louiskv_get_stats", "louiskv_get_memory", "louiskv_set_prefill_timing", "louiskv_get_prefill_times",
-           "louiskv_state_save", "louiskv_state_restore", "louiskv_last_error", "louiskv_version"]
+           "louiskv_state_save", "louiskv_state_restore", "louiskv_get_pool_numa_node", "louiskv_last_error",
+           "louiskv_version"]
 
 
 class LouisKVError(RuntimeError):
@@ -107,6 +108,7 @@ def lib():
         L.louiskv_get_prefill_times.argtypes = [vp, ctypes.POINTER(PrefillTimes)]
         L.louiskv_state_save.argtypes = [vp, vp]
         L.louiskv_state_restore.argtypes = [vp, vp]
+        L.louiskv_get_pool_numa_node.argtypes = [vp, ctypes.POINTER(ctypes.c_int32)]
         L.louiskv_last_error.argtypes = [vp]
         L.louiskv_last_error.restype = ctypes.c_char_p
         L.louiskv_version.restype = ctypes.c_char_p
@@ -283,6 +285,12 @@ class Context:
         t = PrefillTimes()
         self._chk(self._L.louiskv_get_prefill_times(self.h, ctypes.byref(t)))
         return t.as_dict()
+
+    def pool_numa_node(self) -> int:
+        """NUMA node the pinned pool is bound to (-1: cudaHostAlloc, no binding)."""
+        n = ctypes.c_int32()
+        self._chk(self._L.louiskv_get_pool_numa_node(self.h, ctypes.byref(n)))
+        return n.value
 
     def state_save(self, stream=None):
         """Checkpoint the decode state (device resident, stream ordered)."""

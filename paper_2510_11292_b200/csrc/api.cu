@@ -1,5 +1,9 @@
 // C ABI of the LouisKV B200 library: context, capacities, state machine, kernel sequencing.
 // See include/louiskv.h for the contract of every entry point (paper citations there).
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -43,6 +47,8 @@ struct louiskv_ctx {
   bf16* d_qref = nullptr;
   bf16* d_full = nullptr;
   uint8_t* h_pool = nullptr;
+  bool pool_registered = false;  // mmap + mbind + cudaHostRegister (NUMA-local) instead of cudaHostAlloc
+  int pool_numa_node = -1;
   uint8_t* d_pool = nullptr;
   int64_t pool_inst_bytes = 0;
   // scratch
@@ -101,6 +107,48 @@ struct louiskv_ctx {
 };
 
 namespace {
+
+// NUMA node of the GPU's PCI device (sysfs), -1 if unknown; number of NUMA nodes of the host
+int device_numa_node(int dev) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, (int)sizeof(bus), dev) != cudaSuccess) return -1;
+  for (char* p = bus; *p; ++p) *p = (char)tolower(*p);
+  std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+int numa_node_count() {
+  int n = 0;
+  for (int i = 0; i < 64; ++i) {
+    std::string p = "/sys/devices/system/node/node" + std::to_string(i);
+    if (access(p.c_str(), F_OK) == 0) ++n;
+  }
+  return n;
+}
+// The pinned pool on the GPU's NUMA node (multi-socket hosts: every GPU's host-link traffic stays on
+// its own socket): anonymous mmap, MPOL_BIND to the node (raw mbind syscall, no libnuma), then pinned
+// and mapped with cudaHostRegister. Returns nullptr (caller falls back to cudaHostAlloc) on any failure.
+void* alloc_pool_numa(size_t bytes, int node) {
+  if (node < 0 || node >= 64) return nullptr;
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return nullptr;
+  unsigned long mask = 1ul << node;
+  const long MPOL_BIND_ = 2;
+  if (syscall(SYS_mbind, p, bytes, MPOL_BIND_, &mask, (unsigned long)(sizeof(mask) * 8), 0) != 0) {
+    munmap(p, bytes);
+    return nullptr;
+  }
+  if (cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(p, bytes);
+    return nullptr;
+  }
+  return p;
+}
 
 louiskv_status fail(louiskv_ctx* c, louiskv_status s, const std::string& m) {
   if (c) {
@@ -288,7 +336,14 @@ void louiskv_destroy(louiskv_ctx* ctx) {
   for (auto& sb : ctx->snap)
     if (sb.dst) cudaFree(sb.dst);
   for (void* p : ctx->allocs) cudaFree(p);
-  if (ctx->h_pool) cudaFreeHost(ctx->h_pool);
+  if (ctx->h_pool) {
+    if (ctx->pool_registered) {
+      cudaHostUnregister(ctx->h_pool);
+      munmap(ctx->h_pool, (size_t)ctx->host_bytes);
+    } else {
+      cudaFreeHost(ctx->h_pool);
+    }
+  }
   delete ctx;
 }
 
@@ -378,7 +433,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_ssort, (size_t)nl * c->Umax * 26);
   ok = ok && dalloc(c, &c->d_rows, (size_t)nl * std::max(c->Bud, 1));
   ok = ok && dalloc(c, &c->d_jobs, (size_t)c->L * nl);
-  ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 2));
+  ok = ok && dalloc(c, &c->d_part, (size_t)nl * c->max_splits * g * (D + 4));  // (>= every kernel's partial stride)
   ok = ok && dalloc(c, &c->d_counters, (size_t)nl + 1);  // + the fused full-cache step's layer ticket
   ok = ok && dalloc(c, &c->d_km_half, (size_t)nl * (((std::max(c->kmax, 1) + 255) / 256) * 256));
   ok = ok && dalloc(c, &c->d_km_assign, (size_t)nl * std::max<int64_t>(c->Nmax, 1));
@@ -422,7 +477,19 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   const size_t pool_bytes = (size_t)std::max<int64_t>(ni, 1) * c->pool_inst_bytes;
   if (pool_bytes > 0) {
     void* hp = nullptr;
-    if (cudaHostAlloc(&hp, pool_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    // NUMA-local pool on multi-node hosts (LOUISKV_POOL_NUMA=0 disables, =1 forces it on one node)
+    const char* ne = getenv("LOUISKV_POOL_NUMA");
+    const int numa_mode = ne ? atoi(ne) : -1;
+    int node = device_numa_node(k.device);
+    if (numa_mode == 1 && node < 0) node = 0;  // (forced on a host whose sysfs reports no node)
+    if (numa_mode != 0 && node >= 0 && (numa_mode == 1 || numa_node_count() > 1)) {
+      hp = alloc_pool_numa(pool_bytes, node);
+      if (hp) {
+        c->pool_registered = true;
+        c->pool_numa_node = node;
+      }
+    }
+    if (!hp && cudaHostAlloc(&hp, pool_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
       cudaGetLastError();
       louiskv_destroy(c);
       return LOUISKV_ERR_OOM_HOST;
@@ -1003,6 +1070,12 @@ louiskv_status louiskv_state_restore(louiskv_ctx* c, void* stream) {
   c->t = c->snap_t;
   c->stage = c->snap_stage;
   c->last_layer = -1;
+  return LOUISKV_OK;
+}
+
+louiskv_status louiskv_get_pool_numa_node(const louiskv_ctx* c, int32_t* node) {
+  if (!c || !node) return LOUISKV_ERR_INVALID_ARG;
+  *node = c->pool_registered ? c->pool_numa_node : -1;
   return LOUISKV_OK;
 }
 

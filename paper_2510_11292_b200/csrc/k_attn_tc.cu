@@ -22,6 +22,10 @@
 
 namespace lkv {
 namespace fa {
+// per-head stride of a split partial in global memory: D accumulators, max, sum, 2 pad floats (rows
+// stay 16-B aligned for the cp.async merge whatever g is; g = 1 with D + 2 was not)
+constexpr int PSTR = D + 4;
+
 
 constexpr int THREADS = 128;
 constexpr int WARPS = THREADS / 32;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
     }
   }
   __syncthreads();
-  float* part = a.part + ((int64_t)li * nsplit + split) * G * (D + 2);
+  float* part = a.part + ((int64_t)li * nsplit + split) * G * PSTR;
   for (int idx = tid; idx < G * D; idx += THREADS) {
     const int j = idx / D, e = idx % D;
     float M = -INFINITY;
@@ -336,10 +340,10 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
         Lsum += s_ml[(w * G + j) * 2 + 1] * sc;
         A += s_acc[(w * G + j) * D + e] * sc;
       }
-    part[j * (D + 2) + e] = A;
+    part[j * PSTR + e] = A;
     if (e == 0) {
-      part[j * (D + 2) + D] = M;
-      part[j * (D + 2) + D + 1] = Lsum;
+      part[j * PSTR + D] = M;
+      part[j * PSTR + D + 1] = Lsum;
     }
   }
   // ---- the last CTA of this instance merges the splits in split order
@@ -350,10 +354,10 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const float* P0 = a.part + (int64_t)li * nsplit * G * (D + 2);
+  const float* P0 = a.part + (int64_t)li * nsplit * G * PSTR;
   // the splits' partials are staged in shared memory (the idle stage ring) by cp.async in batches
   // of SB splits — one round trip per batch instead of one dependent L2 load per split and output
-  constexpr int PF = G * (D + 2);                      // floats per split partial (16-B multiple)
+  constexpr int PF = G * PSTR;                      // floats per split partial (16-B multiple: PSTR = D + 4)
   constexpr int MAXS = 64;                             // (>= the host's max_splits)
   constexpr int WB = 2 * MAXS * G * 4 + 2 * G * 4;     // bytes of the per-split weights + (M, 1/L)
   constexpr int SB = (STAGES * STAGE_BYTES - WB) / (PF * 4);  // splits per staging batch
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
   // (m, l) of every split-head, all loads in one round (they overlap the first batch's staging)
   for (int t = tid; t < nsplit * G; t += THREADS) {
     const int y = t / G, j = t % G;
-    s_wt[t] = __ldcg(P0 + y * PF + j * (D + 2) + D);
-    s_l[t] = __ldcg(P0 + y * PF + j * (D + 2) + D + 1);
+    s_wt[t] = __ldcg(P0 + y * PF + j * PSTR + D);
+    s_l[t] = __ldcg(P0 + y * PF + j * PSTR + D + 1);
   }
   __syncthreads();
   if (tid < G) {  // global max and normaliser per head, split order
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, FA_MINB) attn_full_tc_kernel(const __
       if (idx < G * D) {
         const int j = idx / D, e = idx % D;
 #pragma unroll 4
-        for (int y = 0; y < nb; ++y) accv[i] = fmaf(s_wt[(y0 + y) * G + j], s_part[y * PF + j * (D + 2) + e], accv[i]);
+        for (int y = 0; y < nb; ++y) accv[i] = fmaf(s_wt[(y0 + y) * G + j], s_part[y * PF + j * PSTR + e], accv[i]);
       }
     }
   }

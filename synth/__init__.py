@@ -161,7 +161,16 @@ def decode_stream(cfg: Config, steps: int, seed: int, device="cpu", plants=None,
                 u = (w.unsqueeze(-1) * dirs).sum(1)
                 u = u / u.norm(dim=-1, keepdim=True) * cfg.q_scale
                 noise = _randn((n_eff, Hq, d), g, device, cfg.q_noise * cfg.q_scale)
-                q[t0:t0 + n_eff, layer, bb] = (u.unsqueeze(0) + noise).to(torch.bfloat16)
+                if cfg.drift > 0:
+                    # graded drift: the direction random-walks inside the segment with a per-segment
+                    # step size, so consecutive-query cosines spread over a range instead of one value
+                    step = float(torch.rand((), generator=gc)) * cfg.drift * cfg.q_scale / math.sqrt(d)
+                    walk = torch.cumsum(_randn((n_eff, Hq, d), g, device, step), dim=0)
+                    uu = u.unsqueeze(0) + walk
+                    uu = uu / uu.norm(dim=-1, keepdim=True) * cfg.q_scale
+                    q[t0:t0 + n_eff, layer, bb] = (uu + noise).to(torch.bfloat16)
+                else:
+                    q[t0:t0 + n_eff, layer, bb] = (u.unsqueeze(0) + noise).to(torch.bfloat16)
                 wdir = _randn((Hkv, d), g, device, 2.0)
                 kk = plant.mu0[bb].unsqueeze(0) + wdir.unsqueeze(0) + _randn((n_eff, Hkv, d), g, device, cfg.key_noise)
                 k[t0:t0 + n_eff, layer, bb] = kk.to(torch.bfloat16)

@@ -39,6 +39,9 @@ class Config:
     q_scale: float = 6.0
     q_noise: float = 0.0203     # per-coordinate sigma relative to |u| (within-segment cos ~0.95)
     max_output_len: int = 0     # 0 -> decode_steps
+    drift: float = 0.0          # > 0: graded within-segment query drift (random walk of the direction,
+                                # per-segment step size uniform in [0, drift] x |u|): spreads r_t so a
+                                # tau sweep traces a retrieval-frequency curve (ablation inputs only)
     clusters_override: int = 0  # C1: k fixed at 64
 
     def __post_init__(self):

@@ -692,3 +692,13 @@ def test_attention_negative_controls():
           f"{n_kt_detect}/{n_kt}")
     assert n_kt == 0 or n_kt_detect == n_kt
     ctx.close()
+
+
+def test_episode_g1_with_full_cache_layer():
+    """g = 1 (one query head per KV head, the per-head case of P:247) next to a full-cache layer: the
+    tensor-core full-cache attention's split partials at g = 1 (stride kept 16-B aligned), both the
+    four-call path and the single launch."""
+    cfg = small_cfg(num_q_heads=2, num_kv_heads=2, decode_steps=16)
+    inp = make_inputs(cfg, 16, 15)
+    for fused in (False, "layer"):
+        run_episode(cfg, inp, 16, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)

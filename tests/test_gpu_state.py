@@ -89,3 +89,34 @@ def test_prefill_timer_counts_and_phases():
             assert np.array_equal(s1, s2) and np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
     ctx.close()
     ctx2.close()
+
+
+def test_numa_bound_pool_path(monkeypatch):
+    """The NUMA-local pool path (mmap + mbind + cudaHostRegister), forced on this single-node host:
+    an episode on it matches one on the cudaHostAlloc pool bit for bit."""
+    lkv = _lkv()
+    cfg = Config("nu", num_layers=2, num_q_heads=8, num_kv_heads=2, head_dim=128, batch=1, prompt_len=900,
+                 decode_steps=10, sink_tokens=16, window_tokens=24, budget_tokens=96, tau=0.85,
+                 avg_cluster_size=16, kmeans_iters=3, full_cache_layers=(0,), seg_mean=4.0)
+    inp = make_inputs(cfg, 10, 41)
+    res = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("LOUISKV_POOL_NUMA", mode)
+        ctx = lkv.Context(lkv.make_config(cfg))
+        if mode == "1":
+            assert ctx.pool_numa_node() >= 0
+        else:
+            assert ctx.pool_numa_node() == -1
+        for l in range(2):
+            ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+        out32 = torch.zeros((2, 1, 8, 128), dtype=torch.float32, device="cuda")
+        out = torch.zeros((2, 1, 8, 128), dtype=torch.bfloat16, device="cuda")
+        for t in range(10):
+            for l in range(2):
+                ctx.decode_layer(l, inp.q[t, l], inp.k[t, l].contiguous(), inp.v[t, l].contiguous(), out[l], out32[l])
+        torch.cuda.synchronize()
+        res.append((out32.cpu().numpy().copy(), ctx.stats(), ctx.get_working_set(1, 0, 1)))
+        ctx.close()
+    assert np.array_equal(res[0][0].view(np.uint32), res[1][0].view(np.uint32))
+    assert res[0][1] == res[1][1] and res[0][1]["bytes_h2d"] > 0
+    assert np.array_equal(res[0][2][0], res[1][2][0])
