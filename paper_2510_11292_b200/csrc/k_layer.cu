@@ -140,8 +140,9 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   // Logits staging (below): up to 6 buffers of RB centroid rows after E (the own logits) in X; E
   // moves to global scratch when that leaves room for more buffers
   constexpr int PITCH = ROW_BYTES + 16;
-  constexpr int HPT = G < 2 ? G : 2;       // heads per thread: two independent fmaf chains (ILP 2)
-  constexpr int RB = AT_THREADS * HPT / G;  // rows per round: every thread busy
+  constexpr int HPT = G;           // heads per thread: g independent fmaf chains (ILP g)
+  constexpr int RB = AT_THREADS;   // rows per round: one per thread (measured: fewer, longer rounds
+                                   // beat more rows in flight — each round is one chain latency)
   const int e_bytes_s = (G * m * 4 + 127) & ~127;
   const int nb_s = big ? 0 : min(6, (x_bytes - e_bytes_s) / (RB * PITCH));
   const int nb_g = min(6, x_bytes / (RB * PITCH));
@@ -230,11 +231,16 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
 #pragma unroll
         for (int k = 0; k < HPT; ++k) E[(hd * HPT + k) * m + b0 + row] = l[k];
         // (the heads' running maxima; compile-time indices only — no dynamically indexed registers)
+        if constexpr (HPT == G) {
 #pragma unroll
-        for (int j = 0; j < G; ++j)
+          for (int j = 0; j < G; ++j) mymax[j] = fmaxf(mymax[j], l[j]);
+        } else {
 #pragma unroll
-          for (int k = 0; k < HPT; ++k)
-            if (j == hd * HPT + k) mymax[j] = fmaxf(mymax[j], l[k]);
+          for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int k = 0; k < HPT; ++k)
+              if (j == hd * HPT + k) mymax[j] = fmaxf(mymax[j], l[k]);
+        }
       }
       __syncthreads();
     }
