@@ -226,6 +226,29 @@ def workload_label(cfg, T_steps=None) -> str:
             f"k-means {cfg.kmeans_iters} iters; planted key groups k/4 = {cfg.k_planted}")
 
 
+def table3_accounting(cfg, hc, m_out):
+    """GPU KV footprint, Table 3: FullCache 4 L h d (n + m), LouisKV 4 L h d (B + n/(2c) +
+    m/(2s)) bytes (fp16 K+V, one fp16 index vector per cluster / segment), for this rank's heads and
+    the whole batch, with s = the config's mean segment length; next to it the same quantities as this
+    build keeps them (retrieval layers: sinks S + double-buffered working set 2B + local buffer W rows
+    of K+V bf16, one fp32 master + one bf16 copy per unit index at the unit-table capacity; full-cache
+    layers: everything)."""
+    L, Lf = cfg.num_layers, len(cfg.full_cache_layers)
+    n, m, B, c, s_ = cfg.prompt_len, m_out, cfg.budget_tokens, cfg.avg_cluster_size, cfg.seg_mean
+    hd = hc * cfg.head_dim * cfg.batch
+    full = 4 * L * hd * (n + m)
+    louis = 4 * L * hd * (B + n / (2 * c) + m / (2 * s_))
+    units_cap = -(-((n - cfg.sink_tokens) // c + m) // 256) * 256
+    ours = (4 * (L - Lf) * hd * (cfg.sink_tokens + 2 * B + cfg.window_tokens + 2)
+            + (L - Lf) * hd * units_cap * (4 + 2)
+            + 4 * Lf * hd * (n + m))
+    return {"fullcache_formula_bytes": full, "louiskv_formula_bytes": louis, "build_kv_state_bytes": ours,
+            "build_over_formula": ours / louis,
+            "note": "the build's excess over the formula: the first two layers kept in full (P:143; not in "
+                    "Table 3), the double-buffered working set, sinks and local buffer, and fp32 + bf16 unit "
+                    "indices sized to capacity (the formula counts one fp16 vector per unit)"}
+
+
 # ----------------------------------------------------------------------------- oracle (CPU) legs
 # Only bench's cpu_baseline leg and --impl reference execute anything under oracle/ (tier rule ③).
 def _oracle_worker(args):
@@ -791,6 +814,7 @@ def main(argv=None):
         "l2_pressure": l2v,
         "host_link_h2d_gbs": host_link_gbs,
         "memory": dict(ctx.memory(), full_kv_bytes=b * hc * L * (cfg.prompt_len + cap_out) * 512,
+                       table3=table3_accounting(cfg, hc, cap_out),
                        note="device_bytes: every device allocation of the context; full_kv_bytes: the K+V bf16 of "
                             "every layer at P + capacity (a full-cache engine's device footprint); the offloaded "
                             "rows live in the pinned host pool (P:404-425)"),
