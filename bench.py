@@ -752,7 +752,14 @@ def main(argv=None):
         roof_full["traffic"] = tr["attn_full_tc_kernel"]
     if "layer_kernel" in tr:
         roof_layer_hbm["traffic"] = tr["layer_kernel"]
-    dominant = roof_full if share_full > share_ret else roof_layer_link
+    # the dominant kernel's binding resource: of the host link and HBM, the one whose lower-bound time
+    # for the measured bytes is larger (C2 / C4: the link; C3, where retrievals move few host bytes:
+    # HBM — the kernel is latency-bound there)
+    lb_link = link_bytes / (host_link_gbs * 1e9) if host_link_gbs else 0.0
+    lb_hbm = ret_bytes / (hbm_peak * 1e9)
+    roof_layer = roof_layer_link if lb_link >= lb_hbm else roof_layer_hbm
+    roof_layer["binding"] = {"host_link_lower_bound_ms": lb_link * 1e3, "hbm_lower_bound_ms": lb_hbm * 1e3}
+    dominant = roof_full if share_full > share_ret else roof_layer
     # k-means: the assignment GEMM (tensor pipe) and the Lloyd loop, from the phase timer
     lloyd_ms = pt["init_ms"] + pt["assign_ms"] + pt["sort_ms"] + pt["update_ms"]
     gemm_tf = pt["assign_flops"] / (pt["assign_ms"] / 1e3) / 1e12 if pt["assign_ms"] > 0 else 0.0

@@ -145,10 +145,10 @@ __global__ void __launch_bounds__(256) km_hist_kernel(KmArgs a, int nchunk) {
   const int32_t* as = a.assign + (int64_t)li * a.Nmax;
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) atomicAdd(&hist[as[i]], 1);
   __syncthreads();
-  // chunk counts are stored transposed, cc[inst][cluster][chunk], so each cluster's prefix over
-  // chunks is one contiguous vector for km_scan
-  int32_t* cc = a.cc + (int64_t)li * a.kmax * a.nchunk_max + c;
-  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) cc[(int64_t)j * a.nchunk_max] = hist[j];
+  // chunk counts, chunk-major cc[inst][chunk][cluster]: one coalesced row per chunk (the column
+  // scan walks the chunks per cluster with one thread per cluster, coalesced too)
+  int32_t* cc = a.cc + ((int64_t)li * a.nchunk_max + c) * a.kmax;
+  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) cc[j] = hist[j];
 }
 
 // column scan of cc + cluster offsets; one 1024-thread CTA per instance
@@ -179,92 +179,29 @@ __device__ int km_block_excl_scan(int v, int& total) {
   return r;
 }
 
-// per-cluster prefix over chunks (contiguous rows of the transposed cc), counts, cluster offsets
-// (counting sort) and the update-task offsets (ceil(count / KM_TASK) tasks per cluster)
-__device__ void km_scan_block(const KmArgs& a, int li, int nchunk) {
-  __shared__ int s_empty;
-  int32_t* cnt = a.cnt + (int64_t)li * a.kmax;
-  int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
-  int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
-  int4* tcl = a.tcl + (int64_t)li * a.task_max;
-  if (threadIdx.x == 0) s_empty = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < a.kc; j += blockDim.x) {
-    int32_t* row = a.cc + ((int64_t)li * a.kmax + j) * a.nchunk_max;
-    int run = 0;
-    int32_t* ccT = a.ccT + (int64_t)li * a.nchunk_max * a.kmax;
-    for (int c0 = 0; c0 < nchunk; c0 += 8) {
-      int v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = (c0 + q < nchunk) ? row[c0 + q] : 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + q < nchunk) {
-          ccT[(int64_t)(c0 + q) * a.kmax + j] = run;
-          run += v[q];
-        }
-    }
-    cnt[j] = run;
-    if (run == 0) s_empty = 1;
-  }
-  __syncthreads();
-  const int per = (a.kc + blockDim.x - 1) / blockDim.x;
-  const int j0 = threadIdx.x * per, j1 = min(a.kc, j0 + per);
-  int local = 0, tloc = 0;
-  for (int j = j0; j < j1; ++j) {
-    local += cnt[j];
-    tloc += (cnt[j] + KM_TASK - 1) / KM_TASK;
-  }
-  int total, ttotal;
-  int run = km_block_excl_scan(local, total);
-  int trun = km_block_excl_scan(tloc, ttotal);
-  for (int j = j0; j < j1; ++j) {
-    off[j] = run;
-    toff[j] = trun;
-    {  // the update tasks of cluster j: (cluster, first member, end member, tasks of the cluster)
-      const int nt = (cnt[j] + KM_TASK - 1) / KM_TASK;
-      for (int q = 0; q < nt; ++q)
-        tcl[trun + q] = make_int4(j, run + q * KM_TASK, min(run + cnt[j], run + (q + 1) * KM_TASK), nt);
-      trun += nt;
-    }
-    run += cnt[j];
-  }
-  if (threadIdx.x == 0) {
-    off[a.kc] = a.N;
-    toff[a.kc] = ttotal;
-    a.flags[li] = s_empty;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(1024) km_scan_kernel(KmArgs a, int nchunk) {
-  pdl_wait_trigger(); km_scan_block(a, blockIdx.x, nchunk); }
-
-// column scan (many CTAs): warp per cluster, lanes over chunks: exclusive prefix of the cluster's
-// chunk counts -> chunk-major ccT[inst][chunk][cluster] (coalesced reads for the scatter), count
+// column scan: one thread per cluster walks the chunks in order (coalesced over clusters): the
+// cluster's exclusive prefix per chunk -> ccT[inst][chunk][cluster] (the scatter's bases), count
 __global__ void __launch_bounds__(256) km_colscan_kernel(KmArgs a, int nchunk, int only_dirty) {
   pdl_wait_trigger();
   const int li = blockIdx.y;
   if (only_dirty && a.flags[li] != 2) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * 8 + warp;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.kc) return;
-  const int32_t* row = a.cc + ((int64_t)li * a.kmax + j) * a.nchunk_max;
-  int32_t* ccT = a.ccT + (int64_t)li * a.nchunk_max * a.kmax;
-  int carry = 0;
-  for (int c0 = 0; c0 < nchunk; c0 += 32) {
-    const int c = c0 + lane;
-    const int v = c < nchunk ? row[c] : 0;
-    int incl = v;
+  const int32_t* cc = a.cc + (int64_t)li * a.nchunk_max * a.kmax + j;
+  int32_t* ccT = a.ccT + (int64_t)li * a.nchunk_max * a.kmax + j;
+  int run = 0;
+  for (int c0 = 0; c0 < nchunk; c0 += 8) {
+    int v[8];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (c < nchunk) ccT[(int64_t)c * a.kmax + j] = carry + incl - v;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
+    for (int q = 0; q < 8; ++q) v[q] = c0 + q < nchunk ? cc[(int64_t)(c0 + q) * a.kmax] : 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (c0 + q < nchunk) {
+        ccT[(int64_t)(c0 + q) * a.kmax] = run;
+        run += v[q];
+      }
   }
-  if (lane == 0) a.cnt[(int64_t)li * a.kmax + j] = carry;
+  a.cnt[(int64_t)li * a.kmax + j] = run;
 }
 
 // cluster offsets and update-task offsets from the counts (one CTA per instance)
@@ -491,8 +428,8 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
       s_cnt[j] = 1;
       as[i] = j;
       dm[i] = -INFINITY;
-      atomicSub(&a.cc[((int64_t)li * a.kmax + cl) * a.nchunk_max + i / KM_CHUNK], 1);
-      atomicAdd(&a.cc[((int64_t)li * a.kmax + j) * a.nchunk_max + i / KM_CHUNK], 1);
+      atomicSub(&a.cc[((int64_t)li * a.nchunk_max + i / KM_CHUNK) * a.kmax + cl], 1);
+      atomicAdd(&a.cc[((int64_t)li * a.nchunk_max + i / KM_CHUNK) * a.kmax + j], 1);
     }
     s_filled = r;
   }
@@ -541,8 +478,8 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
         as[d] = j;
         cnt[j] = 1;
         dm[d] = -INFINITY;
-        atomicSub(&a.cc[((int64_t)li * a.kmax + from) * a.nchunk_max + d / KM_CHUNK], 1);
-        atomicAdd(&a.cc[((int64_t)li * a.kmax + j) * a.nchunk_max + d / KM_CHUNK], 1);
+        atomicSub(&a.cc[((int64_t)li * a.nchunk_max + d / KM_CHUNK) * a.kmax + from], 1);
+        atomicAdd(&a.cc[((int64_t)li * a.nchunk_max + d / KM_CHUNK) * a.kmax + j], 1);
       }
     }
     __syncthreads();
@@ -792,12 +729,12 @@ cudaError_t launch_assign_tc(const KmArgs& a, cudaStream_t st);  // k_kmeans_tc.
 
 static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool repair, cudaStream_t st) {
   launch_k(km_hist_kernel, dim3(dim3(nchunk, ni)), dim3(256), sizeof(int) * a.kc, st, a, nchunk);
-  launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 0);
+  launch_k(km_colscan_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, nchunk, 0);
   launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 0);
   if (repair) {
     const size_t rsm = repair_smem_base(a.kc) + (repair_keys_in_smem(a.kc, a.N) ? sizeof(unsigned) * (size_t)a.N : 0);
     launch_k(km_repair_kernel, dim3(ni), dim3(1024), rsm, st, a, nchunk);
-    launch_k(km_colscan_kernel, dim3(dim3((a.kc + 7) / 8, ni)), dim3(256), 0, st, a, nchunk, 1);
+    launch_k(km_colscan_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, nchunk, 1);
     launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);
   }
   launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), sizeof(int) * a.kc, st, a);

@@ -116,6 +116,7 @@ __device__ __forceinline__ int rep_x_offset(int n, bool big) {
   return big ? ((((n + 31) / 32) * 4 + 15) & ~15) : rep_off_x(n);
 }
 
+
 // Returns the row count of the new working set; *nsel = selected units (LIST entries, at shared
 // offset rep_x_offset(n, big)); own_dst[i] = destination row of own unit lo+i (-1: not selected) for
 // the deferred sel/seloff update.
@@ -661,50 +662,49 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   const int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
   const int64_t* uoff = a.uoff + (int64_t)li * a.Umax;
   unsigned long long reused = 0, fetched = 0, hbytes = 0;
-  constexpr int LB_N = 8;  // the selection-state loads of 8 units are issued together (one round trip)
-  for (int ub = u0; ub < u1; ub += LB_N) {
+  constexpr int LB_N = 8;  // the selection-state loads of up to 8 TAKEN units are issued together
+  int ub = u0;
+  while (true) {
+    int uid[LB_N], nb = 0;
+    while (ub < u1 && nb < LB_N) {  // the next taken units of this thread's id range, in id order
+      if (TK[ub >> 5] >> (ub & 31) & 1u) uid[nb++] = ub;
+      ++ub;
+    }
+    if (nb == 0) break;
     uint8_t hadv[LB_N];
     int sov[LB_N];
     int64_t uov[LB_N];
 #pragma unroll
-    for (int i = 0; i < LB_N; ++i) {
-      const int u = ub + i;
-      hadv[i] = 0;
-      sov[i] = 0;
-      uov[i] = 0;
-      if (u < u1 && (TK[u >> 5] >> (u & 31) & 1u)) {
-        hadv[i] = sel[u];
-        sov[i] = seloff[u];
-        uov[i] = uoff[u];
+    for (int i = 0; i < LB_N; ++i)
+      if (i < nb) {
+        hadv[i] = sel[uid[i]];
+        sov[i] = seloff[uid[i]];
+        uov[i] = uoff[uid[i]];
       }
-    }
 #pragma unroll
     for (int i = 0; i < LB_N; ++i) {
-    const int u = ub + i;
-    if (u >= u1 || !(TK[u >> 5] >> (u & 31) & 1u)) continue;
-    const int sz = SZ[u];
-    const uint8_t had = hadv[i];
-    const int so = sov[i];
-    const int64_t uo = uov[i];
-    SelEnt e;
-    e.dst = dst;
-    e.sz = sz;
-    e.u = u;
-    e.pad = 0;
-    if (had) {
-      e.kb = curK + (int64_t)so * ROW_BYTES;
-      e.vb = curV + (int64_t)so * ROW_BYTES;
-      ++reused;
-    } else {
-      const uint8_t* base = pool + uo * POOL_ROW_BYTES;
-      e.kb = base;
-      e.vb = base + (int64_t)sz * ROW_BYTES;
-      ++fetched;
-      hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
-    }
-    LIST[k++] = e;
-    if (u >= lo && u < hi) own_dst[u - lo] = dst;
-    dst += sz;
+      if (i >= nb) break;
+      const int u = uid[i];
+      const int sz = SZ[u];
+      SelEnt e;
+      e.dst = dst;
+      e.sz = sz;
+      e.u = u;
+      e.pad = 0;
+      if (hadv[i]) {
+        e.kb = curK + (int64_t)sov[i] * ROW_BYTES;
+        e.vb = curV + (int64_t)sov[i] * ROW_BYTES;
+        ++reused;
+      } else {
+        const uint8_t* base = pool + uov[i] * POOL_ROW_BYTES;
+        e.kb = base;
+        e.vb = base + (int64_t)sz * ROW_BYTES;
+        ++fetched;
+        hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
+      }
+      LIST[k++] = e;
+      if (u >= lo && u < hi) own_dst[u - lo] = dst;
+      dst += sz;
     }
   }
   if (rank == 0) {
