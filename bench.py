@@ -752,6 +752,15 @@ def main(argv=None):
         roof_full["traffic"] = tr["attn_full_tc_kernel"]
     if "layer_kernel" in tr:
         roof_layer_hbm["traffic"] = tr["layer_kernel"]
+    # the flagged launches alone against the host link (the resource a retrieval is bound by): the
+    # attribution pass's host-pool bytes ÷ (flagged launches × the fitted flagged-launch time)
+    h2d_attr = st_d["bytes_h2d"] - st_c["bytes_h2d"]
+    fl_gbs = h2d_attr / (n_flg_tot * f_ms / 1e3) / 1e9 if n_flg_tot and f_ms > 0 else 0.0
+    flagged_link = {"kernel": "layer_kernel, flagged launches (trigger + score/select + host gather + append + "
+                              "attention)", "bound": "host_link", "achieved": fl_gbs, "peak": host_link_gbs,
+                    "unit": "GB/s", "frac": fl_gbs / host_link_gbs if host_link_gbs else None,
+                    "bytes_per_flagged_launch": h2d_attr / max(n_flg_tot, 1), "us_per_flagged_launch": f_ms * 1e3,
+                    "note": "counter-backed: ncu pcie__read_bytes on flagged launches, profiles/r02_ncu_summary.md"}
     # the dominant kernel's binding resource: of the host link and HBM, the one whose lower-bound time
     # for the measured bytes is larger (C2 / C4: the link; C3, where retrievals move few host bytes:
     # HBM — the kernel is latency-bound there)
@@ -807,6 +816,7 @@ def main(argv=None):
         "roofline": dominant,
         "roofline_layer_link": roof_layer_link,
         "roofline_layer_hbm": roof_layer_hbm,
+        "roofline_flagged_link": flagged_link,
         "roofline_full_cache": roof_full,
         "roofline_kmeans": roof_km,
         "kmeans_keys_per_s": kmeans["keys_per_s_lloyd"],

@@ -66,6 +66,7 @@ struct louiskv_ctx {
   int32_t* d_km_off = nullptr;
   int32_t* d_km_cnt = nullptr;
   int32_t* d_km_perm = nullptr;
+  int32_t* d_km_tperm = nullptr;
   int32_t* d_km_flags = nullptr;
   int32_t* d_km_toff = nullptr;
   int4* d_km_tcl = nullptr;
@@ -446,6 +447,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   c->km_task_max = std::max(c->kmax, 1) + (int)((c->Nmax + 31) / 32);
   ok = ok && dalloc(c, &c->d_km_toff, (size_t)nl * (c->kmax + 1));
   ok = ok && dalloc(c, &c->d_km_tcl, (size_t)nl * c->km_task_max);
+  ok = ok && dalloc(c, &c->d_km_tperm, (size_t)nl * c->km_task_max * 32);
   ok = ok && dalloc(c, &c->d_km_bext, (size_t)nl * c->Umax * 8);
   ok = ok && dalloc(c, &c->d_km_ccT, (size_t)nl * std::max(c->nchunk_max, 1) * std::max(c->kmax, 1));
   ok = ok && dalloc(c, &c->d_km_upart, (size_t)nl * c->km_task_max * D);
@@ -635,6 +637,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.off = c->d_km_off;
   a.cnt = c->d_km_cnt;
   a.perm = c->d_km_perm;
+  a.tperm = c->d_km_tperm;
   a.flags = c->d_km_flags;
   a.toff = c->d_km_toff;
   a.tcl = c->d_km_tcl;

@@ -491,25 +491,32 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
 // stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
 __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   pdl_wait_trigger();
-  extern __shared__ int base[];  // [kc] running offsets of this chunk
+  extern __shared__ int base[];  // [kc] running offsets of this chunk, then [kc] the padded ones
+  int* pbase = base + a.kc;      // (task-padded order: cluster j's members at 32 toff[j] + rank)
   const int li = blockIdx.y, c = blockIdx.x, lane = threadIdx.x;
   const int32_t* ccT = a.ccT + ((int64_t)li * a.nchunk_max + c) * a.kmax;
   const int32_t* off = a.off + (int64_t)li * (a.kmax + 1);
-  for (int j0 = lane; j0 < a.kc; j0 += 8 * 32) {  // 16 loads per lane in flight per batch
-    int cv[8], ov[8];
+  const int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
+  for (int j0 = lane; j0 < a.kc; j0 += 8 * 32) {  // 24 loads per lane in flight per batch
+    int cv[8], ov[8], tv[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int j = j0 + r * 32;
       cv[r] = j < a.kc ? ccT[j] : 0;
       ov[r] = j < a.kc ? off[j] : 0;
+      tv[r] = j < a.kc ? toff[j] : 0;
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r)
-      if (j0 + r * 32 < a.kc) base[j0 + r * 32] = cv[r] + ov[r];
+      if (j0 + r * 32 < a.kc) {
+        base[j0 + r * 32] = cv[r] + ov[r];
+        pbase[j0 + r * 32] = cv[r] + tv[r] * KM_TASK;
+      }
   }
   __syncwarp();
   const int32_t* as = a.assign + (int64_t)li * a.Nmax;
   int32_t* perm = a.perm + (int64_t)li * a.Nmax;
+  int32_t* tperm = a.tperm + (int64_t)li * a.task_max * KM_TASK;
   const int i0 = c * KM_CHUNK, i1 = min(a.N, i0 + KM_CHUNK);
   // prefetch the chunk's assignments (32 per lane) so the rounds below only touch registers/smem
   int cl_pre[KM_CHUNK / 32];
@@ -526,12 +533,22 @@ __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
     const unsigned peers = __match_any_sync(0xffffffffu, cl);
     const int leader = __ffs(peers) - 1;
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    int bs = 0;
-    if (valid && lane == leader) bs = base[cl];
+    int bs = 0, ps = 0;
+    if (valid && lane == leader) {
+      bs = base[cl];
+      ps = pbase[cl];
+    }
     bs = __shfl_sync(0xffffffffu, bs, leader);
-    if (valid) perm[bs + rank] = i;
+    ps = __shfl_sync(0xffffffffu, ps, leader);
+    if (valid) {
+      perm[bs + rank] = i;
+      tperm[ps + rank] = i;
+    }
     __syncwarp();
-    if (valid && lane == leader) base[cl] = bs + __popc(peers);
+    if (valid && lane == leader) {
+      base[cl] = bs + __popc(peers);
+      pbase[cl] = ps + __popc(peers);
+    }
     __syncwarp();
   }
 }
@@ -568,11 +585,12 @@ __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
   // the task (written with the offsets): cluster j, members [m0, m1) of the cluster-sorted order,
   // tasks of j; lane i holds member m0 + i's position, so all <= 32 member rows are loaded in two
   // batches of 16 (three round trips in all), summed in member order (deterministic)
+  // (the task and its members' positions — task-padded order — load in the same round trip)
   const int4 tk = a.tcl[(int64_t)li * a.task_max + t];
+  const int pi_raw = a.tperm[((int64_t)li * a.task_max + t) * KM_TASK + lane];
   const int j = tk.x, m0 = tk.y, m1 = tk.z, ntask = tk.w;
-  const int32_t* perm = a.perm + (int64_t)li * a.Nmax;
   const int nm = m1 - m0;
-  const int pi = lane < nm ? perm[m0 + lane] : 0;
+  const int pi = lane < nm ? pi_raw : 0;
   float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int rb = 0; rb < KM_TASK; rb += 16) {
@@ -737,7 +755,7 @@ static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool rep
     launch_k(km_colscan_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, nchunk, 1);
     launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);
   }
-  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), sizeof(int) * a.kc, st, a);
+  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), 2 * sizeof(int) * a.kc, st, a);
   return cudaGetLastError();
 }
 

@@ -255,6 +255,7 @@ struct KmArgs {
   int32_t* off;      // [ni][kmax+1]
   int32_t* cnt;      // [ni][kmax]
   int32_t* perm;     // [ni][Nmax]
+  int32_t* tperm;    // [ni][task_max][32] members in task-padded order (update task t: slots 32 t ..)
   int32_t* flags;    // [ni]
   int64_t Nmax;
   int kmax;
