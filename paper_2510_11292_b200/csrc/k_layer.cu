@@ -554,31 +554,49 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   // (b) prefix run taken; (c) tail candidates compacted as key | size << 48
   unsigned long long* T = LB;  // (the lists are dead)
   const int T_CAP = x_bytes / 8;
+  __shared__ int s_tc[LK_W];
+  if (tid == 0) s_nc = 0;  // (every read of s_nc in the radix loop precedes its last barrier)
   __syncthreads();  // (the id lists in the same region are dead)
-  if (tid == 0) s_nc = 0;
-  __syncthreads();
-  // one warp per 32 consecutive units: the taken bits are one TK word (exclusive owner, plain
-  // store), the tail candidates are compacted with one shared atomic per warp
+  // one warp per 32 consecutive units; two passes, no shared counter (a returning atomic per 32
+  // units serialised the warps): (1) the taken bits (one TK word each, exclusive owner) and the
+  // warp's tail-candidate count; (2) after a prefix over the warps, the candidates written in id
+  // order to one contiguous list
+  int wcnt = 0;
   for (int base = warp * 32; base < n; base += AT_THREADS) {
     const int u = base + lane;
     bool take = false, cand = false;
-    unsigned long long k = 0;
     if (u < n) {
-      k = rep_key(RA, u);
+      const unsigned long long k = rep_key(RA, u);
       take = k < pivot;
       cand = rem1 > 0 && k > pivot && SZ[u] <= rem1;
     }
     const unsigned tbits = __ballot_sync(0xffffffffu, take);
-    const unsigned cbits = __ballot_sync(0xffffffffu, cand);
     if (lane == 0) TK[base >> 5] = tbits;
-    int b0 = 0;
-    if (lane == 0 && cbits) b0 = atomicAdd(&s_nc, __popc(cbits));
-    b0 = __shfl_sync(0xffffffffu, b0, 0);
-    if (cand) {
-      const int slot = b0 + __popc(cbits & ((1u << lane) - 1u));
-      if (slot < T_CAP) T[slot] = k | ((unsigned long long)SZ[u] << 48);
+    wcnt += __popc(__ballot_sync(0xffffffffu, cand));
+  }
+  if (lane == 0) s_tc[warp] = wcnt;
+  __syncthreads();
+  int woff = 0, nt_all = 0;
+#pragma unroll
+  for (int w = 0; w < LK_W; ++w) {
+    woff += w < warp ? s_tc[w] : 0;
+    nt_all += s_tc[w];
+  }
+  if (rem1 > 0 && nt_all <= T_CAP) {
+    for (int base = warp * 32; base < n; base += AT_THREADS) {
+      const int u = base + lane;
+      bool cand = false;
+      unsigned long long k = 0;
+      if (u < n) {
+        k = rep_key(RA, u);
+        cand = k > pivot && SZ[u] <= rem1;
+      }
+      const unsigned cbits = __ballot_sync(0xffffffffu, cand);
+      if (cand) T[woff + __popc(cbits & ((1u << lane) - 1u))] = k | ((unsigned long long)SZ[u] << 48);
+      woff += __popc(cbits);
     }
   }
+  if (tid == 0) s_nc = nt_all;
   prof_stamp(prof, 15);
   __syncthreads();
   if (rem1 > 0) {
