@@ -16,7 +16,8 @@
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Hot calls only ENQUEUE work; none of should_retrieve / retrieve /
  *    append_output / sparse_attn synchronises with the host, so a whole decode
- *    step is CUDA-graph capturable.
+ *    step is CUDA-graph capturable (the one exception: retrieve with
+ *    fetch_mode LOUISKV_FETCH_BATCHED_DMA, documented there).
  *  - Layout: head_dim d must be 128. K/V/q/out elements are bf16 (uint16 bits),
  *    d contiguous. Strides are in ELEMENTS.
  *  - Errors: argument/state errors return synchronously and enqueue nothing.
@@ -52,7 +53,15 @@ typedef enum {
 
 enum { LOUISKV_TRIG_PREV_STEP = 0, LOUISKV_TRIG_LAST_RETRIEVAL = 1 };
 enum { LOUISKV_BOUNDARY_PER_LAYER = 0, LOUISKV_BOUNDARY_SHARED = 1 };
-enum { LOUISKV_FETCH_ZERO_COPY = 0 };
+/* gather of the selected units' rows ("transfer data from specific rows"):
+ * ZERO_COPY   — the select kernel's own threads read the pinned pool through its device mapping with
+ *               16-B vector loads (no host involvement; graph-capturable; the default);
+ * BATCHED_DMA — select writes per-unit copy spans (K rows, V rows) into mapped pinned memory; the
+ *               host waits for them (louiskv_retrieve synchronises its stream) and issues ONE
+ *               cudaMemcpyBatchAsync per layer (host pool -> working set for new units, device ->
+ *               device for kept units) on the copy engines. Not graph-capturable (retrieve returns
+ *               STATE inside a capture); louiskv_decode_layer then issues the per-call sequence. */
+enum { LOUISKV_FETCH_ZERO_COPY = 0, LOUISKV_FETCH_BATCHED_DMA = 1 };
 enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
 /* prompt units: semantic k-means clusters (the method) or contiguous pages (the page units of
  * the paper's comparison systems, §3.1 P:63 "partition the entire key cache ... into m fixed-size
@@ -79,7 +88,8 @@ typedef struct {
   int32_t boundary_mode;     /* LOUISKV_BOUNDARY_PER_LAYER | _SHARED */
   int32_t shared_layer;      /* designated layer for SHARED mode */
   int32_t max_open_segment;  /* force-seal bound on the open segment (0 -> window_tokens) */
-  int32_t fetch_mode;        /* LOUISKV_FETCH_ZERO_COPY */
+  int32_t fetch_mode;        /* LOUISKV_FETCH_ZERO_COPY (default) | LOUISKV_FETCH_BATCHED_DMA; other
+                                values: INVALID_ARG at create */
   int32_t device;            /* CUDA device ordinal */
   int32_t attn_impl;         /* full-cache attention: LOUISKV_ATTN_TC (mma.sync + TMA tensor maps,
                                 default) | LOUISKV_ATTN_SIMT (CUDA cores) */
@@ -162,7 +172,9 @@ louiskv_status louiskv_should_retrieve(louiskv_ctx* ctx, int32_t layer, const vo
  * the selected units' KV rows (new units from the pinned host pool over the host link, kept
  * units device-to-device) into the working set. Unflagged sequences are untouched.
  * q_own: device bf16 [batch][g*kv_head_count][d] (owned query heads). No-op on full-cache
- * layers. Errors: INVALID_ARG, STATE. */
+ * layers. fetch_mode BATCHED_DMA: the call synchronises `stream` after the selection (the span lists
+ * must reach the host) and enqueues one batched copy; STATE when `stream` is capturing.
+ * Errors: INVALID_ARG, STATE, CUDA. */
 louiskv_status louiskv_retrieve(louiskv_ctx* ctx, int32_t layer, const void* q_own, int64_t stride_b, void* stream);
 
 /* kvm.store_cache(k_t, v_t, 'decode'): seal the open segment at a boundary

@@ -23,6 +23,7 @@ TRIG_PREV_STEP, TRIG_LAST_RETRIEVAL = 0, 1
 BOUNDARY_PER_LAYER, BOUNDARY_SHARED = 0, 1
 KMEANS_TC, KMEANS_SIMT = 0, 1
 UNITS_KMEANS, UNITS_PAGES = 0, 1
+FETCH_ZERO_COPY, FETCH_BATCHED_DMA = 0, 1
 
 _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE", 5: "OOM_HOST", 6: "CUDA",
            7: "NOT_IMPLEMENTED"}
@@ -141,7 +142,8 @@ def _stream(stream) -> Optional[int]:
 
 def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigger_ref=TRIG_PREV_STEP,
                 boundary_mode=BOUNDARY_PER_LAYER, shared_layer=0, max_open_segment=0, kmeans_impl=KMEANS_TC,
-                device=0, max_output_len=None, attn_impl=0, trigger_stride=0, prompt_units=0) -> Config:
+                device=0, max_output_len=None, attn_impl=0, trigger_stride=0, prompt_units=0,
+                fetch_mode=FETCH_ZERO_COPY) -> Config:
     """Build the C config from a synth.configs.Config-like object (plain numbers)."""
     mask = 0
     for l in cfg.full_cache_layers:
@@ -155,7 +157,7 @@ def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigge
                   tau=cfg.tau, avg_cluster_size=cfg.avg_cluster_size, kmeans_iters=cfg.kmeans_iters,
                   kmeans_impl=kmeans_impl, full_cache_layers=mask, trigger_ref=trigger_ref,
                   boundary_mode=boundary_mode, shared_layer=shared_layer, max_open_segment=max_open_segment,
-                  fetch_mode=0, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride,
+                  fetch_mode=fetch_mode, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride,
                   prompt_units=prompt_units)
 
 

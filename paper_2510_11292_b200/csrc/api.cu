@@ -56,6 +56,17 @@ struct louiskv_ctx {
   uint8_t* d_ssort = nullptr;
   RowSrc* d_rows = nullptr;
   GatherJob* d_jobs = nullptr;  // [L][Bmax*hn]
+  // BATCHED_DMA fetch: span lists written by select into mapped pinned memory, a copy stream for
+  // callers on the legacy default stream (cudaMemcpyBatchAsync rejects it), host-side batch arrays
+  DmaSpan* h_spans = nullptr;
+  int32_t* h_span_n = nullptr;
+  DmaSpan* d_spans = nullptr;
+  int32_t* d_span_n = nullptr;
+  int dma_cap = 0;
+  cudaStream_t dma_stream = nullptr;
+  cudaEvent_t ev_dma = nullptr;
+  std::vector<void*> dma_dst, dma_src;
+  std::vector<size_t> dma_size;
   float* d_part = nullptr;
   int* d_counters = nullptr;
   int max_splits = 64;
@@ -315,6 +326,50 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
   return a;
 }
 
+// BATCHED_DMA fetch (§4.3: selected rows moved by the DMA engines, the analogue of the paper's
+// DGL row transfer): wait for select's span lists (mapped pinned memory), then ONE
+// cudaMemcpyBatchAsync of every span of every flagged instance of the layer — new units host pool ->
+// next working set over the host link, kept units current -> next working set on the device. The
+// copies are mutually independent (disjoint destinations; sources are the pool and the other buffer).
+cudaError_t batched_dma_fetch(louiskv_ctx* c, cudaStream_t st) {
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  c->dma_dst.clear();
+  c->dma_src.clear();
+  c->dma_size.clear();
+  const int ni = c->batch * c->hn;
+  for (int li = 0; li < ni; ++li) {
+    const int n = c->h_span_n[li];
+    if (n < 0 || n > c->dma_cap) return cudaErrorIllegalState;
+    const DmaSpan* sp = c->h_spans + (size_t)li * c->dma_cap;
+    for (int i = 0; i < n; ++i) {
+      uint64_t src = sp[i].src;
+      // host-pool sources: device-mapped address -> the pool's host address
+      const uint64_t dp = reinterpret_cast<uint64_t>(c->d_pool);
+      if (c->d_pool && src >= dp && src < dp + c->host_bytes)
+        src = reinterpret_cast<uint64_t>(c->h_pool) + (src - dp);
+      c->dma_src.push_back(reinterpret_cast<void*>(src));
+      c->dma_dst.push_back(reinterpret_cast<void*>(sp[i].dst));
+      c->dma_size.push_back((size_t)sp[i].bytes);
+    }
+  }
+  if (c->dma_size.empty()) return cudaSuccess;
+  const bool legacy = st == nullptr || st == cudaStreamLegacy;
+  cudaStream_t cs = legacy ? c->dma_stream : st;  // (the batch API rejects the legacy default stream)
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t idx0 = 0, fail_idx = 0;
+  e = cudaMemcpyBatchAsync(c->dma_dst.data(), c->dma_src.data(), c->dma_size.data(), c->dma_size.size(), &attr,
+                           &idx0, 1, &fail_idx, cs);
+  if (e != cudaSuccess) return e;
+  if (legacy) {
+    if ((e = cudaEventRecord(c->ev_dma, cs)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, c->ev_dma, 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -332,6 +387,10 @@ void louiskv_destroy(louiskv_ctx* ctx) {
   for (cudaEvent_t e : {ctx->ev_free[0], ctx->ev_free[1], ctx->ev_staged})
     if (e) cudaEventDestroy(e);
   if (ctx->off_stream) cudaStreamDestroy(ctx->off_stream);
+  if (ctx->dma_stream) cudaStreamDestroy(ctx->dma_stream);
+  if (ctx->ev_dma) cudaEventDestroy(ctx->ev_dma);
+  if (ctx->h_spans) cudaFreeHost(ctx->h_spans);
+  if (ctx->h_span_n) cudaFreeHost(ctx->h_span_n);
   for (cudaEvent_t e : ctx->prec.pool)
     if (e) cudaEventDestroy(e);
   for (auto& sb : ctx->snap)
@@ -359,6 +418,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       k.max_output_len <= 0 || k.budget_tokens < 0 || k.sink_tokens < 0 || k.window_tokens < 1 ||
       k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) || k.trigger_stride < 0 ||
       (k.prompt_units != LOUISKV_UNITS_KMEANS && k.prompt_units != LOUISKV_UNITS_PAGES) ||
+      (k.fetch_mode != LOUISKV_FETCH_ZERO_COPY && k.fetch_mode != LOUISKV_FETCH_BATCHED_DMA) ||
       (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
     return LOUISKV_ERR_INVALID_ARG;
   const int g = k.num_q_heads / k.num_kv_heads;
@@ -470,6 +530,24 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
     c->off_pending.assign(c->L, 0);
     for (int l = 0; l < c->L && ok; ++l)
       ok = cudaEventCreateWithFlags(&c->ev_done[l], cudaEventDisableTiming) == cudaSuccess;
+  }
+  if (ok && k.fetch_mode == LOUISKV_FETCH_BATCHED_DMA) {
+    c->dma_cap = 2 * std::max(c->Bud, 1);
+    void *hs = nullptr, *hn_ = nullptr, *ds = nullptr, *dn = nullptr;
+    ok = cudaHostAlloc(&hs, sizeof(DmaSpan) * nl * c->dma_cap, cudaHostAllocMapped) == cudaSuccess &&
+         cudaHostAlloc(&hn_, sizeof(int32_t) * nl, cudaHostAllocMapped) == cudaSuccess;
+    c->h_spans = reinterpret_cast<DmaSpan*>(hs);
+    c->h_span_n = reinterpret_cast<int32_t*>(hn_);
+    ok = ok && cudaHostGetDevicePointer(&ds, hs, 0) == cudaSuccess &&
+         cudaHostGetDevicePointer(&dn, hn_, 0) == cudaSuccess;
+    c->d_spans = reinterpret_cast<DmaSpan*>(ds);
+    c->d_span_n = reinterpret_cast<int32_t*>(dn);
+    ok = ok && cudaStreamCreateWithFlags(&c->dma_stream, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_dma, cudaEventDisableTiming) == cudaSuccess;
+    c->dma_dst.reserve((size_t)nl * c->dma_cap);
+    c->dma_src.reserve((size_t)nl * c->dma_cap);
+    c->dma_size.reserve((size_t)nl * c->dma_cap);
+    if (!ok) cudaGetLastError();
   }
   if (!ok) {
     louiskv_destroy(c);
@@ -739,6 +817,18 @@ louiskv_status louiskv_retrieve(louiskv_ctx* c, int32_t layer, const void* q_own
   LKV_LAUNCH(c, offload_wait(c, layer, st), "prompt offload wait");
   RetrieveArgs a = retrieve_args(c, layer, q_own, stride_b);
   a.budget = std::max(c->Bud, 0);
+  if (c->cfg.fetch_mode == LOUISKV_FETCH_BATCHED_DMA) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LKV_LAUNCH(c, cudaStreamIsCapturing(st, &cs), "retrieve: capture status");
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(c, LOUISKV_ERR_STATE, "retrieve: BATCHED_DMA synchronises the host and cannot be graph-captured");
+    a.dma_spans = c->d_spans;
+    a.dma_n = c->d_span_n;
+    a.dma_cap = c->dma_cap;
+    LKV_LAUNCH(c, launch_select_gather(a, st), "select (span list)");
+    LKV_LAUNCH(c, batched_dma_fetch(c, st), "batched DMA fetch");
+    return LOUISKV_OK;
+  }
   LKV_LAUNCH(c, launch_select_gather(a, st), "select+gather");
   return LOUISKV_OK;
 }
@@ -838,8 +928,10 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
     }
     if (e != cudaErrorNotSupported) return cuda_fail(c, e, "full-cache step (tensor cores)");
   }
-  if (is_full(c, layer) || std::min(c->Umax, c->Bud) > LAYER_REP_SEL || c->Hq > 64) {
-    // full-cache layer (SIMT attention), or a budget / head count beyond the single launch
+  if (is_full(c, layer) || std::min(c->Umax, c->Bud) > LAYER_REP_SEL || c->Hq > 64 ||
+      c->cfg.fetch_mode == LOUISKV_FETCH_BATCHED_DMA) {
+    // full-cache layer (SIMT attention), a budget / head count beyond the single launch, or the
+    // host-issued batched DMA fetch (the selection must reach the host between select and attention)
     louiskv_status s = louiskv_should_retrieve(c, layer, q_all, stride_q, d_flag_out, d_r_out, stream);
     if (s == LOUISKV_OK) s = louiskv_retrieve(c, layer, q_own, stride_q, stream);
     if (s == LOUISKV_OK) s = louiskv_append_attn(c, layer, k_t, v_t, stride_kv, q_own, stride_q, out, out_f32, stream);

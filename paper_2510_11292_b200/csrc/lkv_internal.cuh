@@ -51,6 +51,13 @@ struct RowSrc {
   const uint4* k;
   const uint4* v;
 };
+// One copy of the BATCHED_DMA fetch (louiskv.h LOUISKV_FETCH_BATCHED_DMA): a contiguous span of K or
+// V rows of one selected unit, from the host pool (new unit) or the current working set (kept unit)
+// into the next working set. Written by select_kernel into mapped pinned host memory, read by the
+// host, which hands the list to cudaMemcpyBatchAsync.
+struct DmaSpan {
+  uint64_t src, dst, bytes;
+};
 
 struct StatsDev {
   unsigned long long retrievals, units_scored, units_selected, units_reused, units_fetched, bytes_h2d,
@@ -90,6 +97,9 @@ struct RetrieveArgs {
   float* scratch_e;          // [batch*hn][g][Umax]
   uint8_t* scratch_sort;     // [batch*hn][Umax * 14] sort buffers when n exceeds the smem capacity
   RowSrc* rows;              // [batch*hn][B]
+  DmaSpan* dma_spans;        // BATCHED_DMA: [batch*hn][dma_cap] spans (device-mapped host), else null
+  int32_t* dma_n;            // BATCHED_DMA: [batch*hn] span counts (device-mapped host)
+  int dma_cap;               // spans per instance (2 per selected unit, <= 2*B)
   StatsDev* stats;
   float r3c[7];              // recipe R3 Taylor coefficients fl32(ln2^i / i!) (r3_coefs)
   float inv_sqrt_d;          // recipe R2 scale fl32(1 / fl64(sqrt(d)))

@@ -78,6 +78,9 @@ def test_invalid_config_rejected_synchronously(lkv):
     bad.num_q_heads = 128  # both trigger paths hold at most 64 query heads
     bad.num_kv_heads = 16
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    bad.num_q_heads, bad.num_kv_heads = 4, 1
+    bad.fetch_mode = 2  # only ZERO_COPY and BATCHED_DMA exist
+    assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     assert L.louiskv_state_restore(None, None) == lkv.ERR_INVALID_ARG
     assert L.louiskv_cluster_prompt(None, 0, None, None, 0, 0, 0, 1, 1, None) == lkv.ERR_INVALID_ARG
 

@@ -38,7 +38,7 @@ def small_cfg(**kw):
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
                 check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False,
-                attn_impl=0, trigger_stride=0):
+                attn_impl=0, trigger_stride=0, fetch_mode=0):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
     fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
     "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
@@ -48,7 +48,8 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     g = cfg.group
     ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
                                       boundary_mode=boundary_mode, max_open_segment=max_open or 0,
-                                      attn_impl=attn_impl, trigger_stride=trigger_stride))
+                                      attn_impl=attn_impl, trigger_stride=trigger_stride,
+                                      fetch_mode=fetch_mode))
     ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
                        kv_head_begin=h0, kv_head_count=hn, trigger_stride=trigger_stride)
     L, b = cfg.num_layers, cfg.batch
@@ -702,3 +703,44 @@ def test_episode_g1_with_full_cache_layer():
     inp = make_inputs(cfg, 16, 15)
     for fused in (False, "layer"):
         run_episode(cfg, inp, 16, lambda l, Kn: planted_assign(cfg, inp.labels[l]), fused=fused)
+
+
+@pytest.mark.parametrize("fused", [False, "layer"])
+def test_episode_batched_dma_fetch(fused):
+    """fetch_mode BATCHED_DMA (§4.3, the DMA-engine analogue of the paper's DGL row transfer):
+    the selection's K/V spans go through one cudaMemcpyBatchAsync per layer instead of the zero-copy
+    loads. Same oracle, every step: flags, r_t bits, selections, working-set bits, unit tables, stats
+    (bytes_h2d counted from the spans) and attention. decode_layer takes the per-call sequence here."""
+    lkv = _lkv()
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, 21)
+    _, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused,
+                                 fetch_mode=lkv.FETCH_BATCHED_DMA)
+    assert n_flags > 5 and st["units_reused"] > 0 and st["units_fetched"] > 0
+
+
+def test_batched_dma_larger_budget_and_default_stream():
+    """BATCHED_DMA on the C4 parameters (B=1024 -> up to 2048 spans per instance, batch 3) with the
+    calls on the legacy default stream (the batch API rejects it: the library's copy stream is used,
+    ordered by an event), and retrieve inside a CUDA-graph capture is refused with STATE."""
+    lkv = _lkv()
+    cfg = C4.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, batch=3,
+                     prompt_len=4096, decode_steps=30)
+    inp = make_inputs(cfg, 30, 22)
+    _, n_flags, st = run_episode(cfg, inp, 30, lambda l, Kn: planted_assign(cfg, inp.labels[l]),
+                                 fetch_mode=lkv.FETCH_BATCHED_DMA)
+    assert st["bytes_h2d"] > 0
+    ctx = lkv.Context(lkv.make_config(cfg, fetch_mode=lkv.FETCH_BATCHED_DMA))
+    for l in range(cfg.num_layers):
+        ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+    ctx.prompt_fence()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    flag = torch.zeros(cfg.batch, dtype=torch.uint8, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(lkv.LouisKVError) as ei:
+        with torch.cuda.graph(g, stream=s):
+            ctx.should_retrieve(1, inp.q[0, 1], flag, stream=s)
+            ctx.retrieve(1, inp.q[0, 1][:, :cfg.group * cfg.num_kv_heads], stream=s)
+    assert ei.value.status == lkv.ERR_STATE
+    ctx.close()

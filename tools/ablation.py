@@ -20,6 +20,10 @@ Qwen3-8B 32K+16K), decode steps graph-replayed with device-residen
 2. tau sweep on a graded-drift query generator (synth drift > 0: per-segment random-walk queries, so
    r_t spreads and the retrieval frequency traces a curve): tau in {0.3 .. 0.95}.
 3. Fixed-stride retrieval every 5 / 16 steps and 16-token pages at tau = 0.7.
+4. Gather variant (§4.3: the paper moves selected rows with DGL's row transfer): the default
+   zero-copy gather vs fetch_mode BATCHED_DMA (one cudaMemcpyBatchAsync per layer, host-issued after
+   a stream sync), both through the four-call sequence launched eagerly (BATCHED_DMA cannot be
+   graph-captured), on the C2 headline shape (--only fetch).
 
 usage: python tools/ablation.py [--steps 64] > profiles/r02_ablation.json
 """
@@ -34,7 +38,7 @@ import torch
 
 import paper_2510_11292_b200 as lkv
 import synth
-from synth.configs import C4
+from synth.configs import C2, C4
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=64)
@@ -47,14 +51,16 @@ BASE = BASE.replace(k_planted=max(BASE.n_clusters // 4, 16))
 dev = torch.device("cuda", 0)
 
 
-def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans"):
-    """One variant: prefill every layer, warm up, time args.steps graph-replayed decode steps."""
+def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetch=0, graph=True):
+    """One variant: prefill every layer, warm up, time args.steps decode steps (graph-replayed, or
+    issued eagerly with graph=False)."""
     L, full, b = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch
     g = cfg.group
     run_cfg = cfg.replace(num_kv_heads=cfg.num_q_heads, k_planted=cfg.k_planted) if per_head else cfg
     T = 2 + 8 + args.steps
     ctx = lkv.Context(lkv.make_config(run_cfg, max_output_len=T + 1, trigger_stride=stride,
-                                      prompt_units=lkv.UNITS_PAGES if units == "pages" else lkv.UNITS_KMEANS))
+                                      prompt_units=lkv.UNITS_PAGES if units == "pages" else lkv.UNITS_KMEANS,
+                                      fetch_mode=fetch))
     plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
     for l in range(L):
         K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
@@ -84,8 +90,11 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans"):
     torch.cuda.synchronize()
     s = torch.cuda.Stream()
     gr = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gr, stream=s):
-        issue()
+    if graph:
+        with torch.cuda.graph(gr, stream=s):
+            issue()
+    else:
+        gr.replay = issue
     i = 1
     for _ in range(8):
         q_in.copy_(q[i]); k_in.copy_(kk[i]); v_in.copy_(vv[i]); gr.replay(); i += 1
@@ -102,7 +111,8 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans"):
     d = {k_: st1[k_] - st0[k_] for k_ in st1}
     nrl = (L - len(full)) * b
     row = {"variant": name, "tau": cfg.tau, "drift": cfg.drift, "per_head": per_head, "fused": fused,
-           "trigger_stride": stride, "units": units, "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
+           "trigger_stride": stride, "units": units, "fetch": ["zero_copy", "batched_dma"][fetch],
+           "graph": graph, "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
            "retrievals_per_layer_step": d["retrievals"] / (args.steps * nrl),
            "h2d_MB_per_step": d["bytes_h2d"] / args.steps / 1e6,
            "reuse_frac": d["units_reused"] / max(d["units_selected"], 1)}
@@ -132,6 +142,14 @@ if args.only in ("", "policies"):
     rows["policies"].append(run("fixed stride 5", BASE, stride=5))
     rows["policies"].append(run("fixed stride 16", BASE, stride=16))
     rows["policies"].append(run("pages of 16, tau=0.7", BASE, units="pages"))
+if args.only == "fetch":
+    C2T = C2.replace(k_planted=max(C2.n_clusters // 4, 16))
+    rows["fetch"] = [run("C2 zero-copy gather, four calls, eager", C2T, fused=False, graph=False),
+                     run("C2 batched DMA gather, four calls, eager", C2T, fused=False, graph=False,
+                         fetch=lkv.FETCH_BATCHED_DMA),
+                     run("C2 zero-copy gather, single launch, graph (the bench's mode)", C2T)]
+    for r in rows["fetch"]:
+        r["h2d_GBps_over_step"] = r["h2d_MB_per_step"] / r["ms_per_step"]
 print(json.dumps({"workload": f"Qwen3-8B LILO shape, {args.prompt}-token prompt, batch {args.batch}, "
                               f"S=64 W=256 B=1024 c=16, {args.steps} timed decode steps (synthetic, seed 0)",
                   "paper": "P:189 (SR ~2.6x, GS +13.1%, CK +15.7% on A6000, Qwen3-8B 32K+16K), P:465 (tau)",
