@@ -57,10 +57,11 @@ enum { LOUISKV_BOUNDARY_PER_LAYER = 0, LOUISKV_BOUNDARY_SHARED = 1 };
  * ZERO_COPY   — the select kernel's own threads read the pinned pool through its device mapping with
  *               16-B vector loads (no host involvement; graph-capturable; the default);
  * BATCHED_DMA — select writes per-unit copy spans (K rows, V rows) into mapped pinned memory; the
- *               host waits for them (louiskv_retrieve synchronises its stream) and issues ONE
- *               cudaMemcpyBatchAsync per layer (host pool -> working set for new units, device ->
- *               device for kept units) on the copy engines. Not graph-capturable (retrieve returns
- *               STATE inside a capture); louiskv_decode_layer then issues the per-call sequence. */
+ *               host waits for them (louiskv_retrieve synchronises its stream), merges spans that are
+ *               contiguous at both ends and enqueues one cudaMemcpyAsync per span on the copy engines
+ *               (host pool -> working set for new units, device -> device for kept units). Not
+ *               graph-capturable (retrieve returns STATE inside a capture); louiskv_decode_layer then
+ *               issues the per-call sequence. */
 enum { LOUISKV_FETCH_ZERO_COPY = 0, LOUISKV_FETCH_BATCHED_DMA = 1 };
 enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
 /* prompt units: semantic k-means clusters (the method) or contiguous pages (the page units of

@@ -56,17 +56,12 @@ struct louiskv_ctx {
   uint8_t* d_ssort = nullptr;
   RowSrc* d_rows = nullptr;
   GatherJob* d_jobs = nullptr;  // [L][Bmax*hn]
-  // BATCHED_DMA fetch: span lists written by select into mapped pinned memory, a copy stream for
-  // callers on the legacy default stream (cudaMemcpyBatchAsync rejects it), host-side batch arrays
+  // BATCHED_DMA fetch: span lists written by select into mapped pinned memory
   DmaSpan* h_spans = nullptr;
   int32_t* h_span_n = nullptr;
   DmaSpan* d_spans = nullptr;
   int32_t* d_span_n = nullptr;
   int dma_cap = 0;
-  cudaStream_t dma_stream = nullptr;
-  cudaEvent_t ev_dma = nullptr;
-  std::vector<void*> dma_dst, dma_src;
-  std::vector<size_t> dma_size;
   float* d_part = nullptr;
   int* d_counters = nullptr;
   int max_splits = 64;
@@ -327,16 +322,23 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
 }
 
 // BATCHED_DMA fetch (§4.3: selected rows moved by the DMA engines, the analogue of the paper's
-// DGL row transfer): wait for select's span lists (mapped pinned memory), then ONE
-// cudaMemcpyBatchAsync of every span of every flagged instance of the layer — new units host pool ->
-// next working set over the host link, kept units current -> next working set on the device. The
-// copies are mutually independent (disjoint destinations; sources are the pool and the other buffer).
+// DGL row transfer): wait for select's span lists (mapped pinned memory), merge spans that are
+// contiguous in both source and destination (runs of kept units; a new unit's K and V spans are
+// adjacent in the pool but not in the working set), then one stream-ordered cudaMemcpyAsync per merged
+// span — new units host pool -> next working set over the host link, kept units current -> next
+// working set on the device. The copies are mutually independent (disjoint destinations).
 cudaError_t batched_dma_fetch(louiskv_ctx* c, cudaStream_t st) {
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  c->dma_dst.clear();
-  c->dma_src.clear();
-  c->dma_size.clear();
+  const uint64_t dp = reinterpret_cast<uint64_t>(c->d_pool), hp = reinterpret_cast<uint64_t>(c->h_pool);
+  uint64_t src0 = 0, dst0 = 0, len = 0;
+  auto flush = [&]() -> cudaError_t {
+    if (!len) return cudaSuccess;
+    const cudaError_t r = cudaMemcpyAsync(reinterpret_cast<void*>(dst0), reinterpret_cast<const void*>(src0),
+                                          (size_t)len, cudaMemcpyDefault, st);
+    len = 0;
+    return r;
+  };
   const int ni = c->batch * c->hn;
   for (int li = 0; li < ni; ++li) {
     const int n = c->h_span_n[li];
@@ -345,29 +347,18 @@ cudaError_t batched_dma_fetch(louiskv_ctx* c, cudaStream_t st) {
     for (int i = 0; i < n; ++i) {
       uint64_t src = sp[i].src;
       // host-pool sources: device-mapped address -> the pool's host address
-      const uint64_t dp = reinterpret_cast<uint64_t>(c->d_pool);
-      if (c->d_pool && src >= dp && src < dp + c->host_bytes)
-        src = reinterpret_cast<uint64_t>(c->h_pool) + (src - dp);
-      c->dma_src.push_back(reinterpret_cast<void*>(src));
-      c->dma_dst.push_back(reinterpret_cast<void*>(sp[i].dst));
-      c->dma_size.push_back((size_t)sp[i].bytes);
+      if (c->d_pool && src >= dp && src < dp + c->host_bytes) src = hp + (src - dp);
+      if (len && src == src0 + len && sp[i].dst == dst0 + len) {
+        len += sp[i].bytes;
+        continue;
+      }
+      if ((e = flush()) != cudaSuccess) return e;
+      src0 = src;
+      dst0 = sp[i].dst;
+      len = sp[i].bytes;
     }
   }
-  if (c->dma_size.empty()) return cudaSuccess;
-  const bool legacy = st == nullptr || st == cudaStreamLegacy;
-  cudaStream_t cs = legacy ? c->dma_stream : st;  // (the batch API rejects the legacy default stream)
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t idx0 = 0, fail_idx = 0;
-  e = cudaMemcpyBatchAsync(c->dma_dst.data(), c->dma_src.data(), c->dma_size.data(), c->dma_size.size(), &attr,
-                           &idx0, 1, &fail_idx, cs);
-  if (e != cudaSuccess) return e;
-  if (legacy) {
-    if ((e = cudaEventRecord(c->ev_dma, cs)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(st, c->ev_dma, 0)) != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  return flush();
 }
 
 }  // namespace
@@ -387,8 +378,6 @@ void louiskv_destroy(louiskv_ctx* ctx) {
   for (cudaEvent_t e : {ctx->ev_free[0], ctx->ev_free[1], ctx->ev_staged})
     if (e) cudaEventDestroy(e);
   if (ctx->off_stream) cudaStreamDestroy(ctx->off_stream);
-  if (ctx->dma_stream) cudaStreamDestroy(ctx->dma_stream);
-  if (ctx->ev_dma) cudaEventDestroy(ctx->ev_dma);
   if (ctx->h_spans) cudaFreeHost(ctx->h_spans);
   if (ctx->h_span_n) cudaFreeHost(ctx->h_span_n);
   for (cudaEvent_t e : ctx->prec.pool)
@@ -542,11 +531,6 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
          cudaHostGetDevicePointer(&dn, hn_, 0) == cudaSuccess;
     c->d_spans = reinterpret_cast<DmaSpan*>(ds);
     c->d_span_n = reinterpret_cast<int32_t*>(dn);
-    ok = ok && cudaStreamCreateWithFlags(&c->dma_stream, cudaStreamNonBlocking) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&c->ev_dma, cudaEventDisableTiming) == cudaSuccess;
-    c->dma_dst.reserve((size_t)nl * c->dma_cap);
-    c->dma_src.reserve((size_t)nl * c->dma_cap);
-    c->dma_size.reserve((size_t)nl * c->dma_cap);
     if (!ok) cudaGetLastError();
   }
   if (!ok) {

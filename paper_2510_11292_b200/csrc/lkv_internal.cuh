@@ -54,7 +54,7 @@ struct RowSrc {
 // One copy of the BATCHED_DMA fetch (louiskv.h LOUISKV_FETCH_BATCHED_DMA): a contiguous span of K or
 // V rows of one selected unit, from the host pool (new unit) or the current working set (kept unit)
 // into the next working set. Written by select_kernel into mapped pinned host memory, read by the
-// host, which hands the list to cudaMemcpyBatchAsync.
+// host, which issues the copies (contiguous spans merged) on the copy engines.
 struct DmaSpan {
   uint64_t src, dst, bytes;
 };

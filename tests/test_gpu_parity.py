@@ -708,8 +708,8 @@ def test_episode_g1_with_full_cache_layer():
 @pytest.mark.parametrize("fused", [False, "layer"])
 def test_episode_batched_dma_fetch(fused):
     """fetch_mode BATCHED_DMA (§4.3, the DMA-engine analogue of the paper's DGL row transfer):
-    the selection's K/V spans go through one cudaMemcpyBatchAsync per layer instead of the zero-copy
-    loads. Same oracle, every step: flags, r_t bits, selections, working-set bits, unit tables, stats
+    the selection's K/V spans go through host-issued copy-engine copies (one per merged span) instead
+    of the zero-copy loads. Same oracle, every step: flags, r_t bits, selections, working-set bits, unit tables, stats
     (bytes_h2d counted from the spans) and attention. decode_layer takes the per-call sequence here."""
     lkv = _lkv()
     cfg = small_cfg()
@@ -720,9 +720,8 @@ def test_episode_batched_dma_fetch(fused):
 
 
 def test_batched_dma_larger_budget_and_default_stream():
-    """BATCHED_DMA on the C4 parameters (B=1024 -> up to 2048 spans per instance, batch 3) with the
-    calls on the legacy default stream (the batch API rejects it: the library's copy stream is used,
-    ordered by an event), and retrieve inside a CUDA-graph capture is refused with STATE."""
+    """BATCHED_DMA on the C4 parameters (B=1024 -> up to 2048 spans per instance, batch 3) on the
+    legacy default stream, and retrieve inside a CUDA-graph capture is refused with STATE."""
     lkv = _lkv()
     cfg = C4.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, batch=3,
                      prompt_len=4096, decode_steps=30)

@@ -21,8 +21,8 @@ Qwen3-8B 32K+16K), decode steps graph-replayed with device-residen
    r_t spreads and the retrieval frequency traces a curve): tau in {0.3 .. 0.95}.
 3. Fixed-stride retrieval every 5 / 16 steps and 16-token pages at tau = 0.7.
 4. Gather variant (§4.3: the paper moves selected rows with DGL's row transfer): the default
-   zero-copy gather vs fetch_mode BATCHED_DMA (one cudaMemcpyBatchAsync per layer, host-issued after
-   a stream sync), both through the four-call sequence launched eagerly (BATCHED_DMA cannot be
+   zero-copy gather vs fetch_mode BATCHED_DMA (copy-engine copies, one per merged span, host-issued
+   after a stream sync), both through the four-call sequence launched eagerly (BATCHED_DMA cannot be
    graph-captured), on the C2 headline shape (--only fetch).
 
 usage: python tools/ablation.py [--steps 64] > profiles/r02_ablation.json
