@@ -936,6 +936,11 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
   if (rank == CL - 1 && tid < 32)
     nv = reinterpret_cast<const uint4*>((tid < 16 ? A.at.app.k_t : A.at.app.v_t) + (int64_t)b * A.at.app.stride_b +
                                         (int64_t)h * D)[tid & 15];
+  // store_cache's ring write of the new token, now (off the step's tail): its slot (decode index
+  // dec0 mod ring_cap) is in no attended window this step — the window's rows occupy distinct slots
+  // (at most ring_cap - 1 of them) and its own row is supplied from registers
+  if (rank == CL - 1 && tid < 32)
+    reinterpret_cast<uint4*>((tid < 16 ? ringK : ringV) + (int64_t)(dec0 % cap) * D)[tid & 15] = nv;
   if (act) {
     c0 = qc4[hh * 16 + l8];
     c1 = qc4[hh * 16 + l8 + 8];
@@ -1174,7 +1179,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
     }
   }
   // store_cache side effects (seal / append / evict) by the last rank; commits the step
-  if (rank == CL - 1) append_one(app, li, flag, &s_S);
+  if (rank == CL - 1) append_one(app, li, flag, &s_S, /*row_written=*/true);
   prof_stamp(prof, 14);
 }
 

@@ -38,8 +38,10 @@ __device__ __forceinline__ void gather_rows(const AppendArgs& a, int li, const G
 // completed-step count, which this call commits (+1); leaves the post-append state in global memory.
 // pre: optional copy of the instance state already in shared memory (else loaded from global).
 // The working-set fields (ws_cur, ws_rows) belong to the retrieval and are not written here.
+// row_written: the caller already stored (k_t, v_t) into the ring slot of this token (decode index
+// = pre->step) — the layer kernel does so from registers right after its inputs arrive.
 __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, const int flag,
-                                           const InstState* pre = nullptr) {
+                                           const InstState* pre = nullptr, const bool row_written = false) {
   const int b = li / a.hn;
   const int tid = threadIdx.x;
   InstState* S = a.inst + li;
@@ -68,7 +70,8 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, co
   __syncthreads();
   // append the token's K and V rows
   const int slot = s_dec % cap;
-  if (tid < 16) {
+  if (row_written) {
+  } else if (tid < 16) {
     const uint4* src = reinterpret_cast<const uint4*>(a.k_t + (int64_t)b * a.stride_b + (int64_t)(li % a.hn) * D);
     reinterpret_cast<uint4*>(ringK + (int64_t)slot * D)[tid] = src[tid];
   } else if (tid < 32) {
