@@ -104,6 +104,15 @@ typedef struct {
                                 avg_cluster_size tokens (the last one shorter), centroid = mean of the
                                 page's keys (fp32), no Lloyd iterations; everything downstream (offload,
                                 scoring, selection, gather) is unchanged. Other values: INVALID_ARG. */
+  int32_t index_offload;     /* 0 (default): the unit index (fp32 centroids + their bf16 scoring copy,
+                                [units][d] per instance) in device memory. 1: the index in pinned,
+                                device-mapped host memory — the paper's future work ("memory
+                                consumption could be further reduced by offloading KV cache indices to
+                                CPU DRAM"): scoring reads the centroid rows over the host link, segment
+                                evictions write them there, and cluster_prompt runs k-means on one
+                                layer's device scratch and copies that layer's centroids out. Results are
+                                bit-identical to 0; device memory drops by ~6*d bytes per unit-table
+                                row. Other values: INVALID_ARG. */
 } louiskv_config;
 
 typedef struct {
@@ -242,7 +251,8 @@ louiskv_status louiskv_get_working_set(louiskv_ctx* ctx, int32_t layer, int32_t 
 louiskv_status louiskv_get_stats(louiskv_ctx* ctx, louiskv_stats* out);
 /* Memory held by the context (the paper's memory comparison, Table 3 / P:404-425): device bytes
  * of every device allocation made at create (sinks, working sets, local buffers, centroids, unit
- * tables, full-cache layers, scratch) and the pinned host-pool bytes. Either pointer may be NULL.
+ * tables, full-cache layers, scratch) and the pinned host bytes (the KV pool, plus the unit index
+ * when index_offload = 1). Either pointer may be NULL.
  * No synchronisation. Errors: INVALID_ARG (null ctx). */
 louiskv_status louiskv_get_memory(const louiskv_ctx* ctx, uint64_t* device_bytes, uint64_t* host_pool_bytes);
 /* NUMA placement of the pinned host pool: on hosts with more than one NUMA node the pool is

@@ -53,7 +53,8 @@ class Config(ctypes.Structure):
                 ("kmeans_impl", ctypes.c_int32), ("full_cache_layers", ctypes.c_uint64),
                 ("trigger_ref", ctypes.c_int32), ("boundary_mode", ctypes.c_int32), ("shared_layer", ctypes.c_int32),
                 ("max_open_segment", ctypes.c_int32), ("fetch_mode", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("attn_impl", ctypes.c_int32), ("trigger_stride", ctypes.c_int32), ("prompt_units", ctypes.c_int32)]
+                ("attn_impl", ctypes.c_int32), ("trigger_stride", ctypes.c_int32), ("prompt_units", ctypes.c_int32),
+                ("index_offload", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -143,7 +144,7 @@ def _stream(stream) -> Optional[int]:
 def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigger_ref=TRIG_PREV_STEP,
                 boundary_mode=BOUNDARY_PER_LAYER, shared_layer=0, max_open_segment=0, kmeans_impl=KMEANS_TC,
                 device=0, max_output_len=None, attn_impl=0, trigger_stride=0, prompt_units=0,
-                fetch_mode=FETCH_ZERO_COPY) -> Config:
+                fetch_mode=FETCH_ZERO_COPY, index_offload=0) -> Config:
     """Build the C config from a synth.configs.Config-like object (plain numbers)."""
     mask = 0
     for l in cfg.full_cache_layers:
@@ -158,7 +159,7 @@ def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigge
                   kmeans_impl=kmeans_impl, full_cache_layers=mask, trigger_ref=trigger_ref,
                   boundary_mode=boundary_mode, shared_layer=shared_layer, max_open_segment=max_open_segment,
                   fetch_mode=fetch_mode, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride,
-                  prompt_units=prompt_units)
+                  prompt_units=prompt_units, index_offload=index_offload)
 
 
 class Context:

@@ -34,8 +34,13 @@ struct louiskv_ctx {
   int64_t ws_buf_stride = 0, ws_inst_stride = 0;
   bf16* d_ring = nullptr;
   int2* d_fifo = nullptr;
-  float* d_cent = nullptr;
+  float* d_cent = nullptr;   // unit index (centroids); index_offload: device-mapped host memory
   bf16* d_centb = nullptr;
+  float* h_cent = nullptr;   // index_offload: the pinned host arrays behind d_cent / d_centb
+  bf16* h_centb = nullptr;
+  float* d_km_cent = nullptr;  // index_offload: one layer's device k-means centroids, copied out after
+  bf16* d_km_centb = nullptr;
+  uint64_t index_host_bytes = 0;
   int32_t* d_usize = nullptr;
   int64_t* d_uoff = nullptr;
   int32_t* d_ufirst = nullptr;
@@ -379,6 +384,8 @@ void louiskv_destroy(louiskv_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->off_stream) cudaStreamDestroy(ctx->off_stream);
   if (ctx->h_spans) cudaFreeHost(ctx->h_spans);
+  if (ctx->h_cent) cudaFreeHost(ctx->h_cent);
+  if (ctx->h_centb) cudaFreeHost(ctx->h_centb);
   if (ctx->h_span_n) cudaFreeHost(ctx->h_span_n);
   for (cudaEvent_t e : ctx->prec.pool)
     if (e) cudaEventDestroy(e);
@@ -408,6 +415,7 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       k.avg_cluster_size < 1 || k.kmeans_iters < 0 || !(std::isfinite(k.tau)) || k.trigger_stride < 0 ||
       (k.prompt_units != LOUISKV_UNITS_KMEANS && k.prompt_units != LOUISKV_UNITS_PAGES) ||
       (k.fetch_mode != LOUISKV_FETCH_ZERO_COPY && k.fetch_mode != LOUISKV_FETCH_BATCHED_DMA) ||
+      (k.index_offload != 0 && k.index_offload != 1) ||
       (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
     return LOUISKV_ERR_INVALID_ARG;
   const int g = k.num_q_heads / k.num_kv_heads;
@@ -467,8 +475,30 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
   ok = ok && dalloc(c, &c->d_ws, (size_t)2 * c->ws_buf_stride);
   ok = ok && dalloc(c, &c->d_ring, (size_t)ni * 2 * c->ring_cap * D);
   ok = ok && dalloc(c, &c->d_fifo, (size_t)ni * c->ring_cap);
-  ok = ok && dalloc(c, &c->d_cent, (size_t)ni * c->Umax * D);
-  ok = ok && dalloc(c, &c->d_centb, (size_t)ni * c->Umax * D);
+  if (k.index_offload) {
+    // the unit index in pinned, device-mapped host memory (the paper's future work): scoring
+    // reads the centroid rows over the host link; k-means runs on one layer's device scratch
+    const size_t ne = std::max<size_t>((size_t)ni * c->Umax * D, 1);
+    void *hc = nullptr, *hb = nullptr, *dc = nullptr, *db = nullptr;
+    ok = ok && cudaHostAlloc(&hc, ne * sizeof(float), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess &&
+         cudaHostAlloc(&hb, ne * sizeof(bf16), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess;
+    c->h_cent = reinterpret_cast<float*>(hc);
+    c->h_centb = reinterpret_cast<bf16*>(hb);
+    if (ok) {
+      memset(hc, 0, ne * sizeof(float));
+      memset(hb, 0, ne * sizeof(bf16));
+      c->index_host_bytes = ne * (sizeof(float) + sizeof(bf16));
+    }
+    ok = ok && cudaHostGetDevicePointer(&dc, hc, 0) == cudaSuccess && cudaHostGetDevicePointer(&db, hb, 0) == cudaSuccess;
+    c->d_cent = reinterpret_cast<float*>(dc);
+    c->d_centb = reinterpret_cast<bf16*>(db);
+    if (!ok) cudaGetLastError();
+    ok = ok && dalloc(c, &c->d_km_cent, (size_t)nl * c->Umax * D);
+    ok = ok && dalloc(c, &c->d_km_centb, (size_t)nl * c->Umax * D);
+  } else {
+    ok = ok && dalloc(c, &c->d_cent, (size_t)ni * c->Umax * D);
+    ok = ok && dalloc(c, &c->d_centb, (size_t)ni * c->Umax * D);
+  }
   ok = ok && dalloc(c, &c->d_usize, (size_t)ni * c->Umax);
   ok = ok && dalloc(c, &c->d_uoff, (size_t)ni * c->Umax);
   ok = ok && dalloc(c, &c->d_ufirst, (size_t)ni * c->Umax);
@@ -677,8 +707,9 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.iters = c->iters;
   a.impl = c->cfg.kmeans_impl;
   a.page = c->cfg.prompt_units == LOUISKV_UNITS_PAGES ? c->cfg.avg_cluster_size : 0;
-  a.cent = c->d_cent + ib * c->Umax * D;
-  a.centb = c->d_centb + ib * c->Umax * D;
+  const bool idx_off = c->cfg.index_offload != 0;
+  a.cent = idx_off ? c->d_km_cent : c->d_cent + ib * c->Umax * D;
+  a.centb = idx_off ? c->d_km_centb : c->d_centb + ib * c->Umax * D;
   a.Umax = c->Umax;
   a.usize = c->d_usize + ib * c->Umax;
   a.uoff = c->d_uoff + ib * c->Umax;
@@ -733,6 +764,13 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
     c->prec.calls += 1;
   }
   cudaError_t e = run_kmeans_prompt(a, st, &c->km_tc_iters, &c->km_simt_iters);
+  if (e == cudaSuccess && idx_off) {
+    // the layer's centroids (fp32 master + bf16 scoring copy) out to the host-resident index
+    const size_t ne = (size_t)batch * c->hn * c->Umax * D;
+    e = cudaMemcpyAsync(c->h_cent + ib * c->Umax * D, c->d_km_cent, ne * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->h_centb + ib * c->Umax * D, c->d_km_centb, ne * sizeof(bf16), cudaMemcpyDeviceToHost, st);
+  }
   if (e == cudaSuccess) e = offload_prompt(c, layer, a, st);
   if (h_assign) {
     cudaStreamSynchronize(st);
@@ -1002,7 +1040,7 @@ louiskv_status louiskv_get_units(louiskv_ctx* c, int32_t layer, int32_t b, int32
   InstState is;
   cudaMemcpy(&is, c->d_inst + gi, sizeof(is), cudaMemcpyDeviceToHost);
   const int n = std::min(is.n_units, std::max(cap, 0));
-  if (cf && n) cudaMemcpy(cf, c->d_cent + gi * c->Umax * D, sizeof(float) * n * D, cudaMemcpyDeviceToHost);
+  if (cf && n) cudaMemcpy(cf, c->d_cent + gi * c->Umax * D, sizeof(float) * n * D, cudaMemcpyDefault);
   if (sizes && n) cudaMemcpy(sizes, c->d_usize + gi * c->Umax, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
   if (first_pos && n) cudaMemcpy(first_pos, c->d_ufirst + gi * c->Umax, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
   if (n_units) *n_units = is.n_units;
@@ -1161,7 +1199,7 @@ louiskv_status louiskv_get_pool_numa_node(const louiskv_ctx* c, int32_t* node) {
 louiskv_status louiskv_get_memory(const louiskv_ctx* c, uint64_t* device_bytes, uint64_t* host_pool_bytes) {
   if (!c) return LOUISKV_ERR_INVALID_ARG;
   if (device_bytes) *device_bytes = c->dev_bytes;
-  if (host_pool_bytes) *host_pool_bytes = c->host_bytes;
+  if (host_pool_bytes) *host_pool_bytes = c->host_bytes + c->index_host_bytes;
   return LOUISKV_OK;
 }
 

@@ -46,10 +46,11 @@ def test_ctypes_struct_layout_matches_c(lkv):
 #include <stddef.h>
 #include "louiskv.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
          offsetof(louiskv_config, full_cache_layers), offsetof(louiskv_config, device),
          sizeof(louiskv_stats), offsetof(louiskv_stats, segments_evicted), sizeof(louiskv_prefill_times),
-         offsetof(louiskv_prefill_times, assign_flops), offsetof(louiskv_prefill_times, calls));
+         offsetof(louiskv_prefill_times, assign_flops), offsetof(louiskv_prefill_times, calls),
+         offsetof(louiskv_config, fetch_mode), offsetof(louiskv_config, index_offload));
   return 0;
 }
 '''
@@ -62,7 +63,7 @@ int main(void) {
     C, S, T = lkv.Config, lkv.Stats, lkv.PrefillTimes
     assert vals == [ctypes.sizeof(C), C.tau.offset, C.full_cache_layers.offset, C.device.offset,
                     ctypes.sizeof(S), S.segments_evicted.offset, ctypes.sizeof(T), T.assign_flops.offset,
-                    T.calls.offset]
+                    T.calls.offset, C.fetch_mode.offset, C.index_offload.offset]
 
 
 def test_invalid_config_rejected_synchronously(lkv):
@@ -80,6 +81,9 @@ def test_invalid_config_rejected_synchronously(lkv):
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     bad.num_q_heads, bad.num_kv_heads = 4, 1
     bad.fetch_mode = 2  # only ZERO_COPY and BATCHED_DMA exist
+    assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    bad.fetch_mode = 0
+    bad.index_offload = 2  # 0 (device index) or 1 (host index)
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     assert L.louiskv_state_restore(None, None) == lkv.ERR_INVALID_ARG
     assert L.louiskv_cluster_prompt(None, 0, None, None, 0, 0, 0, 1, 1, None) == lkv.ERR_INVALID_ARG

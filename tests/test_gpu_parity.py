@@ -38,7 +38,7 @@ def small_cfg(**kw):
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
                 check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False,
-                attn_impl=0, trigger_stride=0, fetch_mode=0):
+                attn_impl=0, trigger_stride=0, fetch_mode=0, index_offload=0):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
     fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
     "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
@@ -49,7 +49,7 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
                                       boundary_mode=boundary_mode, max_open_segment=max_open or 0,
                                       attn_impl=attn_impl, trigger_stride=trigger_stride,
-                                      fetch_mode=fetch_mode))
+                                      fetch_mode=fetch_mode, index_offload=index_offload))
     ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
                        kv_head_begin=h0, kv_head_count=hn, trigger_stride=trigger_stride)
     L, b = cfg.num_layers, cfg.batch
@@ -743,3 +743,56 @@ def test_batched_dma_larger_budget_and_default_stream():
             ctx.retrieve(1, inp.q[0, 1][:, :cfg.group * cfg.num_kv_heads], stream=s)
     assert ei.value.status == lkv.ERR_STATE
     ctx.close()
+
+
+@pytest.mark.parametrize("fused", [False, "layer"])
+def test_episode_index_offload(fused):
+    """index_offload = 1 (the paper's future work: the unit index in host DRAM): scoring reads
+    the centroid rows from pinned host memory over the link, evicted segments write theirs there —
+    same oracle, same bit-exact decisions and unit tables, every step."""
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, 23)
+    _, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused,
+                                 index_offload=1)
+    assert n_flags > 5 and st["segments_evicted"] > 0 and st["units_fetched"] > 0
+
+
+def test_index_offload_gpu_kmeans_bit_identical_and_smaller():
+    """GPU k-means (tcgen05) with the index offloaded equals the device-index run bit for bit (units,
+    centroid bits, positions), a 12-step single-launch decode gives bit-identical outputs and flags,
+    and the device footprint drops by the index (6 d bytes per unit-table row, minus one layer of
+    k-means scratch) while the host bytes grow by as much."""
+    lkv = _lkv()
+    cfg = small_cfg(num_layers=3, batch=2, prompt_len=3000, decode_steps=12)
+    inp = make_inputs(cfg, 12, 24)
+    outs, mems = [], []
+    for off in (0, 1):
+        ctx = lkv.Context(lkv.make_config(cfg, index_offload=off))
+        for l in range(cfg.num_layers):
+            ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+        ctx.prompt_fence()
+        o = torch.zeros((cfg.num_layers, cfg.batch, cfg.num_q_heads, 128), dtype=torch.float32, device="cuda")
+        ob = torch.zeros_like(o, dtype=torch.bfloat16)
+        fl = torch.zeros((cfg.num_layers, cfg.batch), dtype=torch.uint8, device="cuda")
+        res = []
+        for t in range(12):
+            for l in range(cfg.num_layers):
+                ctx.decode_layer(l, inp.q[t, l], inp.k[t, l].contiguous(), inp.v[t, l].contiguous(), ob[l], o[l],
+                                 flag_out=fl[l])
+            torch.cuda.synchronize()
+            res.append((o.cpu().numpy().copy(), fl.cpu().numpy().copy()))
+        units = {(l, bb, hh): ctx.get_units(l, bb, hh) + (ctx.get_unit_positions(l, bb, hh),)
+                 for l in range(cfg.num_layers) if l not in cfg.full_cache_layers
+                 for bb in range(cfg.batch) for hh in range(cfg.num_kv_heads)}
+        outs.append((res, units, ctx.stats()))
+        mems.append(ctx.memory())
+        ctx.close()
+    (r0, u0, s0), (r1, u1, s1) = outs
+    for (a, fa), (b, fb) in zip(r0, r1):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)) and np.array_equal(fa, fb)
+    for key in u0:
+        for x, y in zip(u0[key], u1[key]):
+            assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8)), key
+    assert s0 == s1 and s0["retrievals"] > 0
+    assert mems[1]["device_bytes"] < mems[0]["device_bytes"]
+    assert mems[1]["host_pool_bytes"] > mems[0]["host_pool_bytes"]

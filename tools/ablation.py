@@ -24,6 +24,9 @@ Qwen3-8B 32K+16K), decode steps graph-replayed with device-residen
    zero-copy gather vs fetch_mode BATCHED_DMA (copy-engine copies, one per merged span, host-issued
    after a stream sync), both through the four-call sequence launched eagerly (BATCHED_DMA cannot be
    graph-captured), on the C2 headline shape (--only fetch).
+5. Index placement (the paper's future work: "offloading KV cache indices to CPU DRAM"): the
+   unit index (centroids) in device memory vs in pinned host memory read over the link at every
+   scoring, C2 and the C4 shape at 32K: step time and device bytes (--only index).
 
 usage: python tools/ablation.py [--steps 64] > profiles/r02_ablation.json
 """
@@ -51,7 +54,7 @@ BASE = BASE.replace(k_planted=max(BASE.n_clusters // 4, 16))
 dev = torch.device("cuda", 0)
 
 
-def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetch=0, graph=True):
+def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetch=0, graph=True, index_offload=0):
     """One variant: prefill every layer, warm up, time args.steps decode steps (graph-replayed, or
     issued eagerly with graph=False)."""
     L, full, b = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch
@@ -60,7 +63,7 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetc
     T = 2 + 8 + args.steps
     ctx = lkv.Context(lkv.make_config(run_cfg, max_output_len=T + 1, trigger_stride=stride,
                                       prompt_units=lkv.UNITS_PAGES if units == "pages" else lkv.UNITS_KMEANS,
-                                      fetch_mode=fetch))
+                                      fetch_mode=fetch, index_offload=index_offload))
     plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
     for l in range(L):
         K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
@@ -112,7 +115,7 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetc
     nrl = (L - len(full)) * b
     row = {"variant": name, "tau": cfg.tau, "drift": cfg.drift, "per_head": per_head, "fused": fused,
            "trigger_stride": stride, "units": units, "fetch": ["zero_copy", "batched_dma"][fetch],
-           "graph": graph, "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
+           "graph": graph, "index_offload": index_offload, "memory": ctx.memory(), "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
            "retrievals_per_layer_step": d["retrievals"] / (args.steps * nrl),
            "h2d_MB_per_step": d["bytes_h2d"] / args.steps / 1e6,
            "reuse_frac": d["units_reused"] / max(d["units_selected"], 1)}
@@ -150,6 +153,11 @@ if args.only == "fetch":
                      run("C2 zero-copy gather, single launch, graph (the bench's mode)", C2T)]
     for r in rows["fetch"]:
         r["h2d_GBps_over_step"] = r["h2d_MB_per_step"] / r["ms_per_step"]
+if args.only == "index":
+    C2T = C2.replace(k_planted=max(C2.n_clusters // 4, 16))
+    rows["index"] = [run("C2 index on the device", C2T), run("C2 index in host DRAM", C2T, index_offload=1),
+                     run("C4 shape 32K batch 2, index on the device", BASE),
+                     run("C4 shape 32K batch 2, index in host DRAM", BASE, index_offload=1)]
 print(json.dumps({"workload": f"Qwen3-8B LILO shape, {args.prompt}-token prompt, batch {args.batch}, "
                               f"S=64 W=256 B=1024 c=16, {args.steps} timed decode steps (synthetic, seed 0)",
                   "paper": "P:189 (SR ~2.6x, GS +13.1%, CK +15.7% on A6000, Qwen3-8B 32K+16K), P:465 (tau)",
