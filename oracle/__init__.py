@@ -11,6 +11,7 @@ Numerics live in ``louiskv_oracle.c`` (built to ``liblouiskv_oracle.so``);
 """
 from .core import (  # noqa: F401
     bf16_round,
+    e4m3_round,
     cosine_r1,
     trigger_r1,
     exp_r3,

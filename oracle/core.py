@@ -44,6 +44,8 @@ def lib():
         L.lko_trigger_r1.restype = ctypes.c_int
         L.lko_trigger_r1.argtypes = [_f32p, _f32p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+        L.lko_e4m3_round_n.restype = None
+        L.lko_e4m3_round_n.argtypes = [_f32p, _f32p, ctypes.c_longlong]
         L.lko_bf16_round_n.restype = None
         L.lko_bf16_round_n.argtypes = [_f32p, _f32p, ctypes.c_longlong]
         L.lko_exp_r3_n.restype = None
@@ -78,6 +80,14 @@ def bf16_round(x) -> np.ndarray:
     a = _f32(x)
     out = np.empty_like(a)
     lib().lko_bf16_round_n(a.reshape(-1), out.reshape(-1), a.size)
+    return out
+
+
+def e4m3_round(x) -> np.ndarray:
+    """E4M3 value (RNE, saturating at +-448) of every element, as fp32 (reading R-FP8)."""
+    a = _f32(x)
+    out = np.empty_like(a)
+    lib().lko_e4m3_round_n(a.reshape(-1), out.reshape(-1), a.size)
     return out
 
 

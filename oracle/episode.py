@@ -53,7 +53,8 @@ class _Inst:
 class OracleEpisode:
     def __init__(self, cfg, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, shared_layer=0,
                  max_open_segment: Optional[int] = None, kmeans_mode: int = 1,
-                 kv_head_begin: int = 0, kv_head_count: Optional[int] = None, trigger_stride: int = 0):
+                 kv_head_begin: int = 0, kv_head_count: Optional[int] = None, trigger_stride: int = 0,
+                 pool_fp8: bool = False):
         self.cfg = cfg
         # trigger_stride k >= 1: the fixed-stride retrieval of the paper's ablation — retrieve
         # at t = 1, 1 + k, 1 + 2k, ... instead of on r_t < tau; 0: the semantic boundary
@@ -80,7 +81,15 @@ class OracleEpisode:
         self.kmeans_J: Dict[tuple, np.ndarray] = {}
         self.stats = dict(retrievals=0, units_scored=0, units_selected=0, units_reused=0,
                           units_fetched=0, bytes_h2d=0, bytes_d2h=0, segments_evicted=0)
-        self.row_bytes = 2 * 2 * self.d  # K+V bf16 per token per head
+        # pool_fp8 (reading R-FP8, the FP8 host-pool variant of SURVEY §8(f) row 3): every K/V row that
+        # enters the CPU pool is stored as E4M3 (RNE, saturating), so a unit's rows — the ones
+        # retrieval brings back — are the E4M3 values; sinks and the local buffer stay bf16, centroids
+        # are computed from the bf16 keys
+        self.pool_fp8 = bool(pool_fp8)
+        self.row_bytes = 2 * (1 if self.pool_fp8 else 2) * self.d  # K+V per token per head in the pool
+
+    def _pool(self, x: np.ndarray) -> np.ndarray:
+        return core.e4m3_round(x) if self.pool_fp8 else x
 
     # --------------------------------------------------------------- prefill
     def cluster_prompt(self, layer: int, K: np.ndarray, V: np.ndarray, assign: Optional[np.ndarray] = None):
@@ -116,7 +125,7 @@ class OracleEpisode:
                     Cb = core.bf16_round(C)
                     for j in range(k):
                         mem = np.nonzero(a_i == j)[0]
-                        inst.units.append(Unit(j, mem + S, X[mem].copy(), V[bb, S + mem, hh].copy(),
+                        inst.units.append(Unit(j, mem + S, self._pool(X[mem]), self._pool(V[bb, S + mem, hh]),
                                                C[j].copy(), Cb[j].copy()))
                     self.stats["bytes_d2h"] += N * self.row_bytes
                 self.inst[key] = inst
@@ -204,7 +213,7 @@ class OracleEpisode:
                 while inst.sealed and (sum(s["pos"].size for s in inst.sealed) + len(inst.open_pos)) > self.W:
                     s = inst.sealed.pop(0)
                     uid = len(inst.units)
-                    inst.units.append(Unit(uid, s["pos"], s["K"], s["V"], s["centroid"],
+                    inst.units.append(Unit(uid, s["pos"], self._pool(s["K"]), self._pool(s["V"]), s["centroid"],
                                            core.bf16_round(s["centroid"])))
                     self.stats["bytes_d2h"] += s["pos"].size * self.row_bytes
                     self.stats["segments_evicted"] += 1

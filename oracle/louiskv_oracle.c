@@ -28,6 +28,8 @@
  *                                        planted recovery, sklearn Lloyd equality)
  *   lko_segment_centroid                pinned (S:152-154 closed form)
  *   lko_attention_f64                   pinned (S:402-414 closed forms, SDPA)
+ *   lko_e4m3_round                      pinned (every finite bf16 value vs torch's float8_e4m3fn
+ *                                        cast, hand-worked ties / subnormals / saturation)
  */
 #include <math.h>
 #include <stdint.h>
@@ -415,4 +417,38 @@ int lko_centroids_of(const float* X, const int* assign, int N, int d, int k, flo
   }
   free(sum); free(cnt);
   return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* FP8 (E4M3) host pool — SURVEY §8(f) row 3 ("FP8 KV in the pool halves the  */
+/* link bytes"); the paper keeps its pool in FP16 ("All KV cache is     */
+/* stored in FP16"), so this is a variant, reading R-FP8: a pool  */
+/* row holds e4m3(x) of every bf16 element x, round-to-nearest-even, values  */
+/* beyond the largest finite E4M3 magnitude (448) saturate to +-448.          */
+/* E4M3: 1 sign, 4 exponent bits (bias 7), 3 mantissa bits, no infinities;    */
+/* normal magnitudes 2^-6 .. 448, subnormals m * 2^-9 (m = 1..7).             */
+/* Written out from that definition: the quantum of |x| is 2^(e-3) for the    */
+/* binade [2^e, 2^(e+1)) with e >= -6, else the subnormal quantum 2^-9;       */
+/* x / quantum is exact in fp64, rint() rounds it half-to-even.               */
+/* ------------------------------------------------------------------------ */
+float lko_e4m3_round(float x) {
+  if (x != x) return x;
+  const double ax = fabs((double)x);
+  if (ax == 0.0) return x;
+  double y;
+  if (ax >= 448.0) {
+    y = 448.0;
+  } else {
+    int e;
+    (void)frexp(ax, &e); /* ax = f * 2^e, f in [0.5, 1): binade [2^(e-1), 2^e) */
+    int eb = e - 1;      /* ax in [2^eb, 2^(eb+1)) */
+    if (eb < -6) eb = -6; /* subnormal range shares the quantum of the first normal binade */
+    const double q = ldexp(1.0, eb - 3);
+    y = rint(ax / q) * q; /* (a tie at the top of a binade rounds up into the next: still exact) */
+    if (y > 448.0) y = 448.0;
+  }
+  return (float)(x < 0 ? -y : y);
+}
+void lko_e4m3_round_n(const float* x, float* y, long long n) {
+  for (long long i = 0; i < n; ++i) y[i] = lko_e4m3_round(x[i]);
 }
