@@ -69,6 +69,13 @@ enum { LOUISKV_KMEANS_TC = 0, LOUISKV_KMEANS_SIMT = 1 };
  * pages", page size 16 at P:143) */
 enum { LOUISKV_UNITS_KMEANS = 0, LOUISKV_UNITS_PAGES = 1 };
 enum { LOUISKV_ATTN_TC = 0, LOUISKV_ATTN_SIMT = 1 };
+/* element type of the KV rows in the pinned host pool (config pool_dtype). BF16: the rows as given
+ * (the paper's pool, "All KV cache is stored in FP16"). FP8_E4M3 (a
+ * variant the paper does not have): every row entering the pool (prompt offload, segment eviction)
+ * is stored as E4M3, round-to-nearest-even, saturating at +-448 — half the host-link bytes of every
+ * offload and gather; the gather converts back to bf16 (exactly) into the working set. Sinks, the
+ * local buffer, centroids and full-cache layers stay bf16 / fp32. Not combinable with BATCHED_DMA. */
+enum { LOUISKV_POOL_BF16 = 0, LOUISKV_POOL_FP8_E4M3 = 1 };
 
 typedef struct {
   int32_t num_layers, num_q_heads, num_kv_heads, head_dim; /* head_dim must be 128; num_q_heads <= 64;
@@ -113,6 +120,8 @@ typedef struct {
                                 layer's device scratch and copies that layer's centroids out. Results are
                                 bit-identical to 0; device memory drops by ~6*d bytes per unit-table
                                 row. Other values: INVALID_ARG. */
+  int32_t pool_dtype;        /* LOUISKV_POOL_BF16 (default) | LOUISKV_POOL_FP8_E4M3; other values, or FP8
+                                with fetch_mode BATCHED_DMA: INVALID_ARG */
 } louiskv_config;
 
 typedef struct {
@@ -126,6 +135,7 @@ typedef struct {
   uint64_t segments_evicted;
   uint64_t kmeans_tc_iters;   /* Lloyd assignment passes run on the tcgen05 kernel */
   uint64_t kmeans_simt_iters; /* ... on the SIMT kernel (impl SIMT, or TMA-incompatible strides) */
+  uint64_t dma_copies;        /* fetch_mode BATCHED_DMA: copy-engine copies issued by retrieve */
 } louiskv_stats;
 
 /* Allocates every device buffer and the pinned, device-mapped host pool.

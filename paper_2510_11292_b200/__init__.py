@@ -24,6 +24,7 @@ BOUNDARY_PER_LAYER, BOUNDARY_SHARED = 0, 1
 KMEANS_TC, KMEANS_SIMT = 0, 1
 UNITS_KMEANS, UNITS_PAGES = 0, 1
 FETCH_ZERO_COPY, FETCH_BATCHED_DMA = 0, 1
+POOL_BF16, POOL_FP8_E4M3 = 0, 1
 
 _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "STATE", 3: "CAPACITY", 4: "OOM_DEVICE", 5: "OOM_HOST", 6: "CUDA",
            7: "NOT_IMPLEMENTED"}
@@ -54,13 +55,13 @@ class Config(ctypes.Structure):
                 ("trigger_ref", ctypes.c_int32), ("boundary_mode", ctypes.c_int32), ("shared_layer", ctypes.c_int32),
                 ("max_open_segment", ctypes.c_int32), ("fetch_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("attn_impl", ctypes.c_int32), ("trigger_stride", ctypes.c_int32), ("prompt_units", ctypes.c_int32),
-                ("index_offload", ctypes.c_int32)]
+                ("index_offload", ctypes.c_int32), ("pool_dtype", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("retrievals", "units_scored", "units_selected", "units_reused",
                                                 "units_fetched", "bytes_h2d", "bytes_d2h", "segments_evicted",
-                                                "kmeans_tc_iters", "kmeans_simt_iters")]
+                                                "kmeans_tc_iters", "kmeans_simt_iters", "dma_copies")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -144,7 +145,7 @@ def _stream(stream) -> Optional[int]:
 def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigger_ref=TRIG_PREV_STEP,
                 boundary_mode=BOUNDARY_PER_LAYER, shared_layer=0, max_open_segment=0, kmeans_impl=KMEANS_TC,
                 device=0, max_output_len=None, attn_impl=0, trigger_stride=0, prompt_units=0,
-                fetch_mode=FETCH_ZERO_COPY, index_offload=0) -> Config:
+                fetch_mode=FETCH_ZERO_COPY, index_offload=0, pool_dtype=0) -> Config:
     """Build the C config from a synth.configs.Config-like object (plain numbers)."""
     mask = 0
     for l in cfg.full_cache_layers:
@@ -159,7 +160,7 @@ def make_config(cfg, kv_head_begin=0, kv_head_count=None, max_batch=None, trigge
                   kmeans_impl=kmeans_impl, full_cache_layers=mask, trigger_ref=trigger_ref,
                   boundary_mode=boundary_mode, shared_layer=shared_layer, max_open_segment=max_open_segment,
                   fetch_mode=fetch_mode, device=device, attn_impl=attn_impl, trigger_stride=trigger_stride,
-                  prompt_units=prompt_units, index_offload=index_offload)
+                  prompt_units=prompt_units, index_offload=index_offload, pool_dtype=pool_dtype)
 
 
 class Context:

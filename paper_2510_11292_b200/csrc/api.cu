@@ -67,6 +67,8 @@ struct louiskv_ctx {
   DmaSpan* d_spans = nullptr;
   int32_t* d_span_n = nullptr;
   int dma_cap = 0;
+  uint64_t dma_copies = 0;  // copies issued (louiskv_stats.dma_copies)
+  int prb = POOL_ROW_BYTES;  // host-pool bytes per token (K + V): 512 bf16, 256 E4M3
   float* d_part = nullptr;
   int* d_counters = nullptr;
   int max_splits = 64;
@@ -232,6 +234,7 @@ RetrieveArgs retrieve_args(louiskv_ctx* c, int layer, const void* q, int64_t str
   a.seloff = c->d_seloff + ib * c->Umax;
   a.pool = c->d_pool + ib * c->pool_inst_bytes;
   a.pool_inst_bytes = c->pool_inst_bytes;
+  a.pool_fp8 = c->cfg.pool_dtype == LOUISKV_POOL_FP8_E4M3;
   a.ws = c->d_ws;
   a.ws_buf_stride = c->ws_buf_stride;
   a.ws_inst_stride = c->ws_inst_stride;
@@ -272,6 +275,7 @@ AppendArgs append_args(louiskv_ctx* c, int layer, const void* k_t, const void* v
   a.pool_rows_cap = c->pool_rows_cap;
   a.pool = c->d_pool + ib * c->pool_inst_bytes;
   a.pool_inst_bytes = c->pool_inst_bytes;
+  a.pool_fp8 = c->cfg.pool_dtype == LOUISKV_POOL_FP8_E4M3;
   a.stats = c->d_stats;
   a.jobs = c->d_jobs + (size_t)layer * c->inst_per_layer;
   a.rows = c->d_rows;
@@ -358,6 +362,7 @@ cudaError_t batched_dma_fetch(louiskv_ctx* c, cudaStream_t st) {
         continue;
       }
       if ((e = flush()) != cudaSuccess) return e;
+      ++c->dma_copies;
       src0 = src;
       dst0 = sp[i].dst;
       len = sp[i].bytes;
@@ -416,6 +421,8 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
       (k.prompt_units != LOUISKV_UNITS_KMEANS && k.prompt_units != LOUISKV_UNITS_PAGES) ||
       (k.fetch_mode != LOUISKV_FETCH_ZERO_COPY && k.fetch_mode != LOUISKV_FETCH_BATCHED_DMA) ||
       (k.index_offload != 0 && k.index_offload != 1) ||
+      (k.pool_dtype != LOUISKV_POOL_BF16 && k.pool_dtype != LOUISKV_POOL_FP8_E4M3) ||
+      (k.pool_dtype == LOUISKV_POOL_FP8_E4M3 && k.fetch_mode == LOUISKV_FETCH_BATCHED_DMA) ||
       (k.boundary_mode == LOUISKV_BOUNDARY_SHARED && (k.shared_layer < 0 || k.shared_layer >= k.num_layers)))
     return LOUISKV_ERR_INVALID_ARG;
   const int g = k.num_q_heads / k.num_kv_heads;
@@ -567,7 +574,8 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
     louiskv_destroy(c);
     return LOUISKV_ERR_OOM_DEVICE;
   }
-  c->pool_inst_bytes = c->pool_rows_cap * POOL_ROW_BYTES;
+  c->prb = pool_row_bytes(k.pool_dtype == LOUISKV_POOL_FP8_E4M3);
+  c->pool_inst_bytes = c->pool_rows_cap * c->prb;
   const size_t pool_bytes = (size_t)std::max<int64_t>(ni, 1) * c->pool_inst_bytes;
   if (pool_bytes > 0) {
     void* hp = nullptr;
@@ -614,7 +622,7 @@ static cudaError_t offload_prompt(louiskv_ctx* c, int layer, const KmArgs& a, cu
   const int ni = a.batch * a.hn;
   c->prec.mark(st, PH_STAGE);
   if (a.N > 0 && a.kc > 0) {
-    const int64_t inst_b = (int64_t)a.N * POOL_ROW_BYTES;
+    const int64_t inst_b = (int64_t)a.N * c->prb;
     const int per = (int)std::max<int64_t>(1, std::min<int64_t>(ni, c->stage_bytes / inst_b));
     const int64_t ib = inst_base(c, layer);
     for (int li0 = 0; li0 < ni; li0 += per) {
@@ -719,6 +727,7 @@ static louiskv_status prompt_common(louiskv_ctx* c, int32_t layer, const void* k
   a.pool_rows_cap = c->pool_rows_cap;
   a.pool = c->d_pool + ib * c->pool_inst_bytes;
   a.pool_inst_bytes = c->pool_inst_bytes;
+  a.pool_fp8 = c->cfg.pool_dtype == LOUISKV_POOL_FP8_E4M3;
   a.sinks = c->d_sinks + ib * 2 * std::max(c->S, 1) * D;
   a.S_cap = c->S;
   a.inst = c->d_inst + ib;
@@ -1224,6 +1233,7 @@ louiskv_status louiskv_get_stats(louiskv_ctx* c, louiskv_stats* out) {
   out->segments_evicted = sd.segments_evicted;
   out->kmeans_tc_iters = c->km_tc_iters;
   out->kmeans_simt_iters = c->km_simt_iters;
+  out->dma_copies = c->dma_copies;
   if (derr) return fail(c, LOUISKV_ERR_CAPACITY, "device capacity exceeded (host pool, unit table or full cache)");
   return LOUISKV_OK;
 }

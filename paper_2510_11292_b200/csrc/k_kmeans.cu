@@ -676,9 +676,16 @@ __global__ void __launch_bounds__(128) km_offload_kernel(KmArgs a, int li0, uint
   const int i = perm[r];
   const int j = a.assign[(int64_t)li * a.Nmax + i];
   const int o = off[j], n = off[j + 1] - o;
-  uint4* dst = reinterpret_cast<uint4*>(dst_base + (int64_t)blockIdx.y * dst_stride + (int64_t)o * POOL_ROW_BYTES);
-  dst[(int64_t)(r - o) * 16 + sub] = reinterpret_cast<const uint4*>(xrow(a, li, i))[sub];
-  dst[(int64_t)(n + r - o) * 16 + sub] = reinterpret_cast<const uint4*>(vrow(a, li, i))[sub];
+  uint8_t* dst = dst_base + (int64_t)blockIdx.y * dst_stride + (int64_t)o * pool_row_bytes(a.pool_fp8);
+  const uint4 kx = reinterpret_cast<const uint4*>(xrow(a, li, i))[sub];
+  const uint4 vx = reinterpret_cast<const uint4*>(vrow(a, li, i))[sub];
+  if (a.pool_fp8) {  // FP8 pool (reading R-FP8): E4M3 rows, 8 B per 16-B bf16 piece
+    reinterpret_cast<uint2*>(dst)[(int64_t)(r - o) * 16 + sub] = bf16x8_to_e4m3x8(kx);
+    reinterpret_cast<uint2*>(dst)[(int64_t)(n + r - o) * 16 + sub] = bf16x8_to_e4m3x8(vx);
+  } else {
+    reinterpret_cast<uint4*>(dst)[(int64_t)(r - o) * 16 + sub] = kx;
+    reinterpret_cast<uint4*>(dst)[(int64_t)(n + r - o) * 16 + sub] = vx;
+  }
   if (sub == 0) a.pool_pos[(int64_t)li * a.pool_rows_cap + r] = a.S + i;
 }
 
@@ -708,7 +715,7 @@ __global__ void km_units_kernel(KmArgs a, int P) {
     s.prompt_len = P;
     s.s_eff = min(a.S_cap, P);
     a.inst[li] = s;
-    atomicAdd(&a.stats->bytes_d2h, (unsigned long long)a.N * POOL_ROW_BYTES);
+    atomicAdd(&a.stats->bytes_d2h, (unsigned long long)a.N * pool_row_bytes(a.pool_fp8));
   }
 }
 

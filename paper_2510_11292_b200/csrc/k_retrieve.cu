@@ -358,11 +358,38 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
   int32_t* seloff = a.seloff + (int64_t)li * a.Umax;
   const int64_t* uoff = a.uoff + (int64_t)li * a.Umax;
   RowSrc* rows = a.rows + (int64_t)li * a.budget;
+  // BATCHED_DMA: two spans (K rows, V rows) per selected unit, in unit-id order
+  DmaSpan* spans = a.dma_spans ? a.dma_spans + (int64_t)li * a.dma_cap : nullptr;
+  int ord = 0;
+  if (spans) {
+    int n_sel;
+    ord = block_excl_scan(local_cnt, s_warp, n_sel);
+    if (tid == 0) a.dma_n[li] = 2 * n_sel;
+  }
   unsigned long long reused = 0, fetched = 0, hbytes = 0;
   for (int u = u0; u < u1; ++u) {
     const bool take = s_taken[u >> 5] >> (u & 31) & 1u;
     const bool had = sel[u] != 0;
-    if (take) {
+    if (take && spans) {
+      const int sz = s_sz[u];
+      const uint64_t nb = (uint64_t)sz * ROW_BYTES;  // (BATCHED_DMA implies a bf16 pool)
+      DmaSpan* sp = spans + 2 * ord++;
+      if (had) {
+        const int so = seloff[u];
+        sp[0] = DmaSpan{(uint64_t)(curK + (int64_t)so * D), (uint64_t)(nxtK + (int64_t)dst * D), nb};
+        sp[1] = DmaSpan{(uint64_t)(curV + (int64_t)so * D), (uint64_t)(nxtV + (int64_t)dst * D), nb};
+        ++reused;
+      } else {
+        const uint8_t* base = pool + uoff[u] * POOL_ROW_BYTES;  // unit-major [K rows | V rows]
+        sp[0] = DmaSpan{(uint64_t)base, (uint64_t)(nxtK + (int64_t)dst * D), nb};
+        sp[1] = DmaSpan{(uint64_t)(base + nb), (uint64_t)(nxtV + (int64_t)dst * D), nb};
+        ++fetched;
+        hbytes += 2 * nb;
+      }
+      sel[u] = 1;
+      seloff[u] = dst;
+      dst += sz;
+    } else if (take) {
       const int sz = s_sz[u];
       if (had) {
         const int so = seloff[u];
@@ -371,12 +398,15 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
                                  reinterpret_cast<const uint4*>(curV + (int64_t)(so + i) * D)};
         ++reused;
       } else {
-        const uint8_t* base = pool + uoff[u] * POOL_ROW_BYTES;
+        // unit-major pool span [K rows | V rows]; E4M3 rows (FP8 pool) are tagged in bit 0
+        const int prb = pool_row_bytes(a.pool_fp8), hrb = prb / 2;
+        const uint8_t* base = pool + uoff[u] * prb;
+        const uintptr_t tag = a.pool_fp8 ? 1u : 0u;
         for (int i = 0; i < sz; ++i)
-          rows[dst + i] = RowSrc{reinterpret_cast<const uint4*>(base + (int64_t)i * ROW_BYTES),
-                                 reinterpret_cast<const uint4*>(base + (int64_t)(sz + i) * ROW_BYTES)};
+          rows[dst + i] = RowSrc{reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(base + (int64_t)i * hrb) | tag),
+                                 reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(base + (int64_t)(sz + i) * hrb) | tag)};
         ++fetched;
-        hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
+        hbytes += (unsigned long long)sz * prb;
       }
       sel[u] = 1;
       seloff[u] = dst;
@@ -403,7 +433,8 @@ __device__ __forceinline__ void select_body(const RetrieveArgs& a, const int li,
     S->ws_cur = nxt;
     S->ws_rows = total;
   }
-  if (tid == 0) a.jobs[li] = GatherJob{total, 0, nxtK, nxtV};
+  // (BATCHED_DMA: the host issues the copies; the gather of append_output has nothing to do)
+  if (tid == 0) a.jobs[li] = GatherJob{spans ? 0 : total, 0, nxtK, nxtV};
 }
 
 template <int G>
@@ -411,7 +442,10 @@ __global__ void __launch_bounds__(SS_THREADS) select_kernel(RetrieveArgs a) {
   pdl_wait_trigger();
   const int li = blockIdx.x;
   const int b = li / a.hn;
-  if (!a.flag[b]) return;  // (jobs of unflagged instances were cleared by their consumer)
+  if (!a.flag[b]) {  // (jobs of unflagged instances were cleared by their consumer)
+    if (a.dma_n && threadIdx.x == 0) a.dma_n[li] = 0;
+    return;
+  }
   const int n = a.inst[li].n_units;
   const int cap = a.Umax < SORT_CAP ? a.Umax : SORT_CAP;
   if (n <= cap)

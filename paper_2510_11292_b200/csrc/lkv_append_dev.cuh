@@ -17,12 +17,12 @@ __device__ __forceinline__ void gather_rows(const AppendArgs& a, int li, const G
   for (int r = r0 + (threadIdx.x >> 4); r < r1; r += 2 * rpp) {
     const int r2 = r + rpp;
     const RowSrc s0 = R[r];
-    const uint4 k0 = s0.k[sub], v0 = s0.v[sub];
+    const uint4 k0 = load_row_piece(s0.k, sub), v0 = load_row_piece(s0.v, sub);
     uint4 k1 = k0, v1 = v0;
     if (r2 < r1) {
       const RowSrc s1 = R[r2];
-      k1 = s1.k[sub];
-      v1 = s1.v[sub];
+      k1 = load_row_piece(s1.k, sub);
+      v1 = load_row_piece(s1.v, sub);
     }
     dK[(int64_t)r * (D / 8) + sub] = k0;
     dV[(int64_t)r * (D / 8) + sub] = v0;
@@ -106,14 +106,17 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, co
         centb[(int64_t)uid * D + tid] = f2bf_rne(c);
       }
     }
-    // offload rows: unit-major span [K rows | V rows] at pool row offset prow
-    uint4* dst = reinterpret_cast<uint4*>(pool + prow * POOL_ROW_BYTES);
+    // offload rows: unit-major span [K rows | V rows] at pool row offset prow (FP8 pool: E4M3 rows)
+    uint8_t* dst = pool + prow * pool_row_bytes(a.pool_fp8);
     for (int c = tid; c < 2 * len * 16; c += blockDim.x) {
       const int isV = c >= len * 16;
       const int cc = isV ? c - len * 16 : c;
       const int i = cc >> 4, sub = cc & 15;
       const bf16* src = (isV ? ringV : ringK) + (int64_t)((start + i) % cap) * D;
-      dst[(int64_t)(isV ? len + i : i) * 16 + sub] = reinterpret_cast<const uint4*>(src)[sub];
+      const uint4 x = reinterpret_cast<const uint4*>(src)[sub];
+      const int64_t drow = isV ? len + i : i;
+      if (a.pool_fp8) reinterpret_cast<uint2*>(dst)[drow * 16 + sub] = bf16x8_to_e4m3x8(x);
+      else reinterpret_cast<uint4*>(dst)[drow * 16 + sub] = x;
     }
     for (int i = tid; i < len; i += blockDim.x) ppos[prow + i] = s.prompt_len + start + i;
     __syncthreads();
@@ -129,7 +132,7 @@ __device__ __forceinline__ void append_one(const AppendArgs& a, const int li, co
       s.fifo_head = (s.fifo_head + 1) % cap;
       s.fifo_count--;
       atomicAdd(&a.stats->segments_evicted, 1ull);
-      atomicAdd(&a.stats->bytes_d2h, (unsigned long long)len * POOL_ROW_BYTES);
+      atomicAdd(&a.stats->bytes_d2h, (unsigned long long)len * pool_row_bytes(a.pool_fp8));
     }
     __syncthreads();
   }

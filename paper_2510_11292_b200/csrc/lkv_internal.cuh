@@ -16,7 +16,9 @@ namespace lkv {
 
 constexpr int D = 128;               // head_dim (the paper's models all use 128)
 constexpr int ROW_BYTES = D * 2;     // one bf16 K (or V) row
-constexpr int POOL_ROW_BYTES = 2 * ROW_BYTES;  // K+V of one token in the host pool
+constexpr int POOL_ROW_BYTES = 2 * ROW_BYTES;  // K+V of one token in the host pool (bf16 pool)
+// FP8 pool (config pool_dtype = LOUISKV_POOL_FP8_E4M3, reading R-FP8): E4M3 rows, half the bytes
+__host__ __device__ constexpr int pool_row_bytes(int fp8) { return fp8 ? 2 * D : POOL_ROW_BYTES; }
 
 typedef __nv_bfloat16 bf16;
 
@@ -100,6 +102,7 @@ struct RetrieveArgs {
   DmaSpan* dma_spans;        // BATCHED_DMA: [batch*hn][dma_cap] spans (device-mapped host), else null
   int32_t* dma_n;            // BATCHED_DMA: [batch*hn] span counts (device-mapped host)
   int dma_cap;               // spans per instance (2 per selected unit, <= 2*B)
+  int pool_fp8;              // host-pool rows are E4M3 (converted to bf16 by the gather)
   StatsDev* stats;
   float r3c[7];              // recipe R3 Taylor coefficients fl32(ln2^i / i!) (r3_coefs)
   float inv_sqrt_d;          // recipe R2 scale fl32(1 / fl64(sqrt(d)))
@@ -132,6 +135,7 @@ struct AppendArgs {
   int64_t pool_rows_cap;
   uint8_t* pool;        // host pool (device-mapped), layer base
   int64_t pool_inst_bytes;
+  int pool_fp8;         // evicted rows are written to the pool as E4M3; E4M3 gather sources
   StatsDev* stats;
 };
 cudaError_t launch_append(const AppendArgs& a, cudaStream_t st);  // gather kernel + append kernel
@@ -235,6 +239,7 @@ struct KmArgs {
   const bf16* v;
   int64_t sb, st, sh;
   int batch, hn, S, N, kc, iters, impl;
+  int pool_fp8;      // the prompt offload writes E4M3 rows
   // outputs / state (layer bases)
   float* cent;       // [ni][Umax][D]
   bf16* centb;
@@ -340,6 +345,45 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 #ifdef __CUDACC__
 namespace lkv {
 __device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+// ---- FP8 pool conversions (reading R-FP8): 8 bf16 <-> 8 E4M3, element order kept (lower byte first)
+// bf16 -> fp32 is exact; fp32 -> E4M3 rounds to nearest even and saturates at +-448 (satfinite)
+__device__ __forceinline__ uint2 bf16x8_to_e4m3x8(const uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+    unsigned short p;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(p) : "f"(hi), "f"(lo));  // (a -> upper byte)
+    o[i] = p;
+  }
+  return make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+}
+// E4M3 -> fp16 is exact, fp16 -> fp32 exact, and every E4M3 value has a 3-bit mantissa and an
+// exponent in [-9, 8], so its fp32 bits truncated to bf16 are exact
+__device__ __forceinline__ uint4 e4m3x8_to_bf16x8(const uint2 v) {
+  const uint32_t in[2] = {v.x, v.y};
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned short p = (unsigned short)(in[i >> 1] >> (16 * (i & 1)));
+    uint32_t h2;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(p));
+    float f0, f1;
+    asm("cvt.f32.f16 %0, %1;" : "=f"(f0) : "h"((unsigned short)(h2 & 0xFFFFu)));
+    asm("cvt.f32.f16 %0, %1;" : "=f"(f1) : "h"((unsigned short)(h2 >> 16)));
+    o[i] = (__float_as_uint(f0) >> 16) | (__float_as_uint(f1) & 0xFFFF0000u);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+// 16-B piece `sub` of a working-set row source: bf16 rows are read as is; a source pointer tagged in
+// bit 0 is an E4M3 pool row (8 B per piece), converted
+__device__ __forceinline__ uint4 load_row_piece(const uint4* p, int sub) {
+  const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+  if (u & 1u) return e4m3x8_to_bf16x8(reinterpret_cast<const uint2*>(u & ~(uintptr_t)1)[sub]);
+  return p[sub];
+}
 __device__ __forceinline__ void unpack8(const uint4 u, float* f) {
   f[0] = __uint_as_float(u.x << 16);
   f[1] = __uint_as_float(u.x & 0xFFFF0000u);

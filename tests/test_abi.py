@@ -46,11 +46,12 @@ def test_ctypes_struct_layout_matches_c(lkv):
 #include <stddef.h>
 #include "louiskv.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(louiskv_config), offsetof(louiskv_config, tau),
          offsetof(louiskv_config, full_cache_layers), offsetof(louiskv_config, device),
          sizeof(louiskv_stats), offsetof(louiskv_stats, segments_evicted), sizeof(louiskv_prefill_times),
          offsetof(louiskv_prefill_times, assign_flops), offsetof(louiskv_prefill_times, calls),
-         offsetof(louiskv_config, fetch_mode), offsetof(louiskv_config, index_offload));
+         offsetof(louiskv_config, fetch_mode), offsetof(louiskv_config, index_offload),
+         offsetof(louiskv_config, pool_dtype), offsetof(louiskv_stats, dma_copies));
   return 0;
 }
 '''
@@ -63,7 +64,8 @@ int main(void) {
     C, S, T = lkv.Config, lkv.Stats, lkv.PrefillTimes
     assert vals == [ctypes.sizeof(C), C.tau.offset, C.full_cache_layers.offset, C.device.offset,
                     ctypes.sizeof(S), S.segments_evicted.offset, ctypes.sizeof(T), T.assign_flops.offset,
-                    T.calls.offset, C.fetch_mode.offset, C.index_offload.offset]
+                    T.calls.offset, C.fetch_mode.offset, C.index_offload.offset, C.pool_dtype.offset,
+                    S.dma_copies.offset]
 
 
 def test_invalid_config_rejected_synchronously(lkv):
@@ -84,6 +86,11 @@ def test_invalid_config_rejected_synchronously(lkv):
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     bad.fetch_mode = 0
     bad.index_offload = 2  # 0 (device index) or 1 (host index)
+    assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    bad.index_offload = 0
+    bad.pool_dtype = 2  # BF16 or FP8_E4M3
+    assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
+    bad.pool_dtype, bad.fetch_mode = lkv.POOL_FP8_E4M3, lkv.FETCH_BATCHED_DMA  # copies cannot convert
     assert L.louiskv_create(ctypes.byref(bad), ctypes.byref(h)) == lkv.ERR_INVALID_ARG
     assert L.louiskv_state_restore(None, None) == lkv.ERR_INVALID_ARG
     assert L.louiskv_cluster_prompt(None, 0, None, None, 0, 0, 0, 1, 1, None) == lkv.ERR_INVALID_ARG

@@ -38,7 +38,7 @@ def small_cfg(**kw):
 
 def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode=PER_LAYER, max_open=None,
                 check_every_step=True, kv_head_begin=0, kv_head_count=None, compare_ws=True, fused=False,
-                attn_impl=0, trigger_stride=0, fetch_mode=0, index_offload=0):
+                attn_impl=0, trigger_stride=0, fetch_mode=0, index_offload=0, pool_fp8=False):
     """Drive GPU and oracle through `steps` decode steps; assert parity at every step.
     fused: False = the four per-step calls; True = should_retrieve, retrieve, append_attn;
     "layer" = louiskv_decode_layer (one launch per retrieval layer)."""
@@ -49,9 +49,10 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     ctx = lkv.Context(lkv.make_config(cfg, kv_head_begin=h0, kv_head_count=hn, trigger_ref=trigger_ref,
                                       boundary_mode=boundary_mode, max_open_segment=max_open or 0,
                                       attn_impl=attn_impl, trigger_stride=trigger_stride,
-                                      fetch_mode=fetch_mode, index_offload=index_offload))
+                                      fetch_mode=fetch_mode, index_offload=index_offload,
+                                      pool_dtype=lkv.POOL_FP8_E4M3 if pool_fp8 else lkv.POOL_BF16))
     ep = OracleEpisode(cfg, trigger_ref=trigger_ref, boundary_mode=boundary_mode, max_open_segment=max_open,
-                       kv_head_begin=h0, kv_head_count=hn, trigger_stride=trigger_stride)
+                       kv_head_begin=h0, kv_head_count=hn, trigger_stride=trigger_stride, pool_fp8=pool_fp8)
     L, b = cfg.num_layers, cfg.batch
     for l in range(L):
         Kl = inp.K[l][:, :, h0:h0 + hn]
@@ -141,6 +142,10 @@ def run_episode(cfg, inp, steps, assign_fn, trigger_ref=PREV_STEP, boundary_mode
     for key in ("retrievals", "units_scored", "units_selected", "units_reused", "units_fetched", "bytes_h2d",
                 "bytes_d2h", "segments_evicted"):
         assert st_g[key] == st_o[key], (key, st_g[key], st_o[key])
+    if fetch_mode:  # the copies really went through the copy engines
+        assert st_g["dma_copies"] > 0 or st_o["units_selected"] == 0
+    else:
+        assert st_g["dma_copies"] == 0
     ctx.close()
     return worst, n_flags, st_o
 
@@ -796,3 +801,52 @@ def test_index_offload_gpu_kmeans_bit_identical_and_smaller():
     assert s0 == s1 and s0["retrievals"] > 0
     assert mems[1]["device_bytes"] < mems[0]["device_bytes"]
     assert mems[1]["host_pool_bytes"] > mems[0]["host_pool_bytes"]
+
+
+@pytest.mark.parametrize("fused", [False, True, "layer"])
+def test_episode_fp8_pool(fused):
+    """pool_dtype FP8_E4M3 (reading R-FP8): the prompt offload and the segment
+    evictions store E4M3 rows, the gather converts them back — against the oracle episode with the
+    same pool: flags, r_t, selections, unit tables bit-exact, the working set equal to the E4M3 values
+    of the units' rows bit for bit, half the pool bytes (stats), attention within the bar."""
+    cfg = small_cfg()
+    inp = make_inputs(cfg, cfg.decode_steps, 25)
+    _, n_flags, st = run_episode(cfg, inp, cfg.decode_steps, lambda l, Kn: oracle_assign(cfg, Kn), fused=fused,
+                                 pool_fp8=True)
+    assert n_flags > 5 and st["segments_evicted"] > 0 and st["units_fetched"] > 0
+
+
+def test_fp8_pool_c4_params_gpu_kmeans():
+    """FP8 pool on the C4 parameters (B=1024, batch 3) with the GPU's own k-means and the single-launch
+    layer: decisions identical to the bf16-pool run (the index is unchanged), pool bytes halved, and
+    the attention outputs within the E4M3 error of the bf16-pool outputs."""
+    lkv = _lkv()
+    cfg = C4.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, batch=3,
+                     prompt_len=4096, decode_steps=20)
+    inp = make_inputs(cfg, 20, 26)
+    res = []
+    for pd in (lkv.POOL_BF16, lkv.POOL_FP8_E4M3):
+        ctx = lkv.Context(lkv.make_config(cfg, pool_dtype=pd))
+        for l in range(cfg.num_layers):
+            ctx.cluster_prompt(l, inp.K[l], inp.V[l])
+        o = torch.zeros((cfg.batch, cfg.num_q_heads, 128), dtype=torch.float32, device="cuda")
+        ob = torch.zeros_like(o, dtype=torch.bfloat16)
+        fl = torch.zeros(cfg.batch, dtype=torch.uint8, device="cuda")
+        outs, flags = [], []
+        for t in range(20):
+            for l in range(cfg.num_layers):
+                ctx.decode_layer(l, inp.q[t, l], inp.k[t, l].contiguous(), inp.v[t, l].contiguous(), ob, o,
+                                 flag_out=fl)
+                torch.cuda.synchronize()
+                outs.append(o.cpu().numpy().copy())
+                flags.append(fl.cpu().numpy().copy())
+        sels = [ctx.get_selection(1, bb, hh) for bb in range(cfg.batch) for hh in range(cfg.num_kv_heads)]
+        res.append((outs, flags, sels, ctx.stats(), ctx.memory()))
+        ctx.close()
+    (o0, f0, s0, st0, m0), (o1, f1, s1, st1, m1) = res
+    assert all(np.array_equal(a, b) for a, b in zip(f0, f1))
+    assert all(np.array_equal(a, b) for a, b in zip(s0, s1))
+    assert st1["bytes_h2d"] * 2 == st0["bytes_h2d"] > 0 and st1["bytes_d2h"] * 2 == st0["bytes_d2h"]
+    assert m1["host_pool_bytes"] * 2 == m0["host_pool_bytes"]
+    err = max(np.abs(a - b).max() for a, b in zip(o0, o1))
+    assert 0 < err < 0.1, err

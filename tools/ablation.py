@@ -27,6 +27,8 @@ Qwen3-8B 32K+16K), decode steps graph-replayed with device-residen
 5. Index placement (the paper's future work: "offloading KV cache indices to CPU DRAM"): the
    unit index (centroids) in device memory vs in pinned host memory read over the link at every
    scoring, C2 and the C4 shape at 32K: step time and device bytes (--only index).
+6. Pool element type: bf16 (the paper's) vs E4M3 host pool — half the offload
+   and gather bytes; C2 and the C4 shape at 32K (--only fp8).
 
 usage: python tools/ablation.py [--steps 64] > profiles/r02_ablation.json
 """
@@ -54,7 +56,8 @@ BASE = BASE.replace(k_planted=max(BASE.n_clusters // 4, 16))
 dev = torch.device("cuda", 0)
 
 
-def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetch=0, graph=True, index_offload=0):
+def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetch=0, graph=True, index_offload=0,
+        pool_dtype=0):
     """One variant: prefill every layer, warm up, time args.steps decode steps (graph-replayed, or
     issued eagerly with graph=False)."""
     L, full, b = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch
@@ -63,7 +66,7 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetc
     T = 2 + 8 + args.steps
     ctx = lkv.Context(lkv.make_config(run_cfg, max_output_len=T + 1, trigger_stride=stride,
                                       prompt_units=lkv.UNITS_PAGES if units == "pages" else lkv.UNITS_KMEANS,
-                                      fetch_mode=fetch, index_offload=index_offload))
+                                      fetch_mode=fetch, index_offload=index_offload, pool_dtype=pool_dtype))
     plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
     for l in range(L):
         K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
@@ -115,7 +118,7 @@ def run(name, cfg, *, per_head=False, fused=True, stride=0, units="kmeans", fetc
     nrl = (L - len(full)) * b
     row = {"variant": name, "tau": cfg.tau, "drift": cfg.drift, "per_head": per_head, "fused": fused,
            "trigger_stride": stride, "units": units, "fetch": ["zero_copy", "batched_dma"][fetch],
-           "graph": graph, "index_offload": index_offload, "memory": ctx.memory(), "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
+           "graph": graph, "index_offload": index_offload, "pool": ["bf16", "e4m3"][pool_dtype], "memory": ctx.memory(), "ms_per_step": ms, "tok_per_s": b / (ms / 1e3),
            "retrievals_per_layer_step": d["retrievals"] / (args.steps * nrl),
            "h2d_MB_per_step": d["bytes_h2d"] / args.steps / 1e6,
            "reuse_frac": d["units_reused"] / max(d["units_selected"], 1)}
@@ -158,6 +161,11 @@ if args.only == "index":
     rows["index"] = [run("C2 index on the device", C2T), run("C2 index in host DRAM", C2T, index_offload=1),
                      run("C4 shape 32K batch 2, index on the device", BASE),
                      run("C4 shape 32K batch 2, index in host DRAM", BASE, index_offload=1)]
+if args.only == "fp8":
+    C2T = C2.replace(k_planted=max(C2.n_clusters // 4, 16))
+    rows["fp8"] = [run("C2 bf16 pool", C2T), run("C2 E4M3 pool", C2T, pool_dtype=lkv.POOL_FP8_E4M3),
+                   run("C4 shape 32K batch 2, bf16 pool", BASE),
+                   run("C4 shape 32K batch 2, E4M3 pool", BASE, pool_dtype=lkv.POOL_FP8_E4M3)]
 print(json.dumps({"workload": f"Qwen3-8B LILO shape, {args.prompt}-token prompt, batch {args.batch}, "
                               f"S=64 W=256 B=1024 c=16, {args.steps} timed decode steps (synthetic, seed 0)",
                   "paper": "P:189 (SR ~2.6x, GS +13.1%, CK +15.7% on A6000, Qwen3-8B 32K+16K), P:465 (tau)",
