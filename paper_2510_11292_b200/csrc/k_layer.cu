@@ -78,7 +78,7 @@ constexpr int LK_SMEM = 192 * 1024;
 static_assert(LK_SMEM >= AT_SMEM, "layer arena");
 constexpr int REP_X_MIN = LK_SMEM - rep_off_x(LK_REP_N);
 struct SelEnt {  // one selected unit, in id (= destination) order
-  int dst, sz, u, pad;
+  int dst, sz, u, f8;  // f8: the rows are E4M3 host-pool rows (FP8 pool), converted by the gather
   const uint8_t* kb;  // first K row (current working set, or the host pool span)
   const uint8_t* vb;
 };
@@ -708,17 +708,19 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
       e.dst = dst;
       e.sz = sz;
       e.u = u;
-      e.pad = 0;
+      e.f8 = 0;
       if (hadv[i]) {
         e.kb = curK + (int64_t)sov[i] * ROW_BYTES;
         e.vb = curV + (int64_t)sov[i] * ROW_BYTES;
         ++reused;
       } else {
-        const uint8_t* base = pool + uov[i] * POOL_ROW_BYTES;
+        const int prb = pool_row_bytes(a.pool_fp8);
+        const uint8_t* base = pool + uov[i] * prb;
         e.kb = base;
-        e.vb = base + (int64_t)sz * ROW_BYTES;
+        e.vb = base + (int64_t)sz * (prb / 2);
+        e.f8 = a.pool_fp8;
         ++fetched;
-        hbytes += (unsigned long long)sz * POOL_ROW_BYTES;
+        hbytes += (unsigned long long)sz * prb;
       }
       LIST[k++] = e;
       if (u >= lo && u < hi) own_dst[u - lo] = dst;
@@ -772,8 +774,13 @@ __device__ __forceinline__ void lk_gather_list(const SelEnt* LIST, const int nse
           else hi = mid - 1;
         }
         const int off = r - LIST[lo].dst;
-        kv[i] = reinterpret_cast<const uint4*>(LIST[lo].kb + (int64_t)off * ROW_BYTES)[sub];
-        vv[i] = reinterpret_cast<const uint4*>(LIST[lo].vb + (int64_t)off * ROW_BYTES)[sub];
+        if (LIST[lo].f8) {  // E4M3 pool rows (128 B): 8 B per piece, converted to bf16
+          kv[i] = e4m3x8_to_bf16x8(reinterpret_cast<const uint2*>(LIST[lo].kb + (int64_t)off * D)[sub]);
+          vv[i] = e4m3x8_to_bf16x8(reinterpret_cast<const uint2*>(LIST[lo].vb + (int64_t)off * D)[sub]);
+        } else {
+          kv[i] = reinterpret_cast<const uint4*>(LIST[lo].kb + (int64_t)off * ROW_BYTES)[sub];
+          vv[i] = reinterpret_cast<const uint4*>(LIST[lo].vb + (int64_t)off * ROW_BYTES)[sub];
+        }
       }
     }
 #pragma unroll
