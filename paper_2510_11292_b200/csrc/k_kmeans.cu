@@ -489,6 +489,52 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
 }
 
 // stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
+#ifndef LKV_KM_SCATTER_WARP
+// Stable counting-sort scatter, one 1024-thread CTA per 1024-key chunk: the chunk's keys are sorted
+// on chip by (cluster, position) — a bitonic sort of 26-bit keys cluster << 10 | lane — and key p of
+// the sorted chunk goes to its cluster's base (cluster offset + the chunk's column prefix) plus its
+// rank in the run of equal clusters (p minus the run's first index, by binary search). Positions
+// ascend within every cluster (the lane is the low key part), exactly the order of the warp-per-chunk
+// scatter it replaces (which walked the chunk in 32 dependent rounds at one warp per chunk).
+__global__ void __launch_bounds__(KM_CHUNK) km_scatter_kernel(KmArgs a) {
+  pdl_wait_trigger();
+  __shared__ uint32_t sk[KM_CHUNK];
+  const int li = blockIdx.y, c = blockIdx.x, t = threadIdx.x;
+  const int i0 = c * KM_CHUNK, i1 = min(a.N, i0 + KM_CHUNK);
+  const int32_t* as = a.assign + (int64_t)li * a.Nmax;
+  sk[t] = i0 + t < i1 ? ((uint32_t)as[i0 + t] << 10) | (uint32_t)t : 0xFFFFFFFFu;
+  __syncthreads();
+  for (int k = 2; k <= KM_CHUNK; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int p = t ^ j;
+      if (p > t) {
+        const uint32_t x = sk[t], y = sk[p];
+        const bool up = (t & k) == 0;
+        if ((x > y) == up) {
+          sk[t] = y;
+          sk[p] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t key = sk[t];
+  if (key == 0xFFFFFFFFu) return;
+  const int cl = (int)(key >> 10), lane_i = (int)(key & 1023u);
+  int lo = 0, hi = t;  // first index of this cluster's run
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)(sk[mid] >> 10) < cl) lo = mid + 1;
+    else hi = mid;
+  }
+  const int rank = t - lo;
+  const int cpre = a.ccT[((int64_t)li * a.nchunk_max + c) * a.kmax + cl];
+  const int o = a.off[(int64_t)li * (a.kmax + 1) + cl];
+  const int to = a.toff[(int64_t)li * (a.kmax + 1) + cl];
+  a.perm[(int64_t)li * a.Nmax + o + cpre + rank] = i0 + lane_i;
+  a.tperm[(int64_t)li * a.task_max * KM_TASK + (int64_t)to * KM_TASK + cpre + rank] = i0 + lane_i;
+}
+#else
 __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   pdl_wait_trigger();
   extern __shared__ int base[];  // [kc] running offsets of this chunk, then [kc] the padded ones
@@ -552,6 +598,8 @@ __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
     __syncwarp();
   }
 }
+
+#endif
 
 // centroid update, task based: cluster j is cut into ceil(|j| / KM_TASK) tasks of consecutive
 // members (position order); a warp sums one task (lane = 4 dims, sequential fp32). Single-task
@@ -762,7 +810,11 @@ static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool rep
     launch_k(km_colscan_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, nchunk, 1);
     launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);
   }
+#ifndef LKV_KM_SCATTER_WARP
+  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(KM_CHUNK), 0, st, a);
+#else
   launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), 2 * sizeof(int) * a.kc, st, a);
+#endif
   return cudaGetLastError();
 }
 
