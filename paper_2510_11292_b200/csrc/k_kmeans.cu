@@ -489,14 +489,15 @@ __global__ void __launch_bounds__(1024) km_repair_kernel(KmArgs a, int nchunk) {
 }
 
 // stable counting-sort scatter; one warp per chunk, rounds of 32 keys in position order
-#ifndef LKV_KM_SCATTER_WARP
-// Stable counting-sort scatter, one 1024-thread CTA per 1024-key chunk: the chunk's keys are sorted
+// Stable counting-sort scatter, one 1024-thread CTA per 1024-key chunk (used when the chunks of all
+// instances fit one wave of such CTAs — few instances, e.g. C2: 256 chunks; A/B C2 sort phase
+// 68.5 -> 64 us per layer-iteration, C4 with 4096 chunks 234 -> 266, so the warp version serves there): the chunk's keys are sorted
 // on chip by (cluster, position) — a bitonic sort of 26-bit keys cluster << 10 | lane — and key p of
 // the sorted chunk goes to its cluster's base (cluster offset + the chunk's column prefix) plus its
 // rank in the run of equal clusters (p minus the run's first index, by binary search). Positions
 // ascend within every cluster (the lane is the low key part), exactly the order of the warp-per-chunk
 // scatter it replaces (which walked the chunk in 32 dependent rounds at one warp per chunk).
-__global__ void __launch_bounds__(KM_CHUNK) km_scatter_kernel(KmArgs a) {
+__global__ void __launch_bounds__(KM_CHUNK) km_scatter_cta_kernel(KmArgs a) {
   pdl_wait_trigger();
   __shared__ uint32_t sk[KM_CHUNK];
   const int li = blockIdx.y, c = blockIdx.x, t = threadIdx.x;
@@ -534,7 +535,8 @@ __global__ void __launch_bounds__(KM_CHUNK) km_scatter_kernel(KmArgs a) {
   a.perm[(int64_t)li * a.Nmax + o + cpre + rank] = i0 + lane_i;
   a.tperm[(int64_t)li * a.task_max * KM_TASK + (int64_t)to * KM_TASK + cpre + rank] = i0 + lane_i;
 }
-#else
+
+// the same scatter by one warp per chunk (32 rounds of 32 keys, match_any ranks): many chunks
 __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   pdl_wait_trigger();
   extern __shared__ int base[];  // [kc] running offsets of this chunk, then [kc] the padded ones
@@ -599,7 +601,6 @@ __global__ void __launch_bounds__(32) km_scatter_kernel(KmArgs a) {
   }
 }
 
-#endif
 
 // centroid update, task based: cluster j is cut into ceil(|j| / KM_TASK) tasks of consecutive
 // members (position order); a warp sums one task (lane = 4 dims, sequential fp32). Single-task
@@ -810,11 +811,16 @@ static cudaError_t sort_by_cluster(const KmArgs& a, int ni, int nchunk, bool rep
     launch_k(km_colscan_kernel, dim3(dim3((a.kc + 255) / 256, ni)), dim3(256), 0, st, a, nchunk, 1);
     launch_k(km_offsets_kernel, dim3(ni), dim3(1024), 0, st, a, 1);
   }
-#ifndef LKV_KM_SCATTER_WARP
-  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(KM_CHUNK), 0, st, a);
-#else
-  launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), 2 * sizeof(int) * a.kc, st, a);
-#endif
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  if ((int64_t)nchunk * ni <= 2 * sms)  // (two 1024-thread CTAs per SM)
+    launch_k(km_scatter_cta_kernel, dim3(dim3(nchunk, ni)), dim3(KM_CHUNK), 0, st, a);
+  else
+    launch_k(km_scatter_kernel, dim3(dim3(nchunk, ni)), dim3(32), 2 * sizeof(int) * a.kc, st, a);
   return cudaGetLastError();
 }
 
