@@ -1,7 +1,8 @@
 """Tiny runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck):
 prompt clustering (tcgen05 + SIMT assignment, page units, caller-supplied units), the four per-step ABI
 calls, the fused append+attention, the single-launch layer kernel at cluster sizes 8 and 2 (incl. the
-big-mode select with > 8192 live units), full-cache layers (tensor-core and SIMT attention).
+big-mode select with > 8192 live units), full-cache layers (tensor-core and SIMT attention), (r2) the
+BATCHED_DMA fetch, the host-resident index and the E4M3 pool.
 usage: compute-sanitizer --tool <tool> python tools/sanitize.py"""
 import os
 import sys
@@ -21,9 +22,9 @@ base = Config("san", num_layers=2, num_q_heads=8, num_kv_heads=2, head_dim=128, 
               kmeans_iters=2, full_cache_layers=(0,), seg_mean=3.0)
 
 
-def episode(cfg, steps, mode, units=lkv.UNITS_KMEANS, kimpl=0, aimpl=0, assign=None):
+def episode(cfg, steps, mode, units=lkv.UNITS_KMEANS, kimpl=0, aimpl=0, assign=None, **variant):
     inp = make_inputs(cfg, steps, 1)
-    ctx = lkv.Context(lkv.make_config(cfg, kmeans_impl=kimpl, attn_impl=aimpl, prompt_units=units))
+    ctx = lkv.Context(lkv.make_config(cfg, kmeans_impl=kimpl, attn_impl=aimpl, prompt_units=units, **variant))
     for l in range(cfg.num_layers):
         if assign is not None and l not in cfg.full_cache_layers:
             a = assign(cfg, inp, l)
@@ -61,6 +62,11 @@ runs = [
     ("append_attn, SIMT k-means, SIMT full attention", lambda: episode(base, 6, "fused", kimpl=1, aimpl=1)),
     ("decode_layer CL=8", lambda: episode(base, 6, "layer")),
     ("decode_layer pages", lambda: episode(base, 4, "layer", units=lkv.UNITS_PAGES)),
+    ("four-call, BATCHED_DMA fetch", lambda: episode(base, 6, "calls", fetch_mode=lkv.FETCH_BATCHED_DMA)),
+    ("decode_layer, index offload", lambda: episode(base, 6, "layer", index_offload=1)),
+    ("four-call, index offload", lambda: episode(base, 6, "calls", index_offload=1)),
+    ("decode_layer, E4M3 pool", lambda: episode(base, 6, "layer", pool_dtype=lkv.POOL_FP8_E4M3)),
+    ("append_attn, E4M3 pool", lambda: episode(base, 6, "fused", pool_dtype=lkv.POOL_FP8_E4M3)),
 ]
 
 
