@@ -51,7 +51,11 @@ def parse(argv=None):
     p.add_argument("--steps", type=int, default=256)
     p.add_argument("--warmup", type=int, default=16)
     p.add_argument("--impl", default="product", choices=["product", "reference"])
-    p.add_argument("--config", default="C2", choices=["C2", "C3", "C4"])
+    p.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
+    p.add_argument("--shard-of", type=int, default=0,
+                   help="N > 1 at one GPU: run rank 0's share of an N-GPU KV-head-sharded job (its KV heads "
+                        "[0, Hkv/N) of every sequence; the all-gather is not run) — C5's per-GPU work")
+    p.add_argument("--batch", type=int, default=0, help="override the config's batch (host-memory bound)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-l2-variant", action="store_true")
@@ -208,6 +212,9 @@ def n_cores() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+CONFIG_BATCH = {"C1": 1, "C2": 1, "C3": 1, "C4": 8, "C5": 32}
 
 
 def throughput_cfg(name: str):
@@ -445,6 +452,8 @@ def main(argv=None):
     world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
     cfg = throughput_cfg(args.config)
+    if args.batch:
+        cfg = cfg.replace(batch=args.batch, k_planted=cfg.k_planted)
     L, b, Hq, Hkv, d, g = cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.group
     full = set(cfg.full_cache_layers)
     ret_layers = [l for l in range(L) if l not in full]
@@ -454,6 +463,8 @@ def main(argv=None):
     heads = shard == "heads"
     seed = args.seed if heads else rank_seed(args.seed, rank)
     hb, hc = head_range(rank, world, Hkv) if heads else (0, Hkv)
+    if args.shard_of > 1 and world == 1:
+        hb, hc = head_range(0, args.shard_of, Hkv)
     gq = g * hc
     jobs = 1 if heads else world
     cap_out = args.max_output_len or max(cfg.max_output_len, T + 1)
@@ -803,9 +814,15 @@ def main(argv=None):
         "config": {"workload": workload_label(cfg), "global_batch": b * jobs, "seq_len": cfg.prompt_len,
                    "decode_window": f"steps t = {s0 + 1}..{s0 + K} of the generation (after {W} warm-up steps)",
                    "capacity_max_output_len": cap_out,
-                   "parallelism": (f"kv-head shard x{world} (heads [{hb}, {hb + hc}) on rank {rank}; NCCL all-gather "
-                                   f"of the per-head outputs {'per layer' if args.gather == 'layer' else 'once per step'})")
-                   if heads else f"weak dp{world} (independent sequences per rank, no collective)",
+                   **({"batch_override": f"batch {b} instead of the config's {CONFIG_BATCH[cfg.name]}: the pinned pool "
+                                         f"of the full batch exceeds this box's host memory"}
+                      if args.batch else {}),
+                   "parallelism": ((f"one rank's share of a {args.shard_of}-GPU KV-head shard: heads [{hb}, {hb + hc}) "
+                                    f"of {Hkv} (the all-gather of the per-head outputs is not run at one GPU)")
+                                   if args.shard_of > 1 and world == 1 else
+                                   (f"kv-head shard x{world} (heads [{hb}, {hb + hc}) on rank {rank}; NCCL all-gather "
+                                    f"of the per-head outputs {'per layer' if args.gather == 'layer' else 'once per step'})")
+                                   if heads else f"weak dp{world} (independent sequences per rank, no collective)"),
                    "l2": (f"inputs larger than L2: {kv_step_bytes / 1e6:.0f} MB of KV read per step per rank > 2 x 126 MB"
                           if flush_buf is None else
                           f"L2 flushed between steps ({kv_step_bytes / 1e6:.0f} MB of KV per step per rank)"),
