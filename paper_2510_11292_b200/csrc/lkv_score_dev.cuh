@@ -31,22 +31,33 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
   return ((unsigned long long)hi << 32) | lo;
 }
 
-// R1 per-head cosines of one sequence into s_cos[Hq] (all NT threads call; warp-uniform loop, two
-// heads per warp, lanes past the last head shuffle zeros). Caller syncs before reading s_cos.
+// R1 per-head cosines of one sequence into s_cos[Hq] (all NT threads call; two heads per warp per
+// round, lanes past the last head shuffle zeros). Every round's q_ref / q_t pieces are loaded before
+// any arithmetic (Hq <= 64: at most 4 rounds at NT = 256), so the loads cost one round trip, not one
+// per round. Caller syncs before reading s_cos.
 template <int NT>
 __device__ __forceinline__ void trigger_cosines(const uint16_t* qc, const uint16_t* qr, int Hq, double* s_cos) {
+  constexpr int HPR = (NT / 32) * 2;          // heads per round
+  constexpr int MAXR = (64 + HPR - 1) / HPR;  // rounds for the largest Hq (64, louiskv_create)
   const int tid = threadIdx.x, l16 = tid & 15, warp = tid >> 5, lane = tid & 31;
-  for (int hb = warp * 2; hb < Hq; hb += (NT / 32) * 2) {
-    const int hh = hb + (lane >> 4);
-    const bool act = hh < Hq;
-    uint4 ua = make_uint4(0, 0, 0, 0), uc = ua;
-    if (act) {
-      ua = reinterpret_cast<const uint4*>(qr + hh * D)[l16];
-      uc = reinterpret_cast<const uint4*>(qc + hh * D)[l16];
+  uint4 ua[MAXR], uc[MAXR];
+#pragma unroll
+  for (int it = 0; it < MAXR; ++it) {
+    const int hh = warp * 2 + it * HPR + (lane >> 4);
+    ua[it] = uc[it] = make_uint4(0, 0, 0, 0);
+    if (hh < Hq) {
+      ua[it] = reinterpret_cast<const uint4*>(qr + hh * D)[l16];
+      uc[it] = reinterpret_cast<const uint4*>(qc + hh * D)[l16];
     }
+  }
+#pragma unroll
+  for (int it = 0; it < MAXR; ++it) {
+    if (warp * 2 + it * HPR >= Hq) break;  // (warp-uniform)
+    const int hh = warp * 2 + it * HPR + (lane >> 4);
+    const bool act = hh < Hq;
     float fa[8], fc[8];
-    unpack8(ua, fa);
-    unpack8(uc, fc);
+    unpack8(ua[it], fa);
+    unpack8(uc[it], fc);
     double dot = 0.0, na = 0.0, nb = 0.0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {

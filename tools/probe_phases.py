@@ -22,24 +22,27 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 tau = float(sys.argv[2]) if len(sys.argv) > 2 else None
 if tau is not None:
     cfg = cfg.replace(tau=tau)
+if os.environ.get("LKV_PROBE_BATCH"):  # (e.g. C5's per-GPU share: batch 16, one KV head)
+    cfg = cfg.replace(batch=int(os.environ["LKV_PROBE_BATCH"]), k_planted=max(cfg.n_clusters // 4, 16))
 dev = torch.device("cuda", 0)
-L, full, b, Hkv = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch, cfg.num_kv_heads
+L, full, b = cfg.num_layers, set(cfg.full_cache_layers), cfg.batch
+Hkv = int(os.environ.get("LKV_PROBE_HEADS", cfg.num_kv_heads))  # owned KV heads [0, Hkv)
 STEPS = 24
-ctx = lkv.Context(lkv.make_config(cfg, max_output_len=STEPS + 4))
+ctx = lkv.Context(lkv.make_config(cfg, max_output_len=STEPS + 4, kv_head_count=Hkv))
 plants = [synth.planted(cfg, l, 0, dev) for l in range(L)]
 for l in range(L):
     K, V = synth.prompt_kv(cfg, l, 0, dev, plants[l])
-    ctx.cluster_prompt(l, K, V)
+    ctx.cluster_prompt(l, K[:, :, :Hkv], V[:, :, :Hkv])
     del K, V
 q, kk, vv, _ = synth.decode_stream(cfg, STEPS + 2, 0, dev, plants)
 q_in, k_in, v_in = q[0].clone(), kk[0].clone(), vv[0].clone()
-out = torch.empty_like(q_in)
+out = torch.empty((L, b, cfg.group * Hkv, cfg.head_dim), dtype=q_in.dtype, device=dev)
 flags = torch.zeros((L, b), dtype=torch.uint8, device=dev)
 
 
 def issue():
     for l in range(L):
-        ctx.decode_layer(l, q_in[l], k_in[l], v_in[l], out[l], flag_out=flags[l])
+        ctx.decode_layer(l, q_in[l], k_in[l][:, :Hkv], v_in[l][:, :Hkv], out[l], flag_out=flags[l])
 
 
 issue()
