@@ -143,7 +143,8 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   constexpr int PITCH = ROW_BYTES + 16;
   constexpr int HPT = G;           // heads per thread: g independent fmaf chains (ILP g)
   constexpr int RB = AT_THREADS;   // rows per round: one per thread (measured: fewer, longer rounds
-                                   // beat more rows in flight — each round is one chain latency)
+                                   // beat more rows in flight — each round is one chain latency; at
+                                   // g = 8, two threads per row with E in shared memory: C5 -4 %)
   const int e_bytes_s = (G * m * 4 + 127) & ~127;
   const int nb_s = big ? 0 : min(6, (x_bytes - e_bytes_s) / (RB * PITCH));
   const int nb_g = min(6, x_bytes / (RB * PITCH));

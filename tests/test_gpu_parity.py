@@ -297,6 +297,20 @@ def test_decode_layer_many_units(prompt_len):
         assert st["units_scored"] >= N and n_flags >= 2
 
 
+@pytest.mark.parametrize("prompt_len", [8000 + 16, 9000 + 16])
+def test_decode_layer_many_units_g8(prompt_len):
+    """g = 8 (C5's Qwen3-32B group: 64 query heads, two threads per logits row) at ~8K units — the
+    on-chip select with the own logits in shared memory — and ~9K units (global-scratch select), the
+    regime of C5's 8188 prompt clusters; every step compared."""
+    cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=8, batch=1, num_kv_heads=2, num_q_heads=16,
+                    prompt_len=prompt_len, avg_cluster_size=1, budget_tokens=300, tau=0.95)
+    inp = make_inputs(cfg, 8, 27)
+    N = prompt_len - cfg.sink_tokens
+    a = np.arange(N, dtype=np.int32)[None, None, :].repeat(2, 1)
+    _, n_flags, st = run_episode(cfg, inp, 8, lambda l, Kn: a, fused="layer")
+    assert st["units_scored"] >= 2 * N and n_flags >= 2
+
+
 def test_zero_query_and_prompt_shorter_than_sinks():
     cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=6, batch=1, prompt_len=12, sink_tokens=16)
     inp = make_inputs(cfg, 6, 8)
