@@ -992,6 +992,8 @@ louiskv_status louiskv_decode_layer(louiskv_ctx* c, int32_t layer, const void* q
   la.at.app = append_args(c, layer, k_t, v_t, stride_kv);
   la.layer = layer;
   la.early = early;
+  // the speculative prefetch of the centroid rows etc. pays only while a launch's unit index is small
+  la.spec_pf = (int64_t)c->batch * c->hn * std::max(c->kmax, 1) * ROW_BYTES <= (8ll << 20) ? 1 : 0;
   LKV_LAUNCH(c, launch_layer(la, st), "decode_layer");
   c->last_layer = layer;
   c->last_stream = stream;

@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(AT_THREADS, G <= 4 ? LKV_LAYER_MINB : 1) layer
 #ifndef LKV_NO_SPEC_PREFETCH
   // (only at 8 CTAs per instance, i.e. few instances: measured +1.2 % at C2; at batch (C4, CL 4) the
   // unflagged launches' wasted prefetch traffic costs 4 %)
-  if (CL == 8 && tid == 0) {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/CL): centroid
+  if (CL == 8 && A.spec_pf && tid == 0) {  // speculative L2 prefetch of what a retrieval reads (this rank's 1/CL): centroid
      // rows, sizes and the old selection / pool offsets — five bulk prefetches (TMA unit, no LSU
      // traffic). The trigger resolves in ~2 us; on an unflagged step the lines are simply not used.
     const int nu = s_S.n_units, mu = (nu + CL - 1) / CL;

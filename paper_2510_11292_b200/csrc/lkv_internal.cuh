@@ -198,6 +198,8 @@ struct LayerArgs {
   int early;    // 1: the previous kernel in the stream is another layer's layer kernel, so this layer's own
                 // state (written only by kernels that completed before that one passed its wait) may be
                 // read before griddepcontrol.wait — the prologue overlaps the previous layer
+  int spec_pf;  // speculative L2 prefetch of the retrieval operands (small unit tables only: the
+                // prefetch runs on every launch, flagged or not; C2 +1.2 %, C5's 33 MB per launch -1.4 %)
 };
 constexpr int PROF_SLOTS = 32;  // LKV_PROF: [64 layers][2048 CTAs][PROF_SLOTS] globaltimer stamps
 // the single launch selects on-chip for instances with at most LAYER_REP_UNITS live units (more: the
