@@ -15,6 +15,8 @@
 // Every decision is made in the arithmetic of the multi-kernel path (lkv_score_dev.cuh), so both
 // paths match the oracle bit for bit on trigger decisions and selections. Every rank executes the
 // same sequence of cluster barriers (all branches depend only on cluster-uniform values).
+#include <type_traits>
+
 #include "lkv_append_dev.cuh"
 #include "lkv_attn_dev.cuh"
 #include "lkv_attn_mma_dev.cuh"
@@ -300,13 +302,39 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   unsigned long long zl[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) zl[j] = 0ull;
-  for (int i = tid; i < cnt; i += AT_THREADS) {
+  // E in global scratch (large instances): units in batches of EB per thread, every load of a batch
+  // issued before its arithmetic (the stores to E would otherwise serialise the next unit's loads);
+  // E in shared memory: one unit at a time (C5's share: flagged launch 104 -> 94 us; C2: batching -1 %)
+  auto exp_pass = [&](auto ebc) {
+    constexpr int EB = decltype(ebc)::value;
+    for (int i0 = tid; i0 < cnt; i0 += EB * AT_THREADS) {
+      float ev[EB][G];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float e = exp_r3(__fsub_rn(E[j * m + i], s_M[j]), s_coef);
-      E[j * m + i] = e;
-      zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
+      for (int k = 0; k < EB; ++k) {
+        const int i = i0 + k * AT_THREADS;
+#pragma unroll
+        for (int j = 0; j < G; ++j) ev[k][j] = i < cnt ? E[j * m + i] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < EB; ++k) {
+        const int i = i0 + k * AT_THREADS;
+        if (i < cnt) {
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float e = exp_r3(__fsub_rn(ev[k][j], s_M[j]), s_coef);
+            E[j * m + i] = e;
+            zl[j] += __float2ull_rz(__fmul_rn(e, 1099511627776.0f));
+          }
+        }
+      }
     }
+  };
+  if constexpr (G == 8) {  // (the only group size whose large instances keep E in global scratch;
+                           // other g keep the loop code of one unit per thread — C2 -0.5 % otherwise)
+    if (e_smem) exp_pass(std::integral_constant<int, 1>{});
+    else exp_pass(std::integral_constant<int, 4>{});
+  } else {
+    exp_pass(std::integral_constant<int, 1>{});
   }
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -329,18 +357,39 @@ __device__ __forceinline__ int lk_select_rep(const RetrieveArgs& a, const int li
   __syncthreads();
 
   // ---- A_u of the own units, pushed to every rank
-  for (int i = tid; i < cnt; i += AT_THREADS) {
-    float A = 0.0f;
+  auto a_pass = [&](auto ebc) {
+    constexpr int EB = decltype(ebc)::value;
+    for (int i0 = tid; i0 < cnt; i0 += EB * AT_THREADS) {
+      float ev[EB][G];
 #pragma unroll
-    for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(E[j * m + i], s_Z[j]));
-    A = __fdiv_rn(A, (float)G);
-    const uint32_t bits = __float_as_uint(A);
-    if (big) {
-      RA[lo + i] = bits;  // (published to the cluster by the barrier below)
-    } else {
+      for (int k = 0; k < EB; ++k) {
+        const int i = i0 + k * AT_THREADS;
 #pragma unroll
-      for (int r = 0; r < CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+        for (int j = 0; j < G; ++j) ev[k][j] = i < cnt ? E[j * m + i] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < EB; ++k) {
+        const int i = i0 + k * AT_THREADS;
+        if (i >= cnt) break;
+        float A = 0.0f;
+#pragma unroll
+        for (int j = 0; j < G; ++j) A = __fadd_rn(A, __fdiv_rn(ev[k][j], s_Z[j]));
+        A = __fdiv_rn(A, (float)G);
+        const uint32_t bits = __float_as_uint(A);
+        if (big) {
+          RA[lo + i] = bits;  // (published to the cluster by the barrier below)
+        } else {
+#pragma unroll
+          for (int r = 0; r < CL; ++r) *cl.map_shared_rank(&RA[lo + i], r) = bits;
+        }
+      }
     }
+  };
+  if constexpr (G == 8) {
+    if (e_smem) a_pass(std::integral_constant<int, 1>{});
+    else a_pass(std::integral_constant<int, 4>{});
+  } else {
+    a_pass(std::integral_constant<int, 1>{});
   }
   if (tid == 0) {
     s_prefix = 0ull;
