@@ -18,7 +18,7 @@ per layer) is timed with the library's phase timer: k-means keys/s (Lloyd only) 
 GEMM's TFLOP/s, with the prompt offload reported separately.
 
 Multi-GPU (torchrun): --shard batch (weak scaling: every rank its own sequences, no collective) or
---shard heads (the default at N > 1 for C4: ranks own contiguous KV-head ranges of the same batch;
+--shard heads (the default at N > 1 for C4 and C5: ranks own contiguous KV-head ranges of the same batch;
 one NCCL all-gather of the per-head outputs per layer, or one per step with --gather step).
 ``--impl reference`` times the CPU oracle (the reference arm of this tier) on the box's host cores.
 """
@@ -66,7 +66,7 @@ def parse(argv=None):
                    help="multi-GPU partitioning: 'batch' = every rank its own sequences (weak scaling, no "
                         "collective); 'heads' = ranks own contiguous KV-head ranges of the same sequences and "
                         "all-gather the per-head attention outputs over NCCL (strong scaling); auto = heads for "
-                        "C4 at N > 1, else batch")
+                        "C4 and C5 at N > 1, else batch")
     p.add_argument("--gather", default="layer", choices=["layer", "step"],
                    help="heads mode: one all-gather per layer (model-faithful) or one batched per step")
     return p.parse_args(argv)
@@ -459,7 +459,7 @@ def main(argv=None):
     ret_layers = [l for l in range(L) if l not in full]
     K, W = args.steps, args.warmup
     T = 1 + W + K + 2
-    shard = args.shard if args.shard != "auto" else ("heads" if (world > 1 and cfg.name == "C4") else "batch")
+    shard = args.shard if args.shard != "auto" else ("heads" if (world > 1 and cfg.name in ("C4", "C5")) else "batch")
     heads = shard == "heads"
     seed = args.seed if heads else rank_seed(args.seed, rank)
     hb, hc = head_range(rank, world, Hkv) if heads else (0, Hkv)
