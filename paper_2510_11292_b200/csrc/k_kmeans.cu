@@ -15,8 +15,6 @@
 //     update  C_j = (sequential fp32 sum of member keys) / |j|, one warp per cluster
 //   offload   KV rows permuted cluster-major and written to the pinned host pool (zero-copy
 //             stores), unit table, sinks kept on the device.
-#include <algorithm>
-
 #include "lkv_internal.cuh"
 
 namespace lkv {
@@ -626,86 +624,47 @@ __device__ __forceinline__ void km_write_centroid(const KmArgs& a, int li, int j
   }
 }
 
-// Warps loop over the tasks of their instance (grid sized to the resident warps, not to the task
-// count): while a task's member rows are in flight, the next task's description and member positions
-// are loaded, so the per-task chain (description -> positions -> rows) is paid once per warp instead of
-// once per task (a one-task-per-warp grid ran ~7 short waves of three round trips each).
 __global__ void __launch_bounds__(128) km_update_kernel(KmArgs a) {
   pdl_wait_trigger();
   const int li = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = gridDim.x * 4;
+  const int t = blockIdx.x * 4 + warp;
   const int32_t* toff = a.toff + (int64_t)li * (a.kmax + 1);
-  const int ntk = toff[a.kc];
-  int t = blockIdx.x * 4 + warp;
-  if (t >= ntk) return;
+  if (t >= toff[a.kc]) return;
   // the task (written with the offsets): cluster j, members [m0, m1) of the cluster-sorted order,
-  // tasks of j; lane i holds member m0 + i's position (task-padded order: one load with the task)
-  const int4* tcl = a.tcl + (int64_t)li * a.task_max;
-  const int32_t* tperm = a.tperm + (int64_t)li * a.task_max * KM_TASK;
-  int4 tk = tcl[t];
-  int pi_raw = tperm[(int64_t)t * KM_TASK + lane];
-  while (true) {
-    const int j = tk.x, m0 = tk.y, m1 = tk.z, ntask = tk.w;
-    const int nm = m1 - m0;
-    const int pi = lane < nm ? pi_raw : 0;
-    const int tn = t + nw;
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
-    int4 tkn = make_int4(0, 0, 0, 0);
-    int pin_raw = 0;
+  // tasks of j; lane i holds member m0 + i's position, so all <= 32 member rows are loaded in two
+  // batches of 16 (three round trips in all), summed in member order (deterministic)
+  // (the task and its members' positions — task-padded order — load in the same round trip)
+  const int4 tk = a.tcl[(int64_t)li * a.task_max + t];
+  const int pi_raw = a.tperm[((int64_t)li * a.task_max + t) * KM_TASK + lane];
+  const int j = tk.x, m0 = tk.y, m1 = tk.z, ntask = tk.w;
+  const int nm = m1 - m0;
+  const int pi = lane < nm ? pi_raw : 0;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int rb = 0; rb < KM_TASK; rb += 16) {
-      if (rb >= nm) break;
-      uint2 u[16];
+  for (int rb = 0; rb < KM_TASK; rb += 16) {
+    if (rb >= nm) break;
+    uint2 u[16];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int idx = __shfl_sync(0xffffffffu, pi, rb + r);
-        if (rb + r < nm) u[r] = reinterpret_cast<const uint2*>(xrow(a, li, idx))[lane];
+    for (int r = 0; r < 16; ++r) {
+      const int idx = __shfl_sync(0xffffffffu, pi, rb + r);
+      if (rb + r < nm) u[r] = reinterpret_cast<const uint2*>(xrow(a, li, idx))[lane];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (rb + r < nm) {
+        s[0] = __fadd_rn(s[0], __uint_as_float(u[r].x << 16));
+        s[1] = __fadd_rn(s[1], __uint_as_float(u[r].x & 0xFFFF0000u));
+        s[2] = __fadd_rn(s[2], __uint_as_float(u[r].y << 16));
+        s[3] = __fadd_rn(s[3], __uint_as_float(u[r].y & 0xFFFF0000u));
       }
-      if (rb == 0 && tn < ntk) {  // the next task's description, in flight with these rows
-        tkn = tcl[tn];
-        pin_raw = tperm[(int64_t)tn * KM_TASK + lane];
-      }
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (rb + r < nm) {  // member order: deterministic fp32 sums
-          s[0] = __fadd_rn(s[0], __uint_as_float(u[r].x << 16));
-          s[1] = __fadd_rn(s[1], __uint_as_float(u[r].x & 0xFFFF0000u));
-          s[2] = __fadd_rn(s[2], __uint_as_float(u[r].y << 16));
-          s[3] = __fadd_rn(s[3], __uint_as_float(u[r].y & 0xFFFF0000u));
-        }
-    }
-    if (ntask == 1) {
-      km_write_centroid(a, li, j, s, nm, lane);
-    } else {
-      float4* P = reinterpret_cast<float4*>(a.upart + ((int64_t)li * a.task_max + t) * D);
-      P[lane] = make_float4(s[0], s[1], s[2], s[3]);
-    }
-    if (tn >= ntk) break;
-    if (nm == 0) {  // (no rows were issued: the next description was not loaded above)
-      tkn = tcl[tn];
-      pin_raw = tperm[(int64_t)tn * KM_TASK + lane];
-    }
-    t = tn;
-    tk = tkn;
-    pi_raw = pin_raw;
   }
-}
-
-// update grid: blocks per instance so that the instances' warps fill the resident capacity (the
-// occupancy calculator's CTAs per SM at the kernel's register count), never more than one task per warp
-static dim3 km_update_grid(const KmArgs& a, int ni) {
-  static int sms = 0, per_sm = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km_update_kernel, 128, 0) != cudaSuccess ||
-        per_sm <= 0)
-      per_sm = 4;
+  if (ntask == 1) {
+    km_write_centroid(a, li, j, s, nm, lane);
+  } else {
+    float4* P = reinterpret_cast<float4*>(a.upart + ((int64_t)li * a.task_max + t) * D);
+    P[lane] = make_float4(s[0], s[1], s[2], s[3]);
   }
-  const int per_inst = std::max(1, (sms * per_sm + ni - 1) / ni);
-  return dim3((unsigned)std::min((a.task_max + 3) / 4, per_inst), (unsigned)ni);
 }
 
 __global__ void __launch_bounds__(128) km_finalize_kernel(KmArgs a) {
@@ -892,7 +851,7 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
     // pages: fixed assignment, one centroid update (mean of each page's keys), no iterations
     launch_k(km_page_kernel, dim3(dim3(64, ni)), dim3(256), 0, st, a);
     if ((e = sort_by_cluster(a, ni, nchunk, false, st)) != cudaSuccess) return e;
-    launch_k(km_update_kernel, km_update_grid(a, ni), dim3(128), 0, st, a);
+    launch_k(km_update_kernel, dim3(dim3((a.task_max + 3) / 4, ni)), dim3(128), 0, st, a);
     launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
   } else {
     launch_k(km_init_kernel, dim3(gk), dim3(128), 0, st, a);
@@ -915,7 +874,7 @@ cudaError_t run_kmeans_prompt(const KmArgs& a, cudaStream_t st, uint64_t* tc_ite
       if (a.rec) a.rec->mark(st, PH_SORT);
       if ((e = sort_by_cluster(a, ni, nchunk, true, st)) != cudaSuccess) return e;
       if (a.rec) a.rec->mark(st, PH_UPDATE);
-      launch_k(km_update_kernel, km_update_grid(a, ni), dim3(128), 0, st, a);
+      launch_k(km_update_kernel, dim3(dim3((a.task_max + 3) / 4, ni)), dim3(128), 0, st, a);
       launch_k(km_finalize_kernel, dim3(gk), dim3(128), 0, st, a);
     }
   }
