@@ -864,3 +864,21 @@ def test_fp8_pool_c4_params_gpu_kmeans():
     assert m1["host_pool_bytes"] * 2 == m0["host_pool_bytes"]
     err = max(np.abs(a - b).max() for a, b in zip(o0, o1))
     assert 0 < err < 0.1, err
+
+
+@pytest.mark.timeout(1800)
+def test_variants_combined_at_capacity():
+    """The config variants together at the long-output capacities, every step against the oracle:
+    C3's parameters (1K prompt, 32K-token capacity, evicted segments become units) with the E4M3 pool
+    and the host-resident index through the single launch; the same with BATCHED_DMA (bf16 pool, the
+    per-call sequence) and the host-resident index."""
+    lkv = _lkv()
+    cfg = C3.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, decode_steps=120,
+                     max_output_len=32768)
+    inp = make_inputs(cfg, 120, 28)
+    _, n_flags, st = run_episode(cfg, inp, 120, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer",
+                                 pool_fp8=True, index_offload=1)
+    assert st["segments_evicted"] > 0 and st["units_fetched"] > 0 and n_flags > 3
+    _, n_flags, st = run_episode(cfg, inp, 120, lambda l, Kn: oracle_assign(cfg, Kn), fused=False,
+                                 fetch_mode=lkv.FETCH_BATCHED_DMA, index_offload=1)
+    assert st["segments_evicted"] > 0 and st["units_fetched"] > 0
