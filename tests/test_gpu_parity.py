@@ -873,12 +873,12 @@ def test_variants_combined_at_capacity():
     and the host-resident index through the single launch; the same with BATCHED_DMA (bf16 pool, the
     per-call sequence) and the host-resident index."""
     lkv = _lkv()
-    cfg = C3.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, decode_steps=120,
-                     max_output_len=32768)
-    inp = make_inputs(cfg, 120, 28)
-    _, n_flags, st = run_episode(cfg, inp, 120, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer",
+    cfg = C3.replace(num_layers=2, full_cache_layers=(0,), num_q_heads=8, num_kv_heads=2, decode_steps=200,
+                     max_output_len=32768)  # (W = 128: segments start to be evicted after ~130 steps)
+    inp = make_inputs(cfg, 200, 28)
+    _, n_flags, st = run_episode(cfg, inp, 200, lambda l, Kn: oracle_assign(cfg, Kn), fused="layer",
                                  pool_fp8=True, index_offload=1)
     assert st["segments_evicted"] > 0 and st["units_fetched"] > 0 and n_flags > 3
-    _, n_flags, st = run_episode(cfg, inp, 120, lambda l, Kn: oracle_assign(cfg, Kn), fused=False,
+    _, n_flags, st = run_episode(cfg, inp, 200, lambda l, Kn: oracle_assign(cfg, Kn), fused=False,
                                  fetch_mode=lkv.FETCH_BATCHED_DMA, index_offload=1)
     assert st["segments_evicted"] > 0 and st["units_fetched"] > 0
