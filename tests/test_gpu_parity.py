@@ -283,17 +283,19 @@ def test_duplicate_centroids_ties_to_lower_id():
     run_episode(cfg, inp, 6, lambda l, Kn_: a, fused="layer")
 
 
-@pytest.mark.parametrize("prompt_len", [12000 + 16, 16600 + 16])
-def test_decode_layer_many_units(prompt_len):
-    """Single-size units (c=1): ~12K units keep 6 units per thread per rank in shared memory; ~16.6K
-    units exceed the on-chip capacity (16384) and run the global-scratch variant of the select."""
+@pytest.mark.parametrize("prompt_len,variant", [(12000 + 16, {}), (16600 + 16, {}),
+                                                (16600 + 16, {"pool_fp8": True, "index_offload": 1})])
+def test_decode_layer_many_units(prompt_len, variant):
+    """Single-size units (c=1): ~12K and ~16.6K live units (more than 8192) run the select with its
+    per-unit arrays in global scratch ("big" mode), (r2) also with the E4M3 pool and the host index."""
     cfg = small_cfg(num_layers=1, full_cache_layers=(), decode_steps=8, batch=1, num_kv_heads=1, num_q_heads=4,
                     prompt_len=prompt_len, avg_cluster_size=1, budget_tokens=300, tau=0.95)
     inp = make_inputs(cfg, 8, 10)
     N = prompt_len - cfg.sink_tokens
     a = np.arange(N, dtype=np.int32)[None, None, :]
     for fused in (False, "layer"):
-        _, n_flags, st = run_episode(cfg, inp, 8, lambda l, Kn: a, fused=fused, compare_ws=(fused == "layer"))
+        _, n_flags, st = run_episode(cfg, inp, 8, lambda l, Kn: a, fused=fused, compare_ws=(fused == "layer"),
+                                     **variant)
         assert st["units_scored"] >= N and n_flags >= 2
 
 
