@@ -322,7 +322,13 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
 #ifndef FA_SPLIT_CTAS
 #define FA_SPLIT_CTAS 296
 #endif
+#ifndef LKV_FA_SPLIT_CEIL
+  // (floor: never more CTAs than one wave of 2 per SM — the ceiling put C4's 64 instances x 5 splits =
+  // 320 CTAs on 296 slots, a 24-CTA second wave; C5's share 16 x 19 = 304)
+  const int64_t want = std::max<int64_t>(1, FA_SPLIT_CTAS / n_ctas);
+#else
   const int64_t want = (FA_SPLIT_CTAS + n_ctas - 1) / n_ctas;
+#endif
   const int64_t chunks = (max_rows + 63) / 64;
   int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
   if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));
