@@ -69,6 +69,7 @@ struct louiskv_ctx {
   int dma_cap = 0;
   uint64_t dma_copies = 0;  // copies issued (louiskv_stats.dma_copies)
   int prb = POOL_ROW_BYTES;  // host-pool bytes per token (K + V): 512 bf16, 256 E4M3
+  int sms = 148;             // SMs of the context's device (split-K grid sizing)
   float* d_part = nullptr;
   int* d_counters = nullptr;
   int max_splits = 64;
@@ -317,18 +318,18 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
     a.ring_cap = c->ring_cap;
     max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
   }
-  // split-K: ~2 CTAs per SM when the rows allow it; a split never ends with a tiny tail chunk
-  // (rows per split rounded to whole 64-row pipeline chunks)
-#ifndef FA_SPLIT_CTAS
-#define FA_SPLIT_CTAS 296
-#endif
-#ifndef LKV_FA_SPLIT_CEIL
-  // (floor: never more CTAs than one wave of 2 per SM — the ceiling put C4's 64 instances x 5 splits =
-  // 320 CTAs on 296 slots, a 24-CTA second wave; C5's share 16 x 19 = 304)
-  const int64_t want = std::max<int64_t>(1, FA_SPLIT_CTAS / n_ctas);
+  // split-K: one CTA per SM when the rows allow it (splits per instance = floor(SMs / instances), so
+  // the grid never spills into a partial second wave); a split never ends with a tiny tail chunk (rows
+  // per split rounded to whole 64-row pipeline chunks). Measured on the full-cache layers against 2
+  // CTAs per SM (floor(296 / instances)): C2 33.5 -> 29.7 us (half the split partials to merge), C5's
+  // share 167.6 -> 163.6 us, C4 equal (320 us); the ceiling of 296 / instances had left C4 a 24-CTA
+  // second wave (413 us).
+#ifdef FA_SPLIT_CTAS
+  const int64_t slots = FA_SPLIT_CTAS;  // (experiments)
 #else
-  const int64_t want = (FA_SPLIT_CTAS + n_ctas - 1) / n_ctas;
+  const int64_t slots = c->sms;
 #endif
+  const int64_t want = std::max<int64_t>(1, slots / n_ctas);
   const int64_t chunks = (max_rows + 63) / 64;
   int splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, chunks));
   if (chunks > splits) splits = (int)((chunks + (chunks + splits - 1) / splits - 1) / ((chunks + splits - 1) / splits));
@@ -438,6 +439,8 @@ louiskv_status louiskv_create(const louiskv_config* cfg, louiskv_ctx** out) {
 
   louiskv_ctx* c = new louiskv_ctx();
   c->cfg = k;
+  if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, k.device) != cudaSuccess || c->sms <= 0)
+    c->sms = 148;
   c->L = k.num_layers;
   c->Hq = k.num_q_heads;
   c->Hkv = k.num_kv_heads;

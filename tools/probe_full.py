@@ -12,19 +12,24 @@ from synth.configs import CONFIGS
 
 impl = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-cfg = CONFIGS["C2"]
+cfg = CONFIGS[os.environ.get("LKV_PROBE_CFG", "C2")]  # (env: another config, batch, owned KV heads)
+if os.environ.get("LKV_PROBE_BATCH"):
+    cfg = cfg.replace(batch=int(os.environ["LKV_PROBE_BATCH"]))
+hc = int(os.environ.get("LKV_PROBE_HEADS", cfg.num_kv_heads))
 if len(sys.argv) > 3:
     cfg = cfg.replace(prompt_len=int(sys.argv[3]))
 dev = torch.device("cuda", 0)
-ctx = lkv.Context(lkv.make_config(cfg, max_output_len=2 * reps + 64, attn_impl=impl))
+ctx = lkv.Context(lkv.make_config(cfg, max_output_len=2 * reps + 64, attn_impl=impl, kv_head_count=hc))
 layers = sorted(cfg.full_cache_layers)
 plants = {l: synth.planted(cfg, l, 0, dev) for l in layers}
 for l in layers:
-    ctx.cluster_prompt(l, *synth.prompt_kv(cfg, l, 0, dev, plants[l]))
+    Kp, Vp = synth.prompt_kv(cfg, l, 0, dev, plants[l])
+    ctx.cluster_prompt(l, Kp[:, :, :hc], Vp[:, :, :hc])
+    del Kp, Vp
 torch.cuda.synchronize()
 q = torch.randn((cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.head_dim), device=dev).bfloat16()
-k = torch.randn((cfg.num_layers, cfg.batch, cfg.num_kv_heads, cfg.head_dim), device=dev).bfloat16()
-out = torch.empty_like(q)
+k = torch.randn((cfg.num_layers, cfg.batch, hc, cfg.head_dim), device=dev).bfloat16()
+out = torch.empty((cfg.num_layers, cfg.batch, cfg.group * hc, cfg.head_dim), device=dev).bfloat16()
 for l in layers:
     ctx.decode_layer(l, q[l], k[l], k[l], out[l])
 torch.cuda.synchronize()
@@ -52,7 +57,7 @@ b.record()
 torch.cuda.synchronize()
 b2b = a.elapsed_time(b) / (reps // 2) / len(layers)
 rows = cfg.prompt_len + reps
-byts = cfg.batch * cfg.num_kv_heads * rows * 512
+byts = cfg.batch * hc * rows * 512
 med = ts[len(ts) // 2]
 print(json.dumps({"P": cfg.prompt_len, "impl": impl, "tma": bool(os.environ.get("LOUISKV_FA_TMA")), "us_per_layer_median": med * 1e3,
                   "us_min": ts[0] * 1e3, "us_back_to_back": b2b * 1e3, "GBps_b2b": byts / (b2b / 1e3) / 1e9, "GBps": byts / (med / 1e3) / 1e9, "bytes": byts}))
