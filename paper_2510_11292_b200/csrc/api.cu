@@ -318,16 +318,16 @@ AttnArgs attn_args(louiskv_ctx* c, int layer, const void* q_own, int64_t stride_
     a.ring_cap = c->ring_cap;
     max_rows = std::min<int64_t>(c->S, c->P[layer]) + c->Bud + c->ring_cap;
   }
-  // split-K: one CTA per SM when the rows allow it (splits per instance = floor(SMs / instances), so
-  // the grid never spills into a partial second wave); a split never ends with a tiny tail chunk (rows
-  // per split rounded to whole 64-row pipeline chunks). Measured on the full-cache layers against 2
-  // CTAs per SM (floor(296 / instances)): C2 33.5 -> 29.7 us (half the split partials to merge), C5's
-  // share 167.6 -> 163.6 us, C4 equal (320 us); the ceiling of 296 / instances had left C4 a 24-CTA
-  // second wave (413 us).
+  // split-K grid: splits per instance = floor(slots / instances), so the grid never spills into a
+  // partial second wave (the ceiling of 296 / instances had left C4 a 24-CTA second wave: 413 us per
+  // full-cache layer); slots = one CTA per SM for few instances (at most SMs / 4: fewer split partials
+  // to merge — C2 33.5 -> 29.7 us, C5's share 167.6 -> 163.6 us), two per SM otherwise (C4: 318 us vs
+  // 326 at one per SM). A split never ends with a tiny tail chunk (rows per split rounded to whole
+  // 64-row pipeline chunks).
 #ifdef FA_SPLIT_CTAS
   const int64_t slots = FA_SPLIT_CTAS;  // (experiments)
 #else
-  const int64_t slots = c->sms;
+  const int64_t slots = (int64_t)n_ctas * 4 <= c->sms ? c->sms : 2 * (int64_t)c->sms;
 #endif
   const int64_t want = std::max<int64_t>(1, slots / n_ctas);
   const int64_t chunks = (max_rows + 63) / 64;
