@@ -225,14 +225,16 @@ louiskv_status louiskv_append_attn(louiskv_ctx* ctx, int32_t layer, const void* 
 /* One whole decode step of one layer (Algorithm 1: trigger, retrieve when flagged,
  * store_cache, attention), identical in results to should_retrieve -> retrieve ->
  * append_output -> sparse_attn with q_own = q_all + kv_head_begin*g*d (same stride). On a
- * retrieval layer it is ONE clustered launch (8 CTAs per (b, owned head)): every rank recomputes
- * r_t (recipe R1), the flagged instances score with their units split over the 8 ranks and every
+ * retrieval layer it is ONE clustered launch of CL CTAs per (b, owned head) — CL = 8 when every
+ * instance's cluster fits one wave of one CTA per SM, else 4 while two waves suffice, else 2 (env
+ * LOUISKV_LAYER_CL overrides): every rank recomputes r_t (recipe R1), the flagged instances score
+ * with their units split over the CL ranks and every
  * rank runs the budgeted selection on the replicated scores (exchanged through distributed shared
  * memory; instances with more than 8192 LIVE units keep the per-unit select arrays in global
  * scratch instead — same launch, decided on the device per step), the ranks gather the new working
  * set, the last rank appends, all ranks attend one split each. A full-cache layer is one launch
  * too (dense attention with the store_cache fused). Budgets with min(B, unit capacity) > 1024
- * issue the multi-kernel sequence instead. Arguments: q_all
+ * issue the multi-kernel sequence instead, and so does fetch_mode BATCHED_DMA. Arguments: q_all
  * as in should_retrieve (stride_q), k_t/v_t as in append_output (stride_kv), out/out_f32 as in
  * sparse_attn, d_flag_out/d_r_out optional device outputs as in should_retrieve.
  * Errors: INVALID_ARG, STATE (as should_retrieve), CUDA. */
